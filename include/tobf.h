@@ -1,0 +1,187 @@
+/*
+ * tobf.h — C ABI of libtobf.so, the sm_100a engine behind the
+ * paper_2107_09789_b200 drop-in for traceobf's candidate-evaluation path
+ * (NeurObfuscator, arXiv 2107.09789).
+ *
+ * Every entry point is extern "C", takes plain pointers / sizes, never throws,
+ * and returns 0 on success or a negative TOBF_E* code; tobf_last_error()
+ * returns a thread-local message for the most recent failure. Device pointers
+ * are caller-owned; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream). All launches are asynchronous on `stream`.
+ *
+ * Reference interfaces each group replaces (paths relative to the reference
+ * package pkg/src/traceobf/):
+ *   executor     interpreter.py:22-30 conv2d, :33-35 maxpool, :38-41 softmax,
+ *                :44-72 _eval_node, :75-90 execute
+ *   verdict      interpreter.py:93-118 equivalence_check (compare + reduce)
+ *   trace        fusion.py:159-180 default_schedule, :141-156 candidate_triples,
+ *                costmodel.py:166-232 profile_kernel, :96-98 Trace.total_latency
+ *   fitness      SPEC.md:471-486 levenshtein/ler, PAPER.md:425,432 LSTM+CTC,
+ *                PAPER.md:487 / SPEC.md:563-571 Eq. 10 fitness (no reference code)
+ */
+#ifndef TOBF_H_
+#define TOBF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOBF_OK 0
+#define TOBF_E_INVALID -1
+#define TOBF_E_CUDA -2
+#define TOBF_E_FAULT -3 /* device-side protocol timeout (see tobf_check_fault) */
+
+/* ------------------------------------------------------------------ executor */
+
+/* Epilogue step applied to each conv output element, in order. */
+#define TOBF_EPI_NONE 0
+#define TOBF_EPI_AFFINE 1     /* v = v*ptr[c] + ptr[ldc + c]   (folded BatchNorm); aux = ldc */
+#define TOBF_EPI_RELU 2       /* v = max(v, 0) */
+#define TOBF_EPI_ADD_TENSOR 3 /* v += ptr[pixel*aux + c]       (residual / branch sum); aux = channel stride */
+#define TOBF_EPI_ADD_CONST 4  /* v += ptr[((n % aux)*HoWo + p)*Cpo + c] (dummy-add constant); aux = batch period */
+#define TOBF_MAX_EPI 6
+
+typedef struct tobf_epi_step {
+  int32_t op;
+  int32_t aux;
+  const float* ptr;
+} tobf_epi_step;
+
+/* One implicit-GEMM convolution problem (a Conv2D, or a Linear expressed as a
+ * full-extent convolution). Activations are NHWC float32 with the channel
+ * count padded to a multiple of 4 (pad channels hold zeros). GEMM view:
+ * M = batch*Ho*Wo output pixels, N = j output channels, K = k1*k2*Cp. */
+typedef struct tobf_conv_desc {
+  const float* x;    /* input view, first channel of the view */
+  const float* wimg; /* packed weight image from tobf_pack_weights */
+  float* y;          /* output view, first channel of the view */
+  int32_t batch, H, W, Cp;   /* input geometry; Cp = padded channels of the view */
+  int32_t Ho, Wo, Cpo, j;    /* output geometry; Cpo = roundup(j,4) channels written */
+  int32_t k1, k2, stride, pad;
+  int32_t K, kblocks, mtiles, ntiles; /* filled by tobf_conv_prepare */
+  int32_t tile_start, nepi, ldx, ldy; /* ldx/ldy = channel stride of the x/y buffers */
+  tobf_epi_step epi[TOBF_MAX_EPI];
+} tobf_conv_desc;
+
+/* Fill K/kblocks/mtiles/ntiles/tile_start for a group of descriptors (host
+ * memory) for the given N tile width (64 or 128); returns total tile count. */
+int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles);
+
+/* Bytes of the packed weight image for a conv with the given geometry. */
+int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n);
+
+/* Pack a float32 weight tensor into the tile-major, tf32 hi/lo split,
+ * 128B-swizzled operand image the conv kernel streams with bulk copies.
+ * Weight element (u,v,c,n) is read at w[u*su + v*sv + c*sc + n*sn] for
+ * c < c_real (zero for c_real <= c < Cp). HWIO conv weights (k1,k2,c,j):
+ * su=k2*c*j, sv=c*j, sc=j, sn=1. */
+int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
+                      int64_t su, int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg,
+                      void* stream);
+
+/* Grouped 3xTF32 tcgen05 implicit-GEMM convolution over `n` problems whose
+ * descriptors live in DEVICE memory (prepared with tobf_conv_prepare). */
+int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, void* stream);
+
+/* Generic fused element-wise / pooling / copy ops (one op per descriptor). */
+#define TOBF_OP_MAXPOOL 1  /* y = maxpool(x, window=a0, stride=a1) */
+#define TOBF_OP_EPI 2      /* y = epilogue-chain(x) (standalone BN / ReLU / Add) */
+#define TOBF_OP_COPYCH 3   /* y[..., a0:a0+C] = x[..., a1:a1+C] channel copy (Concat / Slice) */
+#define TOBF_OP_SOFTMAX 4  /* y = softmax over channels (spatial 1x1 or per pixel) */
+
+typedef struct tobf_ew_desc {
+  const float* x;
+  float* y;
+  int32_t op, batch, H, W;   /* input geometry */
+  int32_t C, ldx, Ho, Wo;    /* C = channels processed; ldx = input channel stride */
+  int32_t ldy, a0, a1, nepi; /* ldy = output channel stride */
+  int64_t work_start;        /* prefix of work items (filled by tobf_ew_prepare) */
+  int32_t Cpo, pad_;         /* output channels to write (zero-fill C..Cpo) */
+  tobf_epi_step epi[TOBF_MAX_EPI];
+} tobf_ew_desc;
+
+int tobf_ew_prepare(tobf_ew_desc* descs, int n, int64_t* total_work);
+int tobf_ew_grouped(const tobf_ew_desc* d_descs, int n, int64_t total_work, void* stream);
+
+/* Equivalence verdict pieces (interpreter.py:114-117), bit-exact fp32:
+ * for each pair p: worst[p] = max |a-b|/(1+|b|), ok[p] = all(|a-b| <= tol*(1+|b|)).
+ * a/b are NHWC-padded buffers of `pairs` outputs each `count` pixels x C channels
+ * (ld = channel stride); `b_list[p]`, `a_list[p]` are device pointer arrays. */
+int tobf_equiv_compare(const float* const* a_list, const float* const* b_list, int pairs, int64_t pixels,
+                       int32_t C, int32_t ld, float tol, float* worst, int32_t* ok, void* stream);
+
+/* NHWC(padded) -> NCHW (dense) output unpacking. */
+int tobf_nhwc_to_nchw(const float* x, float* y, int32_t batch, int32_t C, int32_t H, int32_t W, int32_t ld,
+                      void* stream);
+/* NCHW (dense) -> NHWC(padded) input packing, pad channels zeroed. */
+int tobf_nchw_to_nhwc(const float* x, float* y, int32_t batch, int32_t C, int32_t H, int32_t W, int32_t ld,
+                      void* stream);
+
+/* ------------------------------------------------------------------ trace */
+
+/* One kernel of a compiled graph, reduced to the exact integers the cost
+ * model reads (costmodel.py:166-232). */
+typedef struct tobf_kern_desc {
+  int64_t work, fused_work, fused_bytes;
+  int64_t in_bytes, w_bytes, out_bytes;
+  int32_t tiled;        /* anchor is Conv2D or MaxPool */
+  int32_t is_conv;      /* Conv2D (else MaxPool) when tiled */
+  int32_t c, k1, k2, s; /* conv: c,k1,k2,stride; pool: c=channels, k1=k2=window, s=stride */
+  int32_t H, W, channel_like;  /* out height/width; attrs j (or channels) */
+  int32_t reuse_x_stream;      /* non-tiled: Linear j else 1 */
+  int32_t ty[3], tx[3];        /* schedule factor triples (input for profile, output of search) */
+  int32_t unroll, label;       /* label: OperatorKind code or -1 */
+  int32_t has_shape, pad_;     /* has_shape = 0 -> degenerate zero step */
+} tobf_kern_desc;
+
+typedef struct tobf_device_profile {
+  int64_t macs_per_cycle, launch_overhead, l1_bytes, l2_bytes, sm_count;
+} tobf_device_profile;
+
+/* Brute-force default_schedule for `n` kernels (DEVICE descriptor array):
+ * writes the lexicographic-argmin (ty, tx) into d_descs[i].ty/tx. */
+int tobf_schedule_search(tobf_kern_desc* d_descs, int n, const tobf_device_profile* prof, void* stream);
+
+/* profile_kernel for every kernel: feats[i*9 + f] in FEATURE_NAMES order
+ * (cycles, dram_read, dram_write, l1_tx, l1_util, l1_hit, l2_tx, l2_util, l2_hit). */
+int tobf_profile_kernels(const tobf_kern_desc* d_descs, int n, const tobf_device_profile* prof, double* feats,
+                         void* stream);
+
+/* Per-candidate CPython-3.12 (Neumaier) sum of cycles: candidate c owns
+ * kernels [offsets[c], offsets[c+1]). */
+int tobf_trace_totals(const double* feats, const int32_t* offsets, int ncand, double* totals, void* stream);
+
+/* ------------------------------------------------------------------ fitness */
+
+/* Batched single-layer LSTM + linear head + greedy CTC decode.
+ * x: [B][T_max][F] fp32 (already normalised), lens[B]; weights packed as
+ * w_ih[4H][F], w_hh[4H][H], b[4H], w_out[NC][H], b_out[NC] (gate order i,f,g,o).
+ * tokens: [B][T_max] int8 decoded labels (collapse + drop blank 0), ntok[B]. */
+int tobf_lstm_ctc(const float* x, const int32_t* lens, int32_t B, int32_t T_max, int32_t F, int32_t H,
+                  int32_t NC, const float* w_ih, const float* w_hh, const float* b, const float* w_out,
+                  const float* b_out, int8_t* tokens, int32_t* ntok, void* stream);
+
+/* Unit-cost Levenshtein distance, one warp per pair, against a single truth.
+ * pred: [B][T_max] int8 with lengths ntok; truth[tlen]. ed[B], ler[B] = ed/tlen. */
+int tobf_levenshtein(const int8_t* pred, const int32_t* ntok, int32_t B, int32_t T_max, const int8_t* truth,
+                     int32_t tlen, int32_t* ed, double* ler, void* stream);
+
+/* Eq. 10 reward per candidate: R = mean_i(ler[i*ncand + c]) / (eps + ((T-(1+budget)T*)/T*)^2),
+ * 0 where feasible[c] == 0. */
+int tobf_fitness_eq10(const double* ler, int32_t npred, int32_t ncand, const double* T, const int32_t* feasible,
+                      double Tstar, double budget, double eps, double* R, double* mean_ler, void* stream);
+
+/* ------------------------------------------------------------------ misc */
+const char* tobf_last_error(void);
+int tobf_version(void);
+/* Reads and clears the device fault word; returns TOBF_E_FAULT if a bounded
+ * wait timed out since the last check. */
+int tobf_check_fault(void* stream);
+int tobf_device_sync(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOBF_H_ */
