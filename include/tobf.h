@@ -155,13 +155,16 @@ int tobf_trace_totals(const double* feats, const int32_t* offsets, int ncand, do
 
 /* ------------------------------------------------------------------ fitness */
 
-/* Batched single-layer LSTM + linear head + greedy CTC decode.
- * x: [B][T_max][F] fp32 (already normalised), lens[B]; weights packed as
- * w_ih[4H][F], w_hh[4H][H], b[4H], w_out[NC][H], b_out[NC] (gate order i,f,g,o).
- * tokens: [B][T_max] int8 decoded labels (collapse + drop blank 0), ntok[B]. */
-int tobf_lstm_ctc(const float* x, const int32_t* lens, int32_t B, int32_t T_max, int32_t F, int32_t H,
-                  int32_t NC, const float* w_ih, const float* w_hh, const float* b, const float* w_out,
-                  const float* b_out, int8_t* tokens, int32_t* ntok, void* stream);
+/* Batched single-layer LSTM sequence predictor + linear head + greedy CTC.
+ * Trace b owns feature rows [offsets[b], offsets[b+1]) of `feats` (fp64,
+ * 9 columns in FEATURE_NAMES order, as written by tobf_profile_kernels); the
+ * first F columns are normalised x = (float)log1p(v) on the fly.
+ * Weights (fp32, gate order i,f,g,o): w_ihT [F][4H], w_hhT [H][4H], b [4H],
+ * w_out [NC][H], b_out [NC]. Output: tokens [B][T_max] int8 decoded labels
+ * (argmax, collapse repeats, drop blank 0), ntok[B]. T_max >= longest trace. */
+int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H, int32_t NC,
+                  const float* w_ihT, const float* w_hhT, const float* b, const float* w_out, const float* b_out,
+                  int8_t* tokens, int32_t T_max, int32_t* ntok, void* stream);
 
 /* Unit-cost Levenshtein distance, one warp per pair, against a single truth.
  * pred: [B][T_max] int8 with lengths ntok; truth[tlen]. ed[B], ler[B] = ed/tlen. */

@@ -96,7 +96,7 @@ SIGNATURES = {
     "tobf_schedule_search": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "tobf_profile_kernels": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
     "tobf_trace_totals": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
-    "tobf_lstm_ctc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "tobf_lstm_ctc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "tobf_levenshtein": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
     "tobf_fitness_eq10": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _f64, _f64, _f64, _vp, _vp, _vp]),
     "tobf_last_error": (C.c_char_p, []),

@@ -1,0 +1,267 @@
+// Memory-bound executor ops, grouped: one launch runs any mix of MaxPool,
+// standalone injective chains, channel copies and SoftMax over many
+// candidates. Work items are float4 channel groups (coalesced, vectorised)
+// except for unaligned channel copies; descriptors are located by binary
+// search over their work-item prefix.
+//
+// Replaces interpreter.py:33-35 (maxpool), :38-41 (softmax), :52-69
+// (ReLU / BatchNorm / Add / Concat / Slice of _eval_node), :114-117 (the
+// equivalence compare + max-reduce), and the NCHW<->NHWC staging of
+// execute()'s input/output (interpreter.py:75-90).
+#include <cmath>
+#include "tobf_internal.h"
+
+namespace tobf {
+
+__device__ __forceinline__ float ew_epi(float v, const tobf_ew_desc& d, int64_t pix, int c, int64_t cbase) {
+  for (int s = 0; s < d.nepi; ++s) {
+    const tobf_epi_step st = d.epi[s];
+    switch (st.op) {
+      case TOBF_EPI_AFFINE:
+        v = v * __ldg(st.ptr + c) + __ldg(st.ptr + st.aux + c);
+        break;
+      case TOBF_EPI_RELU:
+        v = fmaxf(v, 0.0f);
+        break;
+      case TOBF_EPI_ADD_TENSOR:
+        v = v + __ldg(st.ptr + pix * st.aux + c);
+        break;
+      case TOBF_EPI_ADD_CONST:
+        v = v + __ldg(st.ptr + cbase + c);
+        break;
+      default:
+        break;
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ int find_desc(const tobf_ew_desc* __restrict__ descs, int n, int64_t w) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (descs[mid].work_start <= w) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Work items: MAXPOOL / EPI -> one float4 channel group of one output pixel;
+// COPYCH -> one channel of one pixel (a0/a1 need not be 4-aligned);
+// SOFTMAX -> one warp per pixel (work counted in warps * 32 lanes).
+__global__ void ew_grouped_kernel(const tobf_ew_desc* __restrict__ descs, int n, int64_t total) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total; w += stride) {
+    const int di = find_desc(descs, n, w);
+    const tobf_ew_desc& d = descs[di];
+    const int64_t local = w - d.work_start;
+    switch (d.op) {
+      case TOBF_OP_MAXPOOL: {
+        const int groups = d.Cpo >> 2;
+        const int64_t pix = local / groups;
+        const int g = (int)(local - pix * groups);
+        const int64_t hw = (int64_t)d.Ho * d.Wo;
+        const int n_img = (int)(pix / hw);
+        const int rem = (int)(pix - (int64_t)n_img * hw);
+        const int yo = rem / d.Wo, xo = rem - (rem / d.Wo) * d.Wo;
+        const int win = d.a0, st = d.a1;
+        const float* base = d.x + ((int64_t)n_img * d.H * d.W) * d.ldx + g * 4;
+        float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        for (int u = 0; u < win; ++u) {
+          const float* row = base + ((int64_t)(yo * st + u) * d.W) * d.ldx;
+          for (int v = 0; v < win; ++v) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(row + (int64_t)(xo * st + v) * d.ldx));
+            m.x = fmaxf(m.x, q.x); m.y = fmaxf(m.y, q.y); m.z = fmaxf(m.z, q.z); m.w = fmaxf(m.w, q.w);
+          }
+        }
+        *reinterpret_cast<float4*>(d.y + pix * d.ldy + g * 4) = m;
+        break;
+      }
+      case TOBF_OP_EPI: {
+        const int groups = d.Cpo >> 2;
+        const int64_t pix = local / groups;
+        const int g = (int)(local - pix * groups);
+        const float4 q = __ldg(reinterpret_cast<const float4*>(d.x + pix * d.ldx + g * 4));
+        const int64_t hw = (int64_t)d.H * d.W;
+        int period = 1;
+        for (int s = 0; s < d.nepi; ++s)
+          if (d.epi[s].op == TOBF_EPI_ADD_CONST) period = d.epi[s].aux;
+        const int64_t n_img = pix / hw;
+        const int64_t cbase = ((n_img % period) * hw + (pix - n_img * hw)) * d.Cpo;
+        const int c = g * 4;
+        float o[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = (c + e < d.C) ? ew_epi(o[e], d, pix, c + e, cbase) : 0.0f;
+        *reinterpret_cast<float4*>(d.y + pix * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
+        break;
+      }
+      case TOBF_OP_COPYCH: {
+        // channels [0, C) copied; channels [a0+C, Cpo) of the output zero-filled
+        const int span = d.Cpo - d.a0;  // >= C
+        const int64_t pix = local / span;
+        const int c = (int)(local - pix * span);
+        const float v = c < d.C ? __ldg(d.x + pix * d.ldx + d.a1 + c) : 0.0f;
+        d.y[pix * d.ldy + d.a0 + c] = v;
+        break;
+      }
+      case TOBF_OP_SOFTMAX: {
+        const int64_t pix = local >> 5;
+        const int lane = (int)(local & 31);
+        const float* xr = d.x + pix * d.ldx;
+        float mx = -INFINITY;
+        for (int c = lane; c < d.C; c += 32) mx = fmaxf(mx, xr[c]);
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.0f;
+        for (int c = lane; c < d.C; c += 32) sum += expf(xr[c] - mx);
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        float* yr = d.y + pix * d.ldy;
+        for (int c = lane; c < d.Cpo; c += 32) yr[c] = c < d.C ? expf(xr[c] - mx) / sum : 0.0f;
+        break;
+      }
+      default:
+        break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- verdict
+__global__ void equiv_kernel(const float* const* __restrict__ a_list, const float* const* __restrict__ b_list,
+                             int64_t pixels, int C, int ld, float tol, float* __restrict__ worst,
+                             int32_t* __restrict__ ok) {
+  const int p = blockIdx.y;
+  const float* a = a_list[p];
+  const float* b = b_list[p];
+  float wmax = 0.0f;
+  int good = 1;
+  const int64_t total = pixels * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = i / C;
+    const int c = (int)(i - pix * C);
+    const float av = a[pix * ld + c], bv = b[pix * ld + c];
+    const float diff = fabsf(av - bv);        // np.abs(a - b)            (float32)
+    const float den = 1.0f + fabsf(bv);       // 1.0 + np.abs(b)          (float32)
+    const float rel = diff / den;             // IEEE division            (float32)
+    wmax = fmaxf(wmax, rel);
+    if (!(diff <= tol * den)) good = 0;       // |a-b| <= tol*(1+|b|)      (float32)
+  }
+  for (int o = 16; o; o >>= 1) {
+    wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    good &= __shfl_xor_sync(0xffffffffu, good, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(reinterpret_cast<int*>(worst + p), __float_as_int(wmax));  // non-negative floats order as ints
+    if (!good) atomicAnd(ok + p, 0);
+  }
+}
+
+__global__ void init_verdict_kernel(float* worst, int32_t* ok, int pairs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < pairs) {
+    worst[i] = 0.0f;
+    ok[i] = 1;
+  }
+}
+
+__global__ void nhwc_to_nchw_kernel(const float* __restrict__ x, float* __restrict__ y, int B, int C, int H, int W,
+                                    int ld) {
+  const int64_t total = (int64_t)B * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w_ = i % W;
+    const int64_t h = (i / W) % H;
+    const int64_t c = (i / ((int64_t)W * H)) % C;
+    const int64_t b = i / ((int64_t)W * H * C);
+    y[i] = x[((b * H + h) * W + w_) * ld + c];
+  }
+}
+
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, float* __restrict__ y, int B, int C, int H, int W,
+                                    int ld) {
+  const int64_t total = (int64_t)B * H * W * ld;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % ld;
+    const int64_t pix = i / ld;
+    const int64_t w_ = pix % W;
+    const int64_t h = (pix / W) % H;
+    const int64_t b = pix / ((int64_t)W * H);
+    y[i] = c < C ? x[((b * C + c) * H + h) * W + w_] : 0.0f;
+  }
+}
+
+static unsigned grid_for(int64_t work, int threads) {
+  const int64_t blocks = (work + threads - 1) / threads;
+  return (unsigned)std::min<int64_t>(std::max<int64_t>(blocks, 1), 148 * 32);
+}
+
+}  // namespace tobf
+
+using namespace tobf;
+
+extern "C" int tobf_ew_prepare(tobf_ew_desc* descs, int n, int64_t* total_work) {
+  if (n < 0 || (n > 0 && !descs) || !total_work) return tobf_fail(TOBF_E_INVALID, "tobf_ew_prepare: bad arguments");
+  int64_t acc = 0;
+  for (int i = 0; i < n; ++i) {
+    tobf_ew_desc& d = descs[i];
+    const int64_t pix_in = (int64_t)d.batch * d.H * d.W;
+    int64_t work = 0;
+    switch (d.op) {
+      case TOBF_OP_MAXPOOL:
+        if (d.Cpo % 4 || d.ldx % 4 || d.ldy % 4 || d.a0 < 1 || d.a1 < 1)
+          return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad maxpool geometry", i);
+        work = (int64_t)d.batch * d.Ho * d.Wo * (d.Cpo / 4);
+        break;
+      case TOBF_OP_EPI:
+        if (d.Cpo % 4 || d.ldx % 4 || d.ldy % 4 || d.nepi < 0 || d.nepi > TOBF_MAX_EPI)
+          return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad epilogue op", i);
+        work = pix_in * (d.Cpo / 4);
+        break;
+      case TOBF_OP_COPYCH:
+        if (d.Cpo < d.a0 + d.C) return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad channel copy", i);
+        work = pix_in * (d.Cpo - d.a0);
+        break;
+      case TOBF_OP_SOFTMAX:
+        work = pix_in * 32;
+        break;
+      default:
+        return tobf_fail(TOBF_E_INVALID, "ew desc %d: unknown op %d", i, d.op);
+    }
+    d.work_start = acc;
+    acc += work;
+  }
+  *total_work = acc;
+  return TOBF_OK;
+}
+
+extern "C" int tobf_ew_grouped(const tobf_ew_desc* d_descs, int n, int64_t total_work, void* stream) {
+  if (n <= 0 || total_work <= 0) return TOBF_OK;
+  if (!d_descs) return tobf_fail(TOBF_E_INVALID, "tobf_ew_grouped: null descriptors");
+  ew_grouped_kernel<<<grid_for(total_work, 256), 256, 0, (cudaStream_t)stream>>>(d_descs, n, total_work);
+  return tobf_cuda_check("tobf_ew_grouped");
+}
+
+extern "C" int tobf_equiv_compare(const float* const* a_list, const float* const* b_list, int pairs, int64_t pixels,
+                                  int32_t C, int32_t ld, float tol, float* worst, int32_t* ok, void* stream) {
+  if (pairs <= 0) return TOBF_OK;
+  if (!a_list || !b_list || !worst || !ok || C < 1 || ld < C)
+    return tobf_fail(TOBF_E_INVALID, "tobf_equiv_compare: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  init_verdict_kernel<<<(pairs + 127) / 128, 128, 0, st>>>(worst, ok, pairs);
+  const int64_t total = pixels * C;
+  dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 64), (unsigned)pairs);
+  equiv_kernel<<<grid, 256, 0, st>>>(a_list, b_list, pixels, C, ld, tol, worst, ok);
+  return tobf_cuda_check("tobf_equiv_compare");
+}
+
+extern "C" int tobf_nhwc_to_nchw(const float* x, float* y, int32_t B, int32_t C, int32_t H, int32_t W, int32_t ld,
+                                 void* stream) {
+  if (!x || !y || ld < C) return tobf_fail(TOBF_E_INVALID, "tobf_nhwc_to_nchw: bad arguments");
+  const int64_t total = (int64_t)B * C * H * W;
+  nhwc_to_nchw_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, B, C, H, W, ld);
+  return tobf_cuda_check("tobf_nhwc_to_nchw");
+}
+
+extern "C" int tobf_nchw_to_nhwc(const float* x, float* y, int32_t B, int32_t C, int32_t H, int32_t W, int32_t ld,
+                                 void* stream) {
+  if (!x || !y || ld < C) return tobf_fail(TOBF_E_INVALID, "tobf_nchw_to_nhwc: bad arguments");
+  const int64_t total = (int64_t)B * H * W * ld;
+  nchw_to_nhwc_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, B, C, H, W, ld);
+  return tobf_cuda_check("tobf_nchw_to_nhwc");
+}

@@ -1,0 +1,131 @@
+"""Device plumbing: CUDA device/stream selection, arenas, host<->device staging.
+
+PyTorch is used only as the CUDA memory / stream / collective layer; every
+computation on the hot path is a libtobf.so kernel. There is no CPU fallback:
+without a CUDA device or the native library, :func:`device` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native
+
+
+class DeviceUnavailable(RuntimeError):
+    pass
+
+
+_CTX = None
+
+
+class DeviceContext:
+    """Per-process (= per-GPU) engine context: library handle, device, stream."""
+
+    def __init__(self, index: int | None = None):
+        if not torch.cuda.is_available():
+            raise DeviceUnavailable("no CUDA device visible: the tobf engine has no CPU fallback")
+        self.lib = _native.load()
+        if index is None:
+            index = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
+        self.index = index
+        self.device = torch.device("cuda", index)
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        # cache of device copies of host weight arrays, keyed by id(base array);
+        # the base array is held so ids are never recycled while cached
+        self.weight_cache: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
+        self.weight_cache_bytes = 0
+        self.weight_cache_limit = int(os.environ.get("TOBF_WEIGHT_CACHE_BYTES", str(24 << 30)))
+
+    @property
+    def sp(self) -> int:
+        """Raw cudaStream_t of the engine stream."""
+        return self.stream.cuda_stream
+
+    def check(self, rc: int, what: str) -> None:
+        _native.check(rc, what)
+
+    # -- host arrays -> device ----------------------------------------------
+    def upload_bytes(self, buf: bytes | bytearray | memoryview) -> torch.Tensor:
+        host = torch.frombuffer(bytearray(buf), dtype=torch.uint8)
+        return host.pin_memory().to(self.device, non_blocking=True)
+
+    def upload_struct_array(self, arr) -> torch.Tensor:
+        return self.upload_bytes(memoryview(arr).cast("B"))
+
+    def cached_view(self, a: np.ndarray) -> tuple[int, tuple[int, ...]]:
+        """Device address of ``a[0, ..., 0]`` and ``a``'s element strides, with
+        views sharing one upload of their base buffer (cached by identity;
+        the base array is held so its id cannot be recycled while cached)."""
+        base = a
+        while isinstance(base.base, np.ndarray):
+            base = base.base
+        if base.dtype == np.float32 and base.flags.c_contiguous and a.dtype == np.float32:
+            key = id(base)
+            hit = self.weight_cache.get(key)
+            if hit is None or hit[0] is not base:
+                dev = torch.from_numpy(base.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+                self._remember(key, base, dev)
+            dev = self.weight_cache[key][1]
+            off = (a.__array_interface__["data"][0] - base.__array_interface__["data"][0]) // 4
+            return dev.data_ptr() + 4 * off, tuple(st // 4 for st in a.strides)
+        own = np.ascontiguousarray(a, dtype=np.float32)
+        key = id(a)
+        hit = self.weight_cache.get(key)
+        if hit is None or hit[0] is not a:
+            dev = torch.from_numpy(own.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+            self._remember(key, a, dev)
+        return self.weight_cache[key][1].data_ptr(), tuple(st // 4 for st in own.strides)
+
+    def _remember(self, key, base, dev) -> None:
+        if self.weight_cache_bytes > self.weight_cache_limit:
+            self.weight_cache.clear()
+            self.weight_cache_bytes = 0
+        self.weight_cache[key] = (base, dev)
+        self.weight_cache_bytes += dev.numel() * 4
+
+    def clear_cache(self) -> None:
+        self.weight_cache.clear()
+        self.weight_cache_bytes = 0
+
+    def sync(self) -> None:
+        self.stream.synchronize()
+        self.check(self.lib.tobf_check_fault(C.c_void_p(self.sp)), "device pipeline")
+
+
+def device(index: int | None = None) -> DeviceContext:
+    global _CTX
+    if _CTX is None:
+        _CTX = DeviceContext(index)
+    return _CTX
+
+
+class Arena:
+    """One device allocation carved into 256-B aligned float32 slices."""
+
+    def __init__(self, ctx: DeviceContext, floats: int):
+        self.ctx = ctx
+        self.buf = torch.empty(max(floats, 64), dtype=torch.float32, device=ctx.device)
+        self.base = self.buf.data_ptr()
+        self.used = 0
+
+    @staticmethod
+    def round(n: int) -> int:
+        return (n + 63) // 64 * 64
+
+    def take(self, floats: int) -> int:
+        off = self.used
+        self.used += self.round(floats)
+        if self.used > self.buf.numel():
+            raise MemoryError("arena overflow")
+        return self.base + off * 4
+
+    def view(self, ptr: int, floats: int) -> torch.Tensor:
+        off = (ptr - self.base) // 4
+        return self.buf[off:off + floats]

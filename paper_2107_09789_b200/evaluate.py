@@ -1,0 +1,194 @@
+"""Population evaluation — the north-star hot path, end to end.
+
+For a vanilla graph and a batch of obfuscation plans (one GA generation, or
+this rank's shard of it):
+
+  host    apply_plan per plan (knobs.py; infeasible plans score R = 0)
+  device  forward of the vanilla graph once and of every candidate on the
+          stacked ``trials`` inputs, verdicts vs vanilla   (executor.py)
+  device  schedule search for unseen signatures, 9 trace features per kernel,
+          T per candidate                                  (trace.py)
+  device  3 bagged LSTM predictors + greedy CTC, Levenshtein LER vs L*,
+          Eq. 10 reward                                    (fitness.py)
+  D2H     one fixed-size record per candidate
+
+Candidate feasibility = plan applied AND functionally equivalent to the
+vanilla graph (SPEC.md:567,592 score infeasible genomes 0; a
+non-function-preserving candidate is infeasible by the paper's contract).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import device
+from .executor import PopulationRun, compare_outputs, lower, trial_inputs
+from .fitness import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
+from .ir import Graph, label_sequence
+from .knobs import ObfuscationPlan, TransformError, apply_plan
+from .trace import BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, trace_population
+
+RECORD_DTYPE = np.dtype([("reward", "<f8"), ("mean_ler", "<f8"), ("latency", "<f8"), ("worst", "<f4"),
+                         ("ok", "<i4"), ("feasible", "<i4"), ("ntok", "<i4")])
+
+
+@dataclass
+class Evaluator:
+    """The bagged attacker plus the device profile / leakage case
+    the traces are produced under."""
+
+    predictors: list[Predictor] = field(default_factory=bagged_predictors)
+    case: LeakageCase = LeakageCase.C
+    profile: DeviceProfile = BUILTIN_PROFILES["default"]
+
+
+@dataclass
+class Candidate:
+    plan: ObfuscationPlan
+    graph: Graph | None
+    directives: object | None
+    error: str | None = None
+
+
+def build_candidates(vanilla: Graph, plans: list[ObfuscationPlan]) -> list[Candidate]:
+    out = []
+    for p in plans:
+        try:
+            g, d = apply_plan(vanilla, p)
+            out.append(Candidate(p, g, d))
+        except TransformError as exc:
+            out.append(Candidate(p, None, None, str(exc)))
+    return out
+
+
+@dataclass
+class PopulationResult:
+    records: np.ndarray            # RECORD_DTYPE per candidate
+    t_star: float
+    stage_ms: dict
+    forward_flops: int
+    reports: list | None = None
+
+
+class PopulationEvaluator:
+    """Evaluates batches of candidates against one vanilla graph.
+
+    ``prepare`` (host apply_plan, lowering, weight packing, descriptor
+    upload) and ``run`` (the device pipeline) are split so a benchmark can
+    time the device path with its inputs already resident in HBM, and the
+    end-to-end path separately.
+    """
+
+    def __init__(self, vanilla: Graph, evaluator: Evaluator | None = None, budget: float = 0.02, trials: int = 8,
+                 seed: int = 0, tol: float = 1e-5, eps: float = EPSILON, memo: dict | None = None):
+        self.ctx = device()
+        self.vanilla = vanilla
+        self.ev = evaluator or Evaluator()
+        self.budget, self.trials, self.seed, self.tol, self.eps = budget, trials, seed, tol, eps
+        self.memo = _SCHEDULE_CACHE if memo is None else memo
+        self.truth = encode_labels(label_sequence(vanilla))
+        self.lowered_vanilla = lower(vanilla)
+        self.x_host = torch.from_numpy(trial_inputs(vanilla.input_shape, trials, seed)).pin_memory()
+        # T* = latency of the unobfuscated graph under the same profile (Eq. 10)
+        pt = trace_population([(vanilla, None, None)], self.ev.profile, self.memo)
+        self.t_star = float(pt.totals.cpu()[0])
+
+    # ---------------------------------------------------------------- host
+    def prepare(self, plans: list[ObfuscationPlan]) -> dict:
+        t0 = time.perf_counter()
+        cands = build_candidates(self.vanilla, plans)
+        t1 = time.perf_counter()
+        feas = [i for i, c in enumerate(cands) if c.graph is not None]
+        run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph) for i in feas],
+                            reps=self.trials)
+        t2 = time.perf_counter()
+        return {"cands": cands, "feas": feas, "run": run,
+                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1)}}
+
+    # ---------------------------------------------------------------- device
+    def run(self, prep: dict, x_dev: torch.Tensor | None = None, timing: bool = False,
+            fresh_memo: bool = False) -> dict:
+        """Device pipeline over a prepared batch; returns device tensors."""
+        ctx = self.ctx
+        cands, feas, run = prep["cands"], prep["feas"], prep["run"]
+        ev = {}
+        mark = (lambda k: ev.setdefault(k, torch.cuda.Event(enable_timing=True)).record()) if timing else \
+            (lambda k: None)
+        mark("start")
+        if x_dev is None:
+            x_dev = self.x_host.to(ctx.device, non_blocking=True)
+        run.set_input(x_dev)
+        run.run()
+        ok_f, worst_f = compare_outputs(ctx, run, 0, list(range(1, len(feas) + 1)), self.tol)
+        mark("forward")
+        memo = {} if fresh_memo else self.memo
+        items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies)
+                 for i in feas]
+        pt = trace_population(items, self.ev.profile, memo) if items else None
+        mark("trace")
+        n = len(cands)
+        ncf = len(feas)
+        lers = torch.zeros((len(self.ev.predictors), n), dtype=torch.float64, device=ctx.device)
+        T = torch.zeros(n, dtype=torch.float64, device=ctx.device)
+        ok = torch.zeros(n, dtype=torch.int32, device=ctx.device)
+        worst = torch.zeros(n, dtype=torch.float32, device=ctx.device)
+        ntok0 = torch.zeros(n, dtype=torch.int32, device=ctx.device)
+        if ncf:
+            idx = torch.tensor(feas, dtype=torch.long, device=ctx.device)
+            t_max = int(np.diff(pt.offsets_host).max())
+            for p, pred in enumerate(self.ev.predictors):
+                toks, ntok = decode(pt.feats, pt.offsets, ncf, max(t_max, 1), pred)
+                _, lr, _ = edit_distances(toks, ntok, self.truth)
+                lers[p].index_copy_(0, idx, lr)
+                if p == 0:
+                    ntok0.index_copy_(0, idx, ntok)
+            T.index_copy_(0, idx, pt.totals)
+            ok.index_copy_(0, idx, ok_f)
+            worst.index_copy_(0, idx, worst_f)
+        mark("fitness")
+        R, mean = reward(lers, T, ok, self.t_star, self.budget, self.eps)
+        mark("reward")
+        return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": ntok0, "pt": pt, "events": ev,
+                "feasible": [c.graph is not None for c in cands]}
+
+    def collect(self, out: dict) -> np.ndarray:
+        rec = np.zeros(len(out["feasible"]), dtype=RECORD_DTYPE)
+        rec["reward"] = out["R"].cpu().numpy()
+        rec["mean_ler"] = out["mean"].cpu().numpy()
+        rec["latency"] = out["T"].cpu().numpy()
+        rec["worst"] = out["worst"].cpu().numpy()
+        rec["ok"] = out["ok"].cpu().numpy()
+        rec["ntok"] = out["ntok"].cpu().numpy()
+        rec["feasible"] = np.asarray(out["feasible"], dtype=np.int32)
+        self.ctx.sync()
+        return rec
+
+    def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
+        prep = self.prepare(plans)
+        out = self.run(prep, timing=True)
+        rec = self.collect(out)
+        evs = out["events"]
+        keys = list(evs)
+        stage = {b: evs[a].elapsed_time(evs[b]) for a, b in zip(keys, keys[1:])}
+        stage.update(prep["host_ms"])
+        reports = []
+        for i, c in enumerate(prep["cands"]):
+            r = rec[i]
+            reports.append(FitnessReport(c.plan, float(r["latency"]), self.t_star, [], float(r["mean_ler"]),
+                                         float(r["reward"]), feasible=c.graph is not None,
+                                         equivalent=bool(r["ok"]) if c.graph is not None else None,
+                                         worst_rel=float(r["worst"]) if c.graph is not None else None))
+        return PopulationResult(rec, self.t_star, stage, prep["run"].gemm_flops(), reports)
+
+
+def fitness(plan: ObfuscationPlan, graph: Graph, evaluator: Evaluator, budget: float, t_star: float | None = None,
+            trials: int = 8, seed: int = 0) -> FitnessReport:
+    """SPEC.md:563-571 fitness for one plan (GPU-backed)."""
+    pe = PopulationEvaluator(graph, evaluator, budget=budget, trials=trials, seed=seed)
+    if t_star is not None:
+        pe.t_star = float(t_star)
+    return pe.evaluate([plan]).reports[0]

@@ -1,0 +1,481 @@
+"""GPU executor for obfuscated candidate graphs (drop-in for traceobf.interpreter).
+
+``execute`` / ``equivalence_check`` keep the signatures and semantics of
+interpreter.py:75-118; underneath, graphs are lowered to fused device ops
+and run on libtobf.so:
+
+* Conv2D and Linear become implicit-GEMM problems of the tcgen05 3xTF32
+  kernel (Linear = full-extent convolution, its NCHW-flatten weight rows
+  addressed through strides). Sole-consumer BatchNorm / ReLU / Add chains
+  fold into the GEMM epilogue (selective fusion in the executor; the
+  *modelled* kernel partition of the cost model is ``kernels.fuse``).
+* MaxPool, unfused injective chains, Concat / Slice and SoftMax are
+  grouped memory-bound ops.
+* Trials are stacked along the batch dimension (trial t's element k is
+  batch row t*b + k), and a whole population is lowered together: ops are
+  levelled by dependency depth and every level of every candidate launches
+  as ONE grouped conv kernel per N-tile width plus one grouped ew kernel.
+
+Activation layout on the device: NHWC float32, channels padded to a
+multiple of 4 with zeros (16-B vector / bulk-copy alignment).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .engine import Arena, DeviceContext, device
+from .ir import BN_EPS, Graph, OperatorKind as K, ShapeMismatch, TensorShape, shape_map, topo_order
+
+
+def _rup4(c: int) -> int:
+    return (c + 3) // 4 * 4
+
+
+@dataclass
+class Step:
+    """One epilogue step: ('affine', node) | ('relu',) | ('add', value_node) | ('const', node)."""
+    op: str
+    ref: int = -1
+
+
+@dataclass
+class Op:
+    kind: str                  # 'gemm' | 'pool' | 'epi' | 'copy' | 'softmax'
+    out: int                   # node whose value this op materialises
+    src: int                   # value node read (-1 = graph input)
+    node: int = -1             # anchor node (conv/linear/pool)
+    steps: list = field(default_factory=list)
+    deps: list = field(default_factory=list)   # value nodes read (incl. src), -1 = input
+    a0: int = 0                # copy: dst channel offset
+    a1: int = 0                # copy: src channel offset
+    cc: int = 0                # copy: channel count
+    level: int = 0
+
+
+@dataclass
+class Lowered:
+    graph: Graph
+    shapes: dict
+    ops: list
+    values: set      # node ids with a materialised buffer
+    out_node: int
+
+
+_CHAIN_KINDS = (K.BatchNorm, K.ReLU, K.Add)
+
+
+def lower(graph: Graph) -> Lowered:
+    """Partition a graph into device ops (host-only; no device needed)."""
+    order = topo_order(graph)
+    shapes = shape_map(graph, order)
+    succ = graph.successor_index()
+    nodes = graph.nodes
+    covered: set[int] = set()
+    ops: list[Op] = []
+    produced: set[int] = set()  # value nodes already produced by an earlier op
+
+    def absorb(op: Op, tail: int) -> int:
+        """Extend op's epilogue along sole-consumer injective successors."""
+        while tail != graph.output_id:
+            nxt = succ[tail]
+            if len(nxt) != 1:
+                break
+            s = nodes[nxt[0]]
+            if s.kind not in _CHAIN_KINDS:
+                break
+            extra = []
+            if s.kind is K.BatchNorm:
+                extra.append(Step("affine", s.id))
+            elif s.kind is K.ReLU:
+                extra.append(Step("relu"))
+            else:
+                others = [p for p in s.inputs if p != tail]
+                if len(others) != len(s.inputs) - 1:
+                    break  # same value twice
+                if any(p not in produced for p in others):
+                    break  # other operand not yet materialised
+                extra += [Step("add", p) for p in others]
+                if s.weights is not None:
+                    extra.append(Step("const", s.id))
+            if len(op.steps) + len(extra) > N.TOBF_MAX_EPI:
+                break
+            op.steps += extra
+            op.deps += [st.ref for st in extra if st.op == "add"]
+            covered.add(s.id)
+            tail = s.id
+        return tail
+
+    for nid in order:
+        if nid in covered:
+            continue
+        n = nodes[nid]
+        src = n.inputs[0] if n.inputs else -1
+        if n.kind in (K.Conv2D, K.Linear):
+            op = Op("gemm", nid, src, node=nid, deps=[src])
+            op.out = absorb(op, nid)
+        elif n.kind is K.MaxPool:
+            op = Op("pool", nid, src, node=nid, deps=[src])
+        elif n.kind is K.SoftMax:
+            op = Op("softmax", nid, src, node=nid, deps=[src])
+        elif n.kind in (K.BatchNorm, K.ReLU):
+            op = Op("epi", nid, src, node=nid, deps=[src],
+                    steps=[Step("affine", nid) if n.kind is K.BatchNorm else Step("relu")])
+            op.out = absorb(op, nid)
+        elif n.kind is K.Add:
+            srcs = n.inputs if n.inputs else [-1]
+            op = Op("epi", nid, srcs[0], node=nid, deps=list(srcs),
+                    steps=[Step("add", p) for p in srcs[1:]])
+            if n.weights is not None:
+                op.steps.append(Step("const", nid))
+            if len(op.steps) > N.TOBF_MAX_EPI:  # long n-ary Add: split into a chain of copies
+                raise NotImplementedError("Add with more than 6 operands")
+            op.out = absorb(op, nid)
+        elif n.kind is K.Concat:
+            off = 0
+            for p in n.inputs:
+                c = shapes[p].channels
+                ops.append(Op("copy", nid, p, node=nid, deps=[p], a0=off, a1=0, cc=c))
+                off += c
+            covered.add(nid)
+            produced.add(nid)
+            continue
+        elif n.kind is K.Slice:
+            op = Op("copy", nid, src, node=nid, deps=[src], a0=0, a1=n.attrs["start"],
+                    cc=n.attrs["stop"] - n.attrs["start"])
+        else:
+            raise NotImplementedError(n.kind)
+        covered.add(nid)
+        ops.append(op)
+        produced.add(op.out)
+    # dependency levels: level(op) = 1 + max(level of producers of its deps)
+    level_of_value = {-1: 0}
+    concat_level: dict[int, int] = {}
+    for op in ops:
+        lv = 1 + max(level_of_value[d] for d in op.deps)
+        op.level = lv
+        if op.kind == "copy" and nodes[op.out].kind is K.Concat:
+            concat_level[op.out] = max(concat_level.get(op.out, 0), lv)
+            level_of_value[op.out] = concat_level[op.out]
+        else:
+            level_of_value[op.out] = lv
+    values = {op.out for op in ops}
+    return Lowered(graph, shapes, ops, values, graph.output_id)
+
+
+# ---------------------------------------------------------------------------
+# Population run: allocate, pack, describe, launch
+# ---------------------------------------------------------------------------
+
+class PopulationRun:
+    """Runs the forward of several lowered graphs on the same stacked input."""
+
+    def __init__(self, ctx: DeviceContext, lowered: list[Lowered], reps: int):
+        self.ctx = ctx
+        self.lowered = lowered
+        self.reps = reps
+        self._keep: list = []
+        g0 = lowered[0].graph
+        for lw in lowered:
+            if lw.graph.input_shape != g0.input_shape:
+                raise ShapeMismatch(-1, "population graphs disagree on the input shape")
+        ishape = g0.input_shape
+        self.batch = ishape.batch * reps
+        # ---- sizes -> one arena for activations, constants and weight images
+        act_floats = Arena.round(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
+        wimg_floats = 0
+        for lw in lowered:
+            for v in lw.values:
+                s = lw.shapes[v]
+                act_floats += Arena.round(self.batch * s.height * s.width * _rup4(s.channels))
+            for op in lw.ops:
+                if op.kind == "gemm":
+                    k1, k2, cp, j = self._gemm_geom(lw, op)
+                    bn = 128 if j > 64 else 64
+                    wimg_floats += Arena.round(self.ctx.lib.tobf_wimg_bytes(k1, k2, cp, j, bn) // 4)
+                for st in op.steps:
+                    if st.op == "affine":
+                        wimg_floats += Arena.round(2 * _rup4(lw.shapes[st.ref].channels))
+                    elif st.op == "const":
+                        s = lw.shapes[st.ref]
+                        wimg_floats += Arena.round(ishape.batch * s.height * s.width * _rup4(s.channels))
+        self.arena = Arena(ctx, act_floats + wimg_floats + 4096)
+        self.x_ptr = self.arena.take(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
+        self.bufs: list[dict[int, int]] = []
+        for lw in lowered:
+            b = {-1: self.x_ptr}
+            for v in sorted(lw.values):
+                s = lw.shapes[v]
+                b[v] = self.arena.take(self.batch * s.height * s.width * _rup4(s.channels))
+            self.bufs.append(b)
+        self._prepare()
+
+    # -------------------------------------------------------------- helpers
+    @staticmethod
+    def _in_shape(lw: Lowered, op: Op) -> TensorShape:
+        return lw.shapes[op.src] if op.src >= 0 else lw.graph.input_shape
+
+    def _gemm_geom(self, lw: Lowered, op: Op):
+        n = lw.graph.nodes[op.node]
+        s_in = self._in_shape(lw, op)
+        if n.kind is K.Conv2D:
+            return n.attrs["k1"], n.attrs["k2"], _rup4(s_in.channels), n.attrs["j"]
+        return s_in.height, s_in.width, _rup4(s_in.channels), n.attrs["j"]
+
+    def _affine(self, lw: Lowered, nid: int) -> int:
+        w = lw.graph.nodes[nid].weights.astype(np.float64)
+        scale, shift, mean, var = w
+        a = scale / np.sqrt(var + BN_EPS)
+        b = shift - mean * a
+        cp = _rup4(w.shape[1])
+        host = np.zeros((2, cp), np.float32)
+        host[0, :w.shape[1]] = a
+        host[1, :w.shape[1]] = b
+        ptr = self.arena.take(2 * cp)
+        t = torch.from_numpy(host.reshape(-1))
+        self.arena.view(ptr, 2 * cp).copy_(t.pin_memory(), non_blocking=True)
+        self._keep.append(t)
+        return ptr
+
+    def _const(self, lw: Lowered, nid: int) -> int:
+        node = lw.graph.nodes[nid]
+        s = lw.shapes[nid]
+        b0 = lw.graph.input_shape.batch
+        cp = _rup4(s.channels)
+        src_ptr, _ = self.ctx.cached_view(np.ascontiguousarray(node.weights, dtype=np.float32))
+        ptr = self.arena.take(b0 * s.height * s.width * cp)
+        self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(src_ptr), C.c_void_p(ptr), b0, s.channels,
+                                                      s.height, s.width, cp, C.c_void_p(self.ctx.sp)),
+                       "const staging")
+        return ptr
+
+    def _epi_fill(self, lw: Lowered, bufs: dict, steps: list, epi_arr) -> int:
+        for i, st in enumerate(steps):
+            e = epi_arr[i]
+            if st.op == "affine":
+                e.op, e.aux, e.ptr = N.EPI_AFFINE, _rup4(lw.shapes[st.ref].channels), self._affine(lw, st.ref)
+            elif st.op == "relu":
+                e.op, e.aux, e.ptr = N.EPI_RELU, 0, None
+            elif st.op == "add":
+                s = lw.shapes[st.ref] if st.ref >= 0 else lw.graph.input_shape
+                e.op, e.aux, e.ptr = N.EPI_ADD_TENSOR, _rup4(s.channels), bufs[st.ref]
+            elif st.op == "const":
+                e.op, e.aux, e.ptr = N.EPI_ADD_CONST, lw.graph.input_shape.batch, self._const(lw, st.ref)
+        return len(steps)
+
+    # -------------------------------------------------------------- prepare
+    def _prepare(self) -> None:
+        ctx, lib = self.ctx, self.ctx.lib
+        levels: dict[int, dict[str, list]] = {}
+        for gi, lw in enumerate(self.lowered):
+            bufs = self.bufs[gi]
+            for op in lw.ops:
+                lvl = levels.setdefault(op.level, {"g64": [], "g128": [], "ew": []})
+                s_in = self._in_shape(lw, op)
+                s_out = lw.shapes[op.out]
+                if op.kind == "gemm":
+                    n = lw.graph.nodes[op.node]
+                    k1, k2, cp, j = self._gemm_geom(lw, op)
+                    bn = 128 if j > 64 else 64
+                    # weight view -> strides over (u, v, c, n)
+                    wptr, st = ctx.cached_view(n.weights)
+                    if n.kind is K.Conv2D:
+                        su, sv, sc, sn = st
+                        stride, pad = n.attrs["stride"], n.attrs["padding"]
+                    else:
+                        r, cstride = st
+                        H, W = s_in.height, s_in.width
+                        su, sv, sc, sn = W * r, r, H * W * r, cstride
+                        stride, pad = 1, 0
+                    nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
+                    wimg = self.arena.take(nbytes // 4)
+                    ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, s_in.channels, cp, j, su, sv, sc, sn,
+                                                    bn, C.c_void_p(wimg), C.c_void_p(ctx.sp)), "pack weights")
+                    d = N.ConvDesc()
+                    d.x, d.wimg, d.y = bufs[op.src], wimg, bufs[op.out]
+                    d.batch, d.H, d.W, d.Cp = self.batch, s_in.height, s_in.width, cp
+                    d.Ho, d.Wo, d.Cpo, d.j = s_out.height, s_out.width, _rup4(j), j
+                    d.k1, d.k2, d.stride, d.pad = k1, k2, stride, pad
+                    d.ldx, d.ldy = cp, _rup4(j)
+                    d.nepi = self._epi_fill(lw, bufs, op.steps, d.epi)
+                    lvl["g128" if bn == 128 else "g64"].append(d)
+                    continue
+                e = N.EwDesc()
+                e.x, e.y = bufs[op.src], bufs[op.out]
+                e.batch, e.H, e.W = self.batch, s_in.height, s_in.width
+                e.ldx = _rup4(s_in.channels)
+                e.ldy = _rup4(s_out.channels)
+                if op.kind == "pool":
+                    n = lw.graph.nodes[op.node]
+                    e.op, e.C, e.Cpo = N.OP_MAXPOOL, s_in.channels, _rup4(s_in.channels)
+                    e.Ho, e.Wo, e.a0, e.a1 = s_out.height, s_out.width, n.attrs["window"], n.attrs["stride"]
+                elif op.kind == "epi":
+                    e.op, e.C, e.Cpo = N.OP_EPI, s_out.channels, _rup4(s_out.channels)
+                    e.Ho, e.Wo = s_out.height, s_out.width
+                    e.nepi = self._epi_fill(lw, bufs, op.steps, e.epi)
+                elif op.kind == "copy":
+                    total = s_out.channels
+                    last = op.a0 + op.cc == total
+                    e.op, e.C, e.a0, e.a1 = N.OP_COPYCH, op.cc, op.a0, op.a1
+                    e.Cpo = _rup4(total) if last else op.a0 + op.cc
+                elif op.kind == "softmax":
+                    e.op, e.C, e.Cpo = N.OP_SOFTMAX, s_in.channels, _rup4(s_in.channels)
+                lvl["ew"].append(e)
+        # sort GEMM problems by descending K so long tiles are scheduled first
+        self.launches = []
+        blobs = []
+        for lv in sorted(levels):
+            grp = levels[lv]
+            for key, bn in (("g128", 128), ("g64", 64)):
+                lst = sorted(grp[key], key=lambda d: -(d.k1 * d.k2 * d.Cp))
+                if not lst:
+                    continue
+                arr = (N.ConvDesc * len(lst))(*lst)
+                tot = C.c_int64()
+                ctx.check(lib.tobf_conv_prepare(arr, len(lst), bn, C.byref(tot)), "conv prepare")
+                blobs.append(bytes(arr))
+                self.launches.append(("conv", len(blobs) - 1, len(lst), tot.value, bn))
+            if grp["ew"]:
+                arr = (N.EwDesc * len(grp["ew"]))(*grp["ew"])
+                tot = C.c_int64()
+                ctx.check(lib.tobf_ew_prepare(arr, len(grp["ew"]), C.byref(tot)), "ew prepare")
+                blobs.append(bytes(arr))
+                self.launches.append(("ew", len(blobs) - 1, len(grp["ew"]), tot.value, 0))
+        # one H2D copy for every descriptor table
+        offs, total = [], 0
+        for b in blobs:
+            offs.append(total)
+            total += (len(b) + 255) // 256 * 256
+        host = bytearray(total)
+        for o, b in zip(offs, blobs):
+            host[o:o + len(b)] = b
+        self.desc_dev = ctx.upload_bytes(host) if total else None
+        base = self.desc_dev.data_ptr() if total else 0
+        self.launches = [(k, base + offs[i], n, tot, bn) for (k, i, n, tot, bn) in self.launches]
+
+    # -------------------------------------------------------------- run
+    def set_input(self, x_nchw: torch.Tensor) -> None:
+        """x: (batch, C, H, W) float32 on the device (batch = graph batch * reps)."""
+        s = self.lowered[0].graph.input_shape
+        if tuple(x_nchw.shape) != (self.batch, s.channels, s.height, s.width):
+            raise ShapeMismatch(-1, f"input shape {tuple(x_nchw.shape)} != stacked {(self.batch, *s.as_tuple()[1:])}")
+        x = x_nchw.contiguous()
+        self._x_keep = x
+        self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(x.data_ptr()), C.c_void_p(self.x_ptr), self.batch,
+                                                      s.channels, s.height, s.width, _rup4(s.channels),
+                                                      C.c_void_p(self.ctx.sp)), "input staging")
+
+    def run(self) -> None:
+        lib, sp = self.ctx.lib, C.c_void_p(self.ctx.sp)
+        for kind, dptr, n, tot, bn in self.launches:
+            if kind == "conv":
+                rc = lib.tobf_conv_grouped(C.c_void_p(dptr), n, tot, bn, sp)
+            else:
+                rc = lib.tobf_ew_grouped(C.c_void_p(dptr), n, tot, sp)
+            self.ctx.check(rc, kind)
+
+    def output_ptr(self, gi: int) -> tuple[int, TensorShape]:
+        lw = self.lowered[gi]
+        return self.bufs[gi][lw.out_node], lw.shapes[lw.out_node]
+
+    def output_nchw(self, gi: int) -> torch.Tensor:
+        ptr, s = self.output_ptr(gi)
+        out = torch.empty((self.batch, s.channels, s.height, s.width), dtype=torch.float32, device=self.ctx.device)
+        self.ctx.check(self.ctx.lib.tobf_nhwc_to_nchw(C.c_void_p(ptr), C.c_void_p(out.data_ptr()), self.batch,
+                                                      s.channels, s.height, s.width, _rup4(s.channels),
+                                                      C.c_void_p(self.ctx.sp)), "output staging")
+        return out
+
+    def gemm_flops(self) -> int:
+        """Algorithmic conv/linear FLOPs of one run (all graphs, all reps)."""
+        total = 0
+        for lw in self.lowered:
+            for op in lw.ops:
+                if op.kind == "gemm":
+                    n = lw.graph.nodes[op.node]
+                    s = lw.shapes[op.node]
+                    s_in = self._in_shape(lw, op)
+                    kk = (n.attrs["k1"] * n.attrs["k2"] * n.attrs["c"]) if n.kind is K.Conv2D else n.attrs["c"]
+                    total += 2 * self.batch * s.height * s.width * s.channels * kk
+        return total
+
+
+# ---------------------------------------------------------------------------
+# Drop-in API (interpreter.py:75-118)
+# ---------------------------------------------------------------------------
+
+def trial_inputs(shape: TensorShape, trials: int, seed: int) -> np.ndarray:
+    """The exact inputs equivalence_check draws: one default_rng(seed) stream,
+    ``trials`` standard-normal draws of the input shape, cast to float32
+    (interpreter.py:107-111), stacked along the batch dimension."""
+    rng = np.random.default_rng(seed)
+    xs = [rng.standard_normal(shape.as_tuple()).astype(np.float32) for _ in range(trials)]
+    return np.concatenate(xs, axis=0)
+
+
+def execute(graph: Graph, x: np.ndarray) -> np.ndarray:
+    """Run ``graph`` on ``x`` (NCHW float32) on the GPU; returns the output node's
+    tensor as a numpy array (interpreter.py:75-90)."""
+    if tuple(x.shape) != graph.input_shape.as_tuple():
+        raise ShapeMismatch(-1, f"input shape {x.shape} != {graph.input_shape.as_tuple()}")
+    ctx = device()
+    run = PopulationRun(ctx, [lower(graph)], reps=1)
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(ctx.device)
+    run.set_input(xd)
+    run.run()
+    out = run.output_nchw(0)
+    ctx.sync()
+    return out.cpu().numpy()
+
+
+def equivalence_check(g1: Graph, g2: Graph, trials: int = 8, seed: int = 0,
+                      tol: float = 1e-5) -> tuple[bool, float]:
+    """Seeded random-input functional comparison (interpreter.py:93-118): both
+    graphs run all ``trials`` inputs stacked in one batch; verdict and worst
+    relative difference use the reference's float32 formulas bit for bit."""
+    if g1.input_shape != g2.input_shape:
+        raise ShapeMismatch(-1, "input shapes differ")
+    out1 = shape_map(g1)[g1.output_id]
+    out2 = shape_map(g2)[g2.output_id]
+    if out1 != out2:
+        raise ShapeMismatch(-1, f"output shapes differ: {out1} vs {out2}")
+    res = evaluate_equivalence(g1, [g2], trials=trials, seed=seed, tol=tol)
+    return bool(res[0][0]), float(res[1][0])
+
+
+def compare_outputs(ctx: DeviceContext, run: PopulationRun, ref_index: int, cand_indices: list[int],
+                    tol: float) -> tuple[torch.Tensor, torch.Tensor]:
+    """Device verdicts of candidates vs the reference graph output (a = ref, b = cand)."""
+    ref_ptr, s = run.output_ptr(ref_index)
+    a_list = np.array([ref_ptr] * len(cand_indices), dtype=np.uint64)
+    b_list = np.array([run.output_ptr(i)[0] for i in cand_indices], dtype=np.uint64)
+    ptrs = ctx.upload_bytes(a_list.tobytes() + b_list.tobytes())
+    worst = torch.empty(len(cand_indices), dtype=torch.float32, device=ctx.device)
+    ok = torch.empty(len(cand_indices), dtype=torch.int32, device=ctx.device)
+    pixels = run.batch * s.height * s.width
+    ctx.check(ctx.lib.tobf_equiv_compare(C.c_void_p(ptrs.data_ptr()), C.c_void_p(ptrs.data_ptr() + 8 * len(a_list)),
+                                         len(cand_indices), pixels, s.channels, _rup4(s.channels), C.c_float(tol),
+                                         C.c_void_p(worst.data_ptr()), C.c_void_p(ok.data_ptr()),
+                                         C.c_void_p(ctx.sp)), "equivalence compare")
+    run._keep.append(ptrs)
+    return ok, worst
+
+
+def evaluate_equivalence(reference: Graph, candidates: list[Graph], trials: int = 8, seed: int = 0,
+                         tol: float = 1e-5):
+    """Batched equivalence_check(reference, c) for every candidate c: one
+    forward of the reference and of all candidates on the stacked trials.
+    Returns (ok[np.bool_], worst[np.float64]) per candidate."""
+    ctx = device()
+    run = PopulationRun(ctx, [lower(reference)] + [lower(g) for g in candidates], reps=trials)
+    x = trial_inputs(reference.input_shape, trials, seed)
+    run.set_input(torch.from_numpy(x).to(ctx.device))
+    run.run()
+    ok, worst = compare_outputs(ctx, run, 0, list(range(1, len(candidates) + 1)), tol)
+    ctx.sync()
+    return ok.cpu().numpy().astype(bool), worst.cpu().numpy().astype(np.float64)

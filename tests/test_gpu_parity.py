@@ -1,0 +1,219 @@
+"""GPU parity: libtobf.so kernels vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE north_star): executor outputs within 1e-4 relative
+(|gpu - oracle| <= 1e-4 * (1 + |oracle|), fp32 path); trace features,
+schedules, T, decoded tokens, edit distances, LER and rewards bit-exact.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import costmodel_ref as CM
+from oracle import fitness_ref as FR
+from oracle import interp_ref as IR
+from paper_2107_09789_b200 import _native as N
+from paper_2107_09789_b200 import executor, fitness, fixtures, ga, knobs, trace
+from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
+from paper_2107_09789_b200.ir import label_sequence
+
+pytestmark = pytest.mark.gpu
+FP32_TOL = 1e-4
+
+
+def _rel(got, ref):
+    return float(np.max(np.abs(got.astype(np.float64) - ref) / (1.0 + np.abs(ref))))
+
+
+def _plans(graph, mode, n, seed):
+    rng = np.random.default_rng(seed)
+    space = ga.search_space(graph, mode)
+    sizes = ga.domain_sizes(mode, space)
+    return [ga.decode_genome(graph, mode, space, rng.integers(0, sizes)) for _ in range(n)]
+
+
+# ----------------------------------------------------------------- conv kernel
+CONV_CASES = [  # (b, c, h, w, j, k, stride, pad)
+    (2, 64, 56, 56, 128, 3, 1, 1),     # cfg1 C2
+    (1, 3, 64, 64, 64, 7, 2, 3),       # stem (c=3 -> padded 4)
+    (2, 128, 14, 14, 68, 1, 1, 0),     # widened j, 1x1
+    (1, 20, 9, 9, 17, 5, 1, 2),        # in4 branch of a widened layer, kernel-widened
+    (2, 96, 20, 20, 192, 7, 2, 3),     # widened + 2 rings
+    (3, 512, 7, 7, 512, 3, 1, 1),      # late layer, K = 4608 (chunked TMEM drain)
+    (1, 34, 11, 11, 144, 11, 1, 5),    # 11x11 kernel (7x7 + 2 rings)
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_kernel_matches_oracle(ctx, case):
+    b, c, h, w, j, k, s, p = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+    wt = (rng.standard_normal((k, k, c, j)) * np.sqrt(2.0 / (k * k * c))).astype(np.float32)
+    from paper_2107_09789_b200.ir import Graph, Node, OperatorKind, TensorShape
+    g = Graph({0: Node(0, OperatorKind.Conv2D, {"k1": k, "k2": k, "c": c, "j": j, "stride": s, "padding": p}, wt, [])},
+              0, TensorShape(b, c, h, w))
+    got = executor.execute(g, x)
+    ref = IR.conv2d(x, wt, s, p).astype(np.float64)
+    assert got.shape == ref.shape
+    assert _rel(got, ref) <= FP32_TOL
+
+
+# ----------------------------------------------------------------- executor
+@pytest.mark.parametrize("name,mode,size", [("c1c2", "dimension", 24), ("resnet18", "sequence", 64),
+                                            ("resnet18", "dimension", 64), ("vgg16", "dimension", 32)])
+def test_execute_obfuscated_matches_oracle(ctx, name, mode, size):
+    kw = {"hidden": 256} if name == "vgg16" else {}
+    g = fixtures.FIXTURES[name](size=size, **kw)
+    x = np.random.default_rng(5).standard_normal(g.input_shape.as_tuple()).astype(np.float32)
+    for plan in _plans(g, mode, 2, seed=11):
+        og, _ = knobs.apply_plan(g, plan)
+        got = executor.execute(og, x)
+        _, vals = IR.execute(og, x, keep=True)
+        ref = vals[og.output_id].astype(np.float64)
+        assert _rel(got, ref) <= FP32_TOL
+        # pre-softmax logits too (softmax saturates with random init)
+        pre = og.nodes[og.output_id].inputs
+        if og.nodes[og.output_id].kind.value == "SoftMax" and pre:
+            from paper_2107_09789_b200.ir import Graph
+            sub = Graph(og.nodes, pre[0], og.input_shape)
+            got_l = executor.execute(sub, x)
+            assert _rel(got_l, vals[pre[0]].astype(np.float64)) <= FP32_TOL
+
+
+def test_equivalence_verdicts_match_oracle(ctx):
+    g = fixtures.c1c2(size=24)
+    plans = _plans(g, "dimension", 3, seed=3)
+    cands = [knobs.apply_plan(g, p)[0] for p in plans]
+    # a deliberately broken candidate: Eq. 5-literal (non-identity) deepen kernel
+    bad = knobs.deepen_layer(g, 0, kernel_init=lambda ch: np.full((1, 1, ch, ch), 1.0 / ch, np.float32))
+    ok, worst = executor.evaluate_equivalence(g, cands + [bad], trials=3, seed=0)
+    for i, cg in enumerate(cands + [bad]):
+        ref_ok, ref_worst = IR.equivalence_check(g, cg, trials=3, seed=0)
+        assert bool(ok[i]) == ref_ok
+        assert worst[i] < 1e-4 if ref_ok else worst[i] > 1e-3
+    assert not ok[-1]
+
+
+def test_equivalence_check_dropin(ctx):
+    g = fixtures.c1c2(size=16)
+    og, _ = knobs.apply_plan(g, _plans(g, "dimension", 1, seed=9)[0])
+    ok, worst = executor.equivalence_check(g, og, trials=2, seed=1)
+    assert ok is True and 0.0 <= worst < 1e-5
+
+
+# ----------------------------------------------------------------- trace
+@pytest.mark.parametrize("name,mode", [("c1c2", "dimension"), ("resnet18", "sequence"), ("resnet18", "dimension")])
+def test_trace_bit_exact(ctx, name, mode):
+    g = fixtures.FIXTURES[name]()
+    plans = _plans(g, mode, 3, seed=21)
+    items = []
+    for p in plans:
+        og, d = knobs.apply_plan(g, p)
+        items.append((og, d.fusion_limits, d.schedule_strategies))
+    memo_gpu, memo_ref = {}, CM.ScheduleMemo()
+    pt = trace.trace_population(items, trace.BUILTIN_PROFILES["default"], memo_gpu)
+    feats = pt.feats.cpu().numpy()
+    totals = pt.totals.cpu().numpy()
+    for i, (og, lim, st) in enumerate(items):
+        kern, sch, rows, T = CM.profile_pipeline(og, "default", lim, st, memo_ref)
+        cg = pt.compiled[i]
+        assert [k.node_ids for k in cg.kernels] == kern
+        assert [(s.tile_y, s.tile_x) for s in cg.schedules] == sch
+        lo, hi = pt.offsets_host[i], pt.offsets_host[i + 1]
+        want = np.array([[r[f] for f in CM.FEATURES] for r in rows], dtype=np.float64)
+        assert np.array_equal(feats[lo:hi].view(np.uint64), want.view(np.uint64))
+        assert totals[i] == T  # bit-exact Neumaier total
+
+
+def test_profile_pipeline_dropin(ctx):
+    g = fixtures.resnet18()
+    tr = trace.profile_pipeline(g, trace.LeakageCase.C, trace.BUILTIN_PROFILES["default"])
+    assert tr.total_latency == 1846199.5435783395  # T* of the fixture under the reference
+    assert len(tr.steps) == 32
+
+
+# ----------------------------------------------------------------- fitness
+def _random_trace_rows(rng, ncand):
+    g = fixtures.resnet18()
+    items = []
+    for p in _plans(g, "sequence", ncand, seed=int(rng.integers(1 << 30))):
+        og, d = knobs.apply_plan(g, p)
+        items.append((og, d.fusion_limits, d.schedule_strategies))
+    return trace.trace_population(items, trace.BUILTIN_PROFILES["default"], {})
+
+
+@pytest.mark.parametrize("hidden", [128, 256, 512])
+def test_lstm_ctc_bit_exact(ctx, hidden):
+    rng = np.random.default_rng(hidden)
+    pt = _random_trace_rows(rng, 5)
+    pred = fitness.init_predictor(hidden, 9, seed=hidden)
+    t_max = int(np.diff(pt.offsets_host).max())
+    toks, ntok = fitness.decode(pt.feats, pt.offsets, 5, t_max, pred)
+    toks, ntok = toks.cpu().numpy(), ntok.cpu().numpy()
+    feats = pt.feats.cpu().numpy()
+    for i in range(5):
+        lo, hi = pt.offsets_host[i], pt.offsets_host[i + 1]
+        want = FR.lstm_ctc(feats[lo:hi], 9, pred.weights())
+        assert list(toks[i, :ntok[i]]) == want
+
+
+def test_levenshtein_bit_exact(ctx):
+    rng = np.random.default_rng(7)
+    for m in (0, 1, 3, 24, 31, 32, 33, 70):
+        truth = rng.integers(1, 5, m).astype(np.int8)
+        B, t_max = 40, 90
+        lens = rng.integers(0, t_max + 1, B).astype(np.int32)
+        toks = rng.integers(1, 5, (B, t_max)).astype(np.int8)
+        td = torch.from_numpy(toks).to(ctx.device)
+        nd = torch.from_numpy(lens).to(ctx.device)
+        if m == 0:
+            continue  # LER undefined for an empty truth (EmptyTruth); ED covered by lens-only cases
+        ed, lr, _ = fitness.edit_distances(td, nd, truth)
+        ed, lr = ed.cpu().numpy(), lr.cpu().numpy()
+        for b in range(B):
+            want = FR.levenshtein(toks[b, :lens[b]], truth)
+            assert ed[b] == want
+            assert lr[b] == want / m
+
+
+def test_spec_known_answers_on_device(ctx):
+    C_, L_, M_ = 1, 2, 3
+    assert fitness.levenshtein([1, 2, 3], [1, 2, 3]) == 0
+    assert fitness.levenshtein([], [1, 2]) == 2
+    assert fitness.levenshtein([C_, L_, M_], [C_, M_]) == 1
+    assert fitness.ler([1] * 10, [1] * 10) == 0.0
+    assert fitness.ler([1] * 11, [1] * 10) == 0.1
+    lers = torch.tensor([[2.0, 2.0, 0.0]], dtype=torch.float64, device=ctx.device)
+    T = torch.tensor([100.0, 150.0, 100.0], dtype=torch.float64, device=ctx.device)
+    feas = torch.ones(3, dtype=torch.int32, device=ctx.device)
+    R, mean = fitness.reward(lers, T, feas, 100.0, 0.0)
+    R = R.cpu().numpy()
+    assert R[0] == 40.0 and abs(R[1] - 6.666666666666667) < 1e-15 and R[2] == 0.0
+
+
+# ----------------------------------------------------------------- whole path
+def test_population_evaluation_matches_oracles(ctx):
+    g = fixtures.resnet18(size=64)
+    plans = _plans(g, "sequence", 6, seed=4)
+    ev = Evaluator()
+    pe = PopulationEvaluator(g, ev, budget=0.02, trials=2, seed=0, memo={})
+    res = pe.evaluate(plans)
+    rec = res.records
+    truth = fitness.encode_labels(label_sequence(g))
+    memo = CM.ScheduleMemo()
+    _, _, _, t_star = CM.profile_pipeline(g, "default", None, None, CM.ScheduleMemo())
+    assert res.t_star == t_star
+    for i, p in enumerate(plans):
+        og, d = knobs.apply_plan(g, p)
+        kern, sch, rows, T = CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)
+        assert rec["latency"][i] == T
+        ok, _ = IR.equivalence_check(g, og, trials=2, seed=0)
+        assert bool(rec["ok"][i]) == ok
+        feats = np.array([[r[f] for f in CM.FEATURES] for r in rows])
+        lers = [FR.ler(FR.lstm_ctc(feats, 9, pr.weights()), truth) for pr in ev.predictors]
+        R, mean = FR.eq10(lers, T, ok, t_star, 0.02)
+        assert rec["mean_ler"][i] == mean
+        assert rec["reward"][i] == R
