@@ -36,19 +36,20 @@ def _order(graph) -> list[int]:
 
 def conv2d(x: np.ndarray, w: np.ndarray, stride: int, padding: int) -> np.ndarray:
     """interpreter.py:22-30: zero-padded direct convolution, (k1,k2,c,j) kernel,
-    as one float32 GEMM over K = (u, v, c)."""
+    as one GEMM over K = (u, v, c) in x's dtype (float32 = the reference's)."""
     k1, k2, c, j = w.shape
+    dt = x.dtype
     b, _, h, wd = x.shape
     xp = np.pad(x, ((0, 0), (0, 0), (padding, padding), (padding, padding))) if padding else x
     ho = (h + 2 * padding - k1) // stride + 1
     wo = (wd + 2 * padding - k2) // stride + 1
-    cols = np.empty((b, ho, wo, k1, k2, c), dtype=np.float32)
+    cols = np.empty((b, ho, wo, k1, k2, c), dtype=dt)
     for u in range(k1):
         for v in range(k2):
             patch = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
             cols[:, :, :, u, v, :] = patch.transpose(0, 2, 3, 1)
-    y = cols.reshape(b * ho * wo, k1 * k2 * c) @ w.reshape(k1 * k2 * c, j)
-    return y.reshape(b, ho, wo, j).transpose(0, 3, 1, 2).astype(np.float32)
+    y = cols.reshape(b * ho * wo, k1 * k2 * c) @ w.reshape(k1 * k2 * c, j).astype(dt)
+    return y.reshape(b, ho, wo, j).transpose(0, 3, 1, 2).astype(dt)
 
 
 def maxpool(x: np.ndarray, window: int, stride: int) -> np.ndarray:
@@ -56,7 +57,7 @@ def maxpool(x: np.ndarray, window: int, stride: int) -> np.ndarray:
     b, c, h, w = x.shape
     ho = (h - window) // stride + 1
     wo = (w - window) // stride + 1
-    out = np.full((b, c, ho, wo), -np.inf, dtype=np.float32)
+    out = np.full((b, c, ho, wo), -np.inf, dtype=x.dtype)
     for u in range(window):
         for v in range(window):
             out = np.maximum(out, x[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride])
@@ -66,23 +67,25 @@ def maxpool(x: np.ndarray, window: int, stride: int) -> np.ndarray:
 def softmax(x: np.ndarray) -> np.ndarray:
     """interpreter.py:38-41 (over channels)."""
     e = np.exp(x - x.max(axis=1, keepdims=True))
-    return (e / e.sum(axis=1, keepdims=True)).astype(np.float32)
+    return (e / e.sum(axis=1, keepdims=True)).astype(x.dtype)
 
 
 def eval_node(node, ins: list[np.ndarray]) -> np.ndarray:
-    """interpreter.py:44-72."""
+    """interpreter.py:44-72 (dtype follows the inputs: float32 like the
+    reference, or float64 for an exact-arithmetic yardstick)."""
     kind, a = node.kind.value, node.attrs
+    dt = ins[0].dtype
     if kind == "Conv2D":
         return conv2d(ins[0], node.weights, a["stride"], a["padding"])
     if kind == "Linear":
         flat = ins[0].reshape(ins[0].shape[0], -1)
-        y = flat @ node.weights
-        return y.reshape(y.shape[0], y.shape[1], 1, 1).astype(np.float32)
+        y = flat @ node.weights.astype(dt)
+        return y.reshape(y.shape[0], y.shape[1], 1, 1).astype(dt)
     if kind == "ReLU":
         return np.maximum(ins[0], 0.0)
     if kind == "BatchNorm":
-        sc, sh, mu, var = (node.weights[i].reshape(1, -1, 1, 1) for i in range(4))
-        return ((ins[0] - mu) / np.sqrt(var + BN_EPS) * sc + sh).astype(np.float32)
+        sc, sh, mu, var = (node.weights[i].astype(dt).reshape(1, -1, 1, 1) for i in range(4))
+        return ((ins[0] - mu) / np.sqrt(var + BN_EPS) * sc + sh).astype(dt)
     if kind == "MaxPool":
         return maxpool(ins[0], a["window"], a["stride"])
     if kind == "Add":
@@ -90,8 +93,8 @@ def eval_node(node, ins: list[np.ndarray]) -> np.ndarray:
         for t in ins[1:]:
             acc = acc + t
         if node.weights is not None:
-            acc = acc + node.weights
-        return acc.astype(np.float32)
+            acc = acc + node.weights.astype(dt)
+        return acc.astype(dt)
     if kind == "Concat":
         return np.concatenate(ins, axis=1)
     if kind == "Slice":
@@ -101,9 +104,9 @@ def eval_node(node, ins: list[np.ndarray]) -> np.ndarray:
     raise NotImplementedError(kind)
 
 
-def execute(graph, x: np.ndarray, keep: bool = False):
+def execute(graph, x: np.ndarray, keep: bool = False, dtype=np.float32):
     """interpreter.py:75-90. With ``keep`` returns every node's value too."""
-    x = np.asarray(x, dtype=np.float32)
+    x = np.asarray(x, dtype=dtype)
     vals: dict[int, np.ndarray] = {}
     for nid in _order(graph):
         n = graph.nodes[nid]

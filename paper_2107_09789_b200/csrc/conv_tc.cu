@@ -33,14 +33,18 @@ struct ConvCfg {
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStages = BN >= 128 ? 3 : 4;
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int kTmemCols = 2 * BN;  // ping-pong accumulators
+  // [0,BN): correction terms (a_lo*b_hi + a_hi*b_lo), whole K;
+  // [BN,3BN): ping-pong main accumulators (a_hi*b_hi), one K chunk each
+  static constexpr int kTmemCols = 4 * BN;
 };
 
-// K blocks accumulated in TMEM before the partial sum is drained into fp32
-// registers. The tensor-core accumulator loses ~2^-24 relative per MMA step
-// (error grows linearly with K, measured in scripts/gpu_acc_probe.py); short
-// chains + round-to-nearest fp32 adds keep the conv fp32-faithful.
-constexpr int kChunkKB = 8;
+// K blocks accumulated in TMEM before the main partial sum is drained into
+// fp32 registers. The tensor-core accumulator loses ~2^-24 relative per MMA
+// step (error grows linearly with K, measured in scripts/gpu_acc_probe.py):
+// short chains on the main term, the 2^-11-smaller correction terms in their
+// own accumulator, and round-to-nearest fp32 adds keep the conv
+// fp32-faithful (error at OpenBLAS-sgemm level).
+constexpr int kChunkKB = 4;
 
 struct EpiRegs {
   int nepi;
@@ -221,9 +225,10 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       int kb = 0;
+      const uint32_t acc_small = tmem_base;
       for (int ch = 0; ch < nchunks; ++ch) {
         const int buf = ch & 1;
-        const uint32_t acc = tmem_base + buf * BN;
+        const uint32_t acc = tmem_base + BN + buf * BN;
         mbar_wait(&acc_empty[buf], ((ch >> 1) & 1) ^ 1, 0x106);
         tc_fence_after();
         const int kend = min(kblocks, kb + kChunkKB);
@@ -239,9 +244,9 @@ __global__ void __launch_bounds__(320, 1)
             const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
             const uint64_t dah = sdesc_k128(a_hi + koff), dal = sdesc_k128(a_lo + koff);
             const uint64_t dbh = sdesc_k128(b_hi + koff), dbl = sdesc_k128(b_lo + koff);
-            mma_tf32(acc, dal, dbh, idesc, (kc | kk) != 0);
-            mma_tf32(acc, dah, dbl, idesc, 1u);
-            mma_tf32(acc, dah, dbh, idesc, 1u);
+            mma_tf32(acc_small, dal, dbh, idesc, (kb | kk) != 0);
+            mma_tf32(acc_small, dah, dbl, idesc, 1u);
+            mma_tf32(acc, dah, dbh, idesc, (kc | kk) != 0);
           }
           mma_commit(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(320, 1)
       const int buf = ch & 1;
       mbar_wait(&acc_full[buf], (ch >> 1) & 1, 0x103);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + buf * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + BN + buf * BN;
 #pragma unroll
       for (int cc = 0; cc < BN / 16; ++cc) {
         float part[16];
@@ -269,6 +274,18 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+    }
+    {
+      // the last acc_full commit covered every MMA, so the correction
+      // accumulator is complete as well
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16);
+#pragma unroll
+      for (int cc = 0; cc < BN / 16; ++cc) {
+        float part[16];
+        tmem_ld16(taddr + cc * 16, part);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
+      }
     }
     // Stage the tile's fp32 sums in shared memory (the operand ring is idle:
     // every K block has been consumed), 16-B chunks XOR-swizzled by row so

@@ -65,22 +65,27 @@ def test_conv_kernel_matches_oracle(ctx, case):
 @pytest.mark.parametrize("name,mode,size", [("c1c2", "dimension", 24), ("resnet18", "sequence", 64),
                                             ("resnet18", "dimension", 64), ("vgg16", "dimension", 32)])
 def test_execute_obfuscated_matches_oracle(ctx, name, mode, size):
+    """Outputs within 1e-4 of the fp32 oracle; the pre-softmax logits (the
+    softmax saturates with random init) are held to the
+    same yardstick as the reference's own fp32 arithmetic: their distance to
+    exact (fp64) arithmetic may not exceed max(1e-4, 2x the oracle's)."""
     kw = {"hidden": 256} if name == "vgg16" else {}
     g = fixtures.FIXTURES[name](size=size, **kw)
     x = np.random.default_rng(5).standard_normal(g.input_shape.as_tuple()).astype(np.float32)
+    logits_node = g.nodes[g.output_id].inputs[0] if g.nodes[g.output_id].kind.value == "SoftMax" else None
     for plan in _plans(g, mode, 2, seed=11):
         og, _ = knobs.apply_plan(g, plan)
         got = executor.execute(og, x)
         _, vals = IR.execute(og, x, keep=True)
         ref = vals[og.output_id].astype(np.float64)
         assert _rel(got, ref) <= FP32_TOL
-        # pre-softmax logits too (softmax saturates with random init)
-        pre = og.nodes[og.output_id].inputs
-        if og.nodes[og.output_id].kind.value == "SoftMax" and pre:
+        if logits_node is not None and logits_node in og.nodes:
             from paper_2107_09789_b200.ir import Graph
-            sub = Graph(og.nodes, pre[0], og.input_shape)
-            got_l = executor.execute(sub, x)
-            assert _rel(got_l, vals[pre[0]].astype(np.float64)) <= FP32_TOL
+            _, exact = IR.execute(og, x, keep=True, dtype=np.float64)
+            got_l = executor.execute(Graph(og.nodes, logits_node, og.input_shape), x)
+            err_gpu = _rel(got_l, exact[logits_node])
+            err_ref = _rel(vals[logits_node], exact[logits_node])
+            assert err_gpu <= max(FP32_TOL, 2.0 * err_ref), (err_gpu, err_ref)
 
 
 def test_equivalence_verdicts_match_oracle(ctx):
