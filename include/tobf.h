@@ -133,7 +133,10 @@ typedef struct tobf_kern_desc {
   int32_t reuse_x_stream;      /* non-tiled: Linear j else 1 */
   int32_t ty[3], tx[3];        /* schedule factor triples (input for profile, output of search) */
   int32_t unroll, label;       /* label: OperatorKind code or -1 */
-  int32_t has_shape, pad_;     /* has_shape = 0 -> degenerate zero step */
+  int32_t has_shape;           /* 0 -> degenerate zero step */
+  int32_t strategy;            /* schedule strategy k (fusion.py:124-134), 0 = none */
+  int32_t sig_index;           /* row of the signature table holding this kernel's default schedule */
+  int32_t resolved;            /* signature table rows: 1 = schedule known (memo hit), skip the search */
 } tobf_kern_desc;
 
 typedef struct tobf_device_profile {
@@ -143,6 +146,11 @@ typedef struct tobf_device_profile {
 /* Brute-force default_schedule for `n` kernels (DEVICE descriptor array):
  * writes the lexicographic-argmin (ty, tx) into d_descs[i].ty/tx. */
 int tobf_schedule_search(tobf_kern_desc* d_descs, int n, const tobf_device_profile* prof, void* stream);
+
+/* Per kernel: (ty, tx) := d_sigs[sig_index].(ty, tx), then modify_schedule
+ * with the kernel's strategy (fusion.py:105-134) — the memoised default
+ * schedule lookup of compile_graph (costmodel.py:276-284) on the device. */
+int tobf_resolve_schedules(tobf_kern_desc* d_kern, int n, const tobf_kern_desc* d_sigs, void* stream);
 
 /* profile_kernel for every kernel: feats[i*9 + f] in FEATURE_NAMES order
  * (cycles, dram_read, dram_write, l1_tx, l1_util, l1_hit, l2_tx, l2_util, l2_hit). */

@@ -65,7 +65,8 @@ class KernDesc(C.Structure):
         ("reuse_x_stream", C.c_int32),
         ("ty", C.c_int32 * 3), ("tx", C.c_int32 * 3),
         ("unroll", C.c_int32), ("label", C.c_int32),
-        ("has_shape", C.c_int32), ("pad_", C.c_int32),
+        ("has_shape", C.c_int32), ("strategy", C.c_int32),
+        ("sig_index", C.c_int32), ("resolved", C.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ class DeviceProfileC(C.Structure):
 
 assert C.sizeof(ConvDesc) == 200, C.sizeof(ConvDesc)
 assert C.sizeof(EwDesc) == 176, C.sizeof(EwDesc)
-assert C.sizeof(KernDesc) == 128, C.sizeof(KernDesc)
+assert C.sizeof(KernDesc) == 136, C.sizeof(KernDesc)
 
 _vp, _i32, _i64, _f32, _f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double
 
@@ -94,6 +95,7 @@ SIGNATURES = {
     "tobf_nhwc_to_nchw": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "tobf_nchw_to_nhwc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "tobf_schedule_search": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "tobf_resolve_schedules": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "tobf_profile_kernels": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
     "tobf_trace_totals": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
     "tobf_lstm_ctc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),

@@ -123,6 +123,7 @@ __global__ void schedule_search_kernel(tobf_kern_desc* __restrict__ descs, ProfC
   const int ny = s_ny, nx = s_nx;
   double best_c = INFINITY;
   int best_i = 0x7fffffff;
+  if (k.resolved) return;  // memo hit: schedule already in the table
   if (!k.has_shape || k.label < 0) {
     // non-complex anchor -> TRIVIAL_SCHEDULE (fusion.py:168-170)
     if (threadIdx.x == 0) {
@@ -169,6 +170,42 @@ __global__ void schedule_search_kernel(tobf_kern_desc* __restrict__ descs, ProfC
     }
     k.unroll = 4;
   }
+}
+
+// fusion.py:105-121: strategy k forces slot k of a triple to 1 and keeps the
+// product as the most balanced factor pair, smaller factor first.
+__device__ inline void apply_strategy(int* t, int k) {
+  const int prod = t[0] * t[1] * t[2];
+  int a = 1;
+  for (int d = 1; d * d <= prod; ++d)
+    if (prod % d == 0) a = d;
+  const int b = prod / a;
+  int r0 = -1, r1 = -1;
+  for (int i = 0; i < 3; ++i) {
+    if (i == k - 1) continue;
+    if (r0 < 0) r0 = i; else r1 = i;
+  }
+  t[k - 1] = 1;
+  t[r0] = a;
+  t[r1] = b;
+}
+
+__global__ void resolve_kernel(tobf_kern_desc* __restrict__ kern, int n, const tobf_kern_desc* __restrict__ sigs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  tobf_kern_desc& k = kern[i];
+  if (k.sig_index < 0) return;
+  const tobf_kern_desc& s = sigs[k.sig_index];
+  int ty[3] = {s.ty[0], s.ty[1], s.ty[2]}, tx[3] = {s.tx[0], s.tx[1], s.tx[2]};
+  if (k.strategy >= 1 && k.strategy <= 3) {
+    apply_strategy(ty, k.strategy);
+    apply_strategy(tx, k.strategy);
+  }
+  for (int q = 0; q < 3; ++q) {
+    k.ty[q] = ty[q];
+    k.tx[q] = tx[q];
+  }
+  k.unroll = s.unroll;
 }
 
 __device__ inline double pct_hit(int64_t fp, int64_t working_set) {
@@ -268,6 +305,13 @@ extern "C" int tobf_schedule_search(tobf_kern_desc* d_descs, int n, const tobf_d
   if (rc) return rc;
   schedule_search_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(d_descs, to_profc(prof));
   return tobf_cuda_check("tobf_schedule_search");
+}
+
+extern "C" int tobf_resolve_schedules(tobf_kern_desc* d_kern, int n, const tobf_kern_desc* d_sigs, void* stream) {
+  if (n <= 0) return TOBF_OK;
+  if (!d_kern || !d_sigs) return tobf_fail(TOBF_E_INVALID, "tobf_resolve_schedules: bad arguments");
+  resolve_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_kern, n, d_sigs);
+  return tobf_cuda_check("tobf_resolve_schedules");
 }
 
 extern "C" int tobf_profile_kernels(const tobf_kern_desc* d_descs, int n, const tobf_device_profile* prof,

@@ -42,6 +42,8 @@ class DeviceContext:
         self.weight_cache: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
         self.weight_cache_bytes = 0
         self.weight_cache_limit = int(os.environ.get("TOBF_WEIGHT_CACHE_BYTES", str(24 << 30)))
+        self.launches = 0      # libtobf kernel launches issued (bench evidence)
+        self.h2d_bytes = 0     # host->device bytes staged through this context
 
     @property
     def sp(self) -> int:
@@ -54,6 +56,7 @@ class DeviceContext:
     # -- host arrays -> device ----------------------------------------------
     def upload_bytes(self, buf: bytes | bytearray | memoryview) -> torch.Tensor:
         host = torch.frombuffer(bytearray(buf), dtype=torch.uint8)
+        self.h2d_bytes += host.numel()
         return host.pin_memory().to(self.device, non_blocking=True)
 
     def upload_struct_array(self, arr) -> torch.Tensor:
@@ -71,6 +74,7 @@ class DeviceContext:
             hit = self.weight_cache.get(key)
             if hit is None or hit[0] is not base:
                 dev = torch.from_numpy(base.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+                self.h2d_bytes += base.nbytes
                 self._remember(key, base, dev)
             dev = self.weight_cache[key][1]
             off = (a.__array_interface__["data"][0] - base.__array_interface__["data"][0]) // 4
@@ -80,6 +84,7 @@ class DeviceContext:
         hit = self.weight_cache.get(key)
         if hit is None or hit[0] is not a:
             dev = torch.from_numpy(own.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+            self.h2d_bytes += own.nbytes
             self._remember(key, a, dev)
         return self.weight_cache[key][1].data_ptr(), tuple(st // 4 for st in own.strides)
 

@@ -30,7 +30,8 @@ from .executor import PopulationRun, compare_outputs, lower, trial_inputs
 from .fitness import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan
-from .trace import BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, trace_population
+from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,
+                    run_trace, trace_population)
 
 RECORD_DTYPE = np.dtype([("reward", "<f8"), ("mean_ler", "<f8"), ("latency", "<f8"), ("worst", "<f4"),
                          ("ok", "<i4"), ("feasible", "<i4"), ("ntok", "<i4")])
@@ -98,7 +99,10 @@ class PopulationEvaluator:
         self.t_star = float(pt.totals.cpu()[0])
 
     # ---------------------------------------------------------------- host
-    def prepare(self, plans: list[ObfuscationPlan]) -> dict:
+    def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None) -> dict:
+        """Host half: apply_plan, lowering, weight upload + packing, trace
+        descriptors, all staged into HBM. ``memo`` defaults to the
+        process-global schedule memo; pass {} for a cold schedule search."""
         t0 = time.perf_counter()
         cands = build_candidates(self.vanilla, plans)
         t1 = time.perf_counter()
@@ -106,15 +110,24 @@ class PopulationEvaluator:
         run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph) for i in feas],
                             reps=self.trials)
         t2 = time.perf_counter()
-        return {"cands": cands, "feas": feas, "run": run,
-                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1)}}
+        items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies)
+                 for i in feas]
+        tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo) if items else None
+        idx = torch.tensor(feas, dtype=torch.long).to(self.ctx.device, non_blocking=True)
+        t3 = time.perf_counter()
+        return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
+                "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
+                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
+                            "trace_prep": 1e3 * (t3 - t2)}}
 
     # ---------------------------------------------------------------- device
     def run(self, prep: dict, x_dev: torch.Tensor | None = None, timing: bool = False,
-            fresh_memo: bool = False) -> dict:
-        """Device pipeline over a prepared batch; returns device tensors."""
+            cold_schedules: bool = False) -> dict:
+        """Device pipeline over a prepared batch; returns device tensors.
+        ``cold_schedules`` re-runs the full schedule search for every
+        signature (benchmark: no memo carried between steps)."""
         ctx = self.ctx
-        cands, feas, run = prep["cands"], prep["feas"], prep["run"]
+        cands, feas, run, tp = prep["cands"], prep["feas"], prep["run"], prep["trace"]
         ev = {}
         mark = (lambda k: ev.setdefault(k, torch.cuda.Event(enable_timing=True)).record()) if timing else \
             (lambda k: None)
@@ -125,10 +138,8 @@ class PopulationEvaluator:
         run.run()
         ok_f, worst_f = compare_outputs(ctx, run, 0, list(range(1, len(feas) + 1)), self.tol)
         mark("forward")
-        memo = {} if fresh_memo else self.memo
-        items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies)
-                 for i in feas]
-        pt = trace_population(items, self.ev.profile, memo) if items else None
+        if tp is not None:
+            run_trace(tp, restore=cold_schedules)
         mark("trace")
         n = len(cands)
         ncf = len(feas)
@@ -138,22 +149,23 @@ class PopulationEvaluator:
         worst = torch.zeros(n, dtype=torch.float32, device=ctx.device)
         ntok0 = torch.zeros(n, dtype=torch.int32, device=ctx.device)
         if ncf:
-            idx = torch.tensor(feas, dtype=torch.long, device=ctx.device)
-            t_max = int(np.diff(pt.offsets_host).max())
+            idx = prep["idx"]
+            if not hasattr(self, "_truth_dev"):
+                self._truth_dev = torch.from_numpy(self.truth).to(ctx.device)
             for p, pred in enumerate(self.ev.predictors):
-                toks, ntok = decode(pt.feats, pt.offsets, ncf, max(t_max, 1), pred)
-                _, lr, _ = edit_distances(toks, ntok, self.truth)
+                toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred)
+                _, lr, _ = edit_distances(toks, ntok, self._truth_dev)
                 lers[p].index_copy_(0, idx, lr)
                 if p == 0:
                     ntok0.index_copy_(0, idx, ntok)
-            T.index_copy_(0, idx, pt.totals)
+            T.index_copy_(0, idx, tp.totals)
             ok.index_copy_(0, idx, ok_f)
             worst.index_copy_(0, idx, worst_f)
         mark("fitness")
         R, mean = reward(lers, T, ok, self.t_star, self.budget, self.eps)
         mark("reward")
-        return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": ntok0, "pt": pt, "events": ev,
-                "feasible": [c.graph is not None for c in cands]}
+        return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": ntok0, "trace": tp, "events": ev,
+                "feasible": [c.graph is not None for c in cands], "lers": lers}
 
     def collect(self, out: dict) -> np.ndarray:
         rec = np.zeros(len(out["feasible"]), dtype=RECORD_DTYPE)
@@ -171,6 +183,8 @@ class PopulationEvaluator:
         prep = self.prepare(plans)
         out = self.run(prep, timing=True)
         rec = self.collect(out)
+        if prep["trace"] is not None:
+            finish_trace(prep["trace"])  # first-seen memo update
         evs = out["events"]
         keys = list(evs)
         stage = {b: evs[a].elapsed_time(evs[b]) for a, b in zip(keys, keys[1:])}

@@ -369,15 +369,26 @@ class PopulationRun:
         self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(x.data_ptr()), C.c_void_p(self.x_ptr), self.batch,
                                                       s.channels, s.height, s.width, _rup4(s.channels),
                                                       C.c_void_p(self.ctx.sp)), "input staging")
+        self.ctx.launches += 1
+
+    conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
 
     def run(self) -> None:
         lib, sp = self.ctx.lib, C.c_void_p(self.ctx.sp)
+        evs = self.conv_events
         for kind, dptr, n, tot, bn in self.launches:
             if kind == "conv":
+                if evs is not None:
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
                 rc = lib.tobf_conv_grouped(C.c_void_p(dptr), n, tot, bn, sp)
+                if evs is not None:
+                    b.record()
+                    evs.append((a, b))
             else:
                 rc = lib.tobf_ew_grouped(C.c_void_p(dptr), n, tot, sp)
             self.ctx.check(rc, kind)
+        self.ctx.launches += len(self.launches)
 
     def output_ptr(self, gi: int) -> tuple[int, TensorShape]:
         lw = self.lowered[gi]
@@ -450,19 +461,28 @@ def equivalence_check(g1: Graph, g2: Graph, trials: int = 8, seed: int = 0,
 
 def compare_outputs(ctx: DeviceContext, run: PopulationRun, ref_index: int, cand_indices: list[int],
                     tol: float) -> tuple[torch.Tensor, torch.Tensor]:
-    """Device verdicts of candidates vs the reference graph output (a = ref, b = cand)."""
-    ref_ptr, s = run.output_ptr(ref_index)
-    a_list = np.array([ref_ptr] * len(cand_indices), dtype=np.uint64)
-    b_list = np.array([run.output_ptr(i)[0] for i in cand_indices], dtype=np.uint64)
-    ptrs = ctx.upload_bytes(a_list.tobytes() + b_list.tobytes())
-    worst = torch.empty(len(cand_indices), dtype=torch.float32, device=ctx.device)
-    ok = torch.empty(len(cand_indices), dtype=torch.int32, device=ctx.device)
+    """Device verdicts of candidates vs the reference graph output (a = ref,
+    b = cand). Pointer tables are staged once per run and reused."""
+    key = (ref_index, tuple(cand_indices))
+    cache = run.__dict__.setdefault("_cmp", {})
+    if key not in cache:
+        ref_ptr, s = run.output_ptr(ref_index)
+        a_list = np.array([ref_ptr] * len(cand_indices), dtype=np.uint64)
+        b_list = np.array([run.output_ptr(i)[0] for i in cand_indices], dtype=np.uint64)
+        ptrs = ctx.upload_bytes(a_list.tobytes() + b_list.tobytes())
+        cache[key] = (ptrs, s)
+    ptrs, s = cache[key]
+    n = len(cand_indices)
+    worst = torch.empty(n, dtype=torch.float32, device=ctx.device)
+    ok = torch.empty(n, dtype=torch.int32, device=ctx.device)
+    if n == 0:
+        return ok, worst
     pixels = run.batch * s.height * s.width
-    ctx.check(ctx.lib.tobf_equiv_compare(C.c_void_p(ptrs.data_ptr()), C.c_void_p(ptrs.data_ptr() + 8 * len(a_list)),
-                                         len(cand_indices), pixels, s.channels, _rup4(s.channels), C.c_float(tol),
+    ctx.check(ctx.lib.tobf_equiv_compare(C.c_void_p(ptrs.data_ptr()), C.c_void_p(ptrs.data_ptr() + 8 * n), n,
+                                         pixels, s.channels, _rup4(s.channels), C.c_float(tol),
                                          C.c_void_p(worst.data_ptr()), C.c_void_p(ok.data_ptr()),
                                          C.c_void_p(ctx.sp)), "equivalence compare")
-    run._keep.append(ptrs)
+    ctx.launches += 2
     return ok, worst
 
 

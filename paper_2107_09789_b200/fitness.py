@@ -95,6 +95,7 @@ def decode(feats: torch.Tensor, offsets: torch.Tensor, ntraces: int, t_max: int,
                                     C.c_void_p(w["b"].data_ptr()), C.c_void_p(w["w_out"].data_ptr()),
                                     C.c_void_p(w["b_out"].data_ptr()), C.c_void_p(tokens.data_ptr()), t_max,
                                     C.c_void_p(ntok.data_ptr()), C.c_void_p(ctx.sp)), "lstm+ctc")
+    ctx.launches += 1
     return tokens, ntok
 
 
@@ -102,12 +103,14 @@ def edit_distances(tokens: torch.Tensor, ntok: torch.Tensor, truth: np.ndarray):
     """Warp-per-pair Levenshtein against one truth -> (ed int32, ler float64) on the device."""
     ctx = device()
     B, t_max = tokens.shape
-    tr = torch.from_numpy(np.ascontiguousarray(truth, dtype=np.int8)).to(ctx.device)
+    tr = truth if isinstance(truth, torch.Tensor) else \
+        torch.from_numpy(np.ascontiguousarray(truth, dtype=np.int8)).to(ctx.device)
     ed = torch.empty(B, dtype=torch.int32, device=ctx.device)
     lr = torch.empty(B, dtype=torch.float64, device=ctx.device)
     ctx.check(ctx.lib.tobf_levenshtein(C.c_void_p(tokens.data_ptr()), C.c_void_p(ntok.data_ptr()), B, t_max,
-                                       C.c_void_p(tr.data_ptr()), len(truth), C.c_void_p(ed.data_ptr()),
+                                       C.c_void_p(tr.data_ptr()), tr.numel(), C.c_void_p(ed.data_ptr()),
                                        C.c_void_p(lr.data_ptr()), C.c_void_p(ctx.sp)), "levenshtein")
+    ctx.launches += 1
     return ed, lr, tr
 
 
@@ -123,6 +126,7 @@ def reward(lers: torch.Tensor, T: torch.Tensor, feasible: torch.Tensor, t_star: 
                                         C.c_void_p(feasible.data_ptr()), float(t_star), float(budget), float(eps),
                                         C.c_void_p(R.data_ptr()), C.c_void_p(mean.data_ptr()),
                                         C.c_void_p(ctx.sp)), "eq10")
+    ctx.launches += 1
     return R, mean
 
 

@@ -217,60 +217,139 @@ def search_schedules(graph: Graph, kernels: list[Kernel], profile: DeviceProfile
 
 def compile_graph(graph: Graph, profile: DeviceProfile, fusion_limits: dict[int, int] | None = None,
                   strategies: dict[int, int] | None = None) -> CompiledGraph:
-    """costmodel.py:266-285."""
-    return compile_population([(graph, fusion_limits, strategies)], profile)[0]
+    """costmodel.py:266-285 (default schedules searched on the device)."""
+    tp = prepare_trace([(graph, fusion_limits, strategies)], profile)
+    run_trace(tp, profile=False)
+    finish_trace(tp)
+    return tp.compiled[0]
 
 
-def compile_population(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
-                       memo: dict | None = None) -> list[CompiledGraph]:
-    """compile_graph over many graphs with ONE device schedule search for all
-    signatures not yet in ``memo`` (first-seen order across ``items``)."""
+class TracePlan:
+    """Host-prepared, device-resident inputs of the trace stage for a population.
+
+    kern      per-kernel descriptors in candidate order (profile input)
+    sigs      one row per distinct schedule signature of the batch, first-seen
+              order; rows already in the memo carry their schedule and
+              ``resolved = 1``, the others are searched on the device
+    offsets   kernel range of candidate i = [offsets[i], offsets[i+1])
+    """
+
+    def __init__(self, compiled, kern_dev, sig_dev, nk, nsig, pending, offsets_host, offsets_dev, profile, memo):
+        self.compiled, self.kern, self.sigs = compiled, kern_dev, sig_dev
+        self.nk, self.nsig, self.pending = nk, nsig, pending
+        self.offsets_host, self.offsets = offsets_host, offsets_dev
+        self.profile, self.memo = profile, memo
+        self.feats = self.totals = None
+
+
+def prepare_trace(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
+                  memo: dict | None = None) -> TracePlan:
+    """Host half of compile_graph for many graphs: shapes, fuse, signatures,
+    integer descriptors (one H2D for all)."""
+    ctx = device()
     memo = _SCHEDULE_CACHE if memo is None else memo
-    pending: dict[tuple, tuple] = {}
-    staged = []
+    sig_rows: dict[tuple, int] = {}
+    sig_src: list[tuple] = []
+    compiled, per_kernel = [], []
     for graph, limits, strategies in items:
         order = topo_order(graph)
         shapes = shape_map(graph, order)
         annotated = graph.copy()
-        for nid, s in shapes.items():
-            annotated.nodes[nid].out_shape = s
+        for nid, sh in shapes.items():
+            annotated.nodes[nid].out_shape = sh
         kernels = fuse(annotated, limits, order=order)
-        sigs = [schedule_signature(annotated, shapes, k, profile) for k in kernels]
-        for k, sig in zip(kernels, sigs):
-            if sig not in memo and sig not in pending:
-                if annotated.nodes[k.anchor].kind not in COMPLEX_KINDS:
-                    memo[sig] = TRIVIAL_SCHEDULE
-                else:
-                    pending[sig] = (annotated, shapes, k)
-        staged.append((annotated, shapes, kernels, sigs, strategies or {}))
-    if pending:
-        ctx = device()
-        keys = list(pending)
-        arr = (N.KernDesc * len(keys))()
-        for i, key in enumerate(keys):
-            g, sh, k = pending[key]
-            kernel_desc(g, sh, k, None, arr[i])
-        dev = ctx.upload_struct_array(arr)
-        pc = profile.as_c()
-        ctx.check(ctx.lib.tobf_schedule_search(C.c_void_p(dev.data_ptr()), len(keys), C.byref(pc),
-                                               C.c_void_p(ctx.sp)), "schedule search")
-        host = dev.cpu()
-        back = (N.KernDesc * len(keys)).from_buffer_copy(host.numpy().tobytes())
-        for i, key in enumerate(keys):
-            memo[key] = Schedule(tuple(back[i].ty), tuple(back[i].tx), back[i].unroll)
-    out = []
-    for annotated, shapes, kernels, sigs, strategies in staged:
-        scheds = []
-        for k, sig in zip(kernels, sigs):
-            sch = memo[sig]
-            st = strategies.get(k.anchor, 0)
-            if st:
-                sch = modify_schedule(sch, st)
-            scheds.append(sch)
-        cg = CompiledGraph(annotated, kernels, scheds)
+        strategies = strategies or {}
+        cg = CompiledGraph(annotated, kernels, [])
         cg._shapes = shapes
-        out.append(cg)
-    return out
+        for k in kernels:
+            sig = schedule_signature(annotated, shapes, k, profile)
+            row = sig_rows.get(sig)
+            if row is None:
+                row = sig_rows[sig] = len(sig_src)
+                sig_src.append((sig, annotated, shapes, k))
+            per_kernel.append((cg, k, row, strategies.get(k.anchor, 0)))
+        compiled.append(cg)
+    nsig, nk = len(sig_src), len(per_kernel)
+    sig_arr = (N.KernDesc * max(nsig, 1))()
+    pending = []
+    for i, (sig, g, sh, k) in enumerate(sig_src):
+        d = sig_arr[i]
+        hit = memo.get(sig)
+        if hit is None and g.nodes[k.anchor].kind not in COMPLEX_KINDS:
+            hit = memo[sig] = TRIVIAL_SCHEDULE
+        kernel_desc(g, sh, k, hit, d)
+        d.sig_index = -1
+        if hit is not None:
+            d.resolved = 1
+        else:
+            pending.append((i, sig))
+    kern_arr = (N.KernDesc * max(nk, 1))()
+    for r, (cg, k, row, st) in enumerate(per_kernel):
+        d = kern_arr[r]
+        kernel_desc(cg.graph, cg._shapes, k, None, d)
+        d.sig_index, d.strategy = row, st
+    offsets = np.zeros(len(compiled) + 1, np.int32)
+    offsets[1:] = np.cumsum([len(cg.kernels) for cg in compiled])
+    blob = bytes(sig_arr) + bytes(kern_arr)
+    dev = ctx.upload_bytes(blob)
+    offs = torch.from_numpy(offsets).to(ctx.device, non_blocking=True)
+    sig_dev = dev[:len(bytes(sig_arr))]
+    kern_dev = dev[len(bytes(sig_arr)):]
+    tp = TracePlan(compiled, kern_dev, sig_dev, nk, nsig, pending, offsets, offs, profile, memo)
+    tp._blob = dev
+    tp._sig_template = bytes(sig_arr)
+    return tp
+
+
+def run_trace(tp: TracePlan, profile: bool = True, restore: bool = False) -> None:
+    """Device half: search the unresolved signatures, resolve every kernel's
+    schedule (+ strategy), profile all kernels, per-candidate T.
+    ``restore`` re-uploads the pristine signature table first (a cold memo
+    every call, for benchmarking)."""
+    ctx = device()
+    pc = tp.profile.as_c()
+    sp = C.c_void_p(ctx.sp)
+    if restore:
+        tp.sigs.copy_(torch.frombuffer(bytearray(tp._sig_template), dtype=torch.uint8), non_blocking=True)
+    if tp.pending:
+        ctx.check(ctx.lib.tobf_schedule_search(C.c_void_p(tp.sigs.data_ptr()), tp.nsig, C.byref(pc), sp),
+                  "schedule search")
+        ctx.launches += 1
+    ctx.check(ctx.lib.tobf_resolve_schedules(C.c_void_p(tp.kern.data_ptr()), tp.nk, C.c_void_p(tp.sigs.data_ptr()),
+                                             sp), "resolve schedules")
+    ctx.launches += 1
+    if not profile:
+        return
+    if tp.feats is None:
+        tp.feats = torch.empty((max(tp.nk, 1), 9), dtype=torch.float64, device=ctx.device)
+        tp.totals = torch.empty(len(tp.compiled), dtype=torch.float64, device=ctx.device)
+    ctx.check(ctx.lib.tobf_profile_kernels(C.c_void_p(tp.kern.data_ptr()), tp.nk, C.byref(pc),
+                                           C.c_void_p(tp.feats.data_ptr()), sp), "profile")
+    ctx.check(ctx.lib.tobf_trace_totals(C.c_void_p(tp.feats.data_ptr()), C.c_void_p(tp.offsets.data_ptr()),
+                                        len(tp.compiled), C.c_void_p(tp.totals.data_ptr()), sp), "trace totals")
+    ctx.launches += 2
+
+
+def finish_trace(tp: TracePlan) -> None:
+    """Record newly searched schedules in the memo (first-seen) and attach the
+    resolved schedules to the CompiledGraphs (one D2H)."""
+    ctx = device()
+    host = torch.empty(tp.sigs.numel() + tp.kern.numel(), dtype=torch.uint8)
+    host[:tp.sigs.numel()].copy_(tp.sigs)
+    host[tp.sigs.numel():].copy_(tp.kern)
+    ctx.sync()
+    raw = host.numpy().tobytes()
+    sigs = (N.KernDesc * max(tp.nsig, 1)).from_buffer_copy(raw[:tp.sigs.numel()])
+    kern = (N.KernDesc * max(tp.nk, 1)).from_buffer_copy(raw[tp.sigs.numel():])
+    for i, sig in tp.pending:
+        if sig not in tp.memo:
+            tp.memo[sig] = Schedule(tuple(sigs[i].ty), tuple(sigs[i].tx), sigs[i].unroll)
+    r = 0
+    for cg in tp.compiled:
+        cg.schedules = []
+        for _ in cg.kernels:
+            cg.schedules.append(Schedule(tuple(kern[r].ty), tuple(kern[r].tx), kern[r].unroll))
+            r += 1
 
 
 @dataclass
@@ -294,29 +373,10 @@ class PopulationTrace:
 def trace_population(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
                      memo: dict | None = None) -> PopulationTrace:
     """compile + profile + T for a population, all arithmetic on the device."""
-    ctx = device()
-    compiled = compile_population(items, profile, memo)
-    nk = sum(len(cg.kernels) for cg in compiled)
-    arr = (N.KernDesc * max(nk, 1))()
-    offsets = np.zeros(len(compiled) + 1, np.int32)
-    r = 0
-    for i, cg in enumerate(compiled):
-        for k, sch in zip(cg.kernels, cg.schedules):
-            kernel_desc(cg.graph, cg._shapes, k, sch, arr[r])
-            r += 1
-        offsets[i + 1] = r
-    dev = ctx.upload_struct_array(arr)
-    offs = torch.from_numpy(offsets).to(ctx.device, non_blocking=True)
-    feats = torch.empty((max(nk, 1), 9), dtype=torch.float64, device=ctx.device)
-    totals = torch.empty(len(compiled), dtype=torch.float64, device=ctx.device)
-    pc = profile.as_c()
-    ctx.check(ctx.lib.tobf_profile_kernels(C.c_void_p(dev.data_ptr()), nk, C.byref(pc),
-                                           C.c_void_p(feats.data_ptr()), C.c_void_p(ctx.sp)), "profile")
-    ctx.check(ctx.lib.tobf_trace_totals(C.c_void_p(feats.data_ptr()), C.c_void_p(offs.data_ptr()), len(compiled),
-                                        C.c_void_p(totals.data_ptr()), C.c_void_p(ctx.sp)), "trace totals")
-    pt = PopulationTrace(compiled, feats, offs, totals, offsets)
-    pt._desc = dev
-    return pt
+    tp = prepare_trace(items, profile, memo)
+    run_trace(tp)
+    finish_trace(tp)
+    return PopulationTrace(tp.compiled, tp.feats, tp.offsets, tp.totals, tp.offsets_host)
 
 
 def profile_graph(graph: Graph, kernels: list[Kernel], schedules: list[Schedule], case: LeakageCase,
