@@ -243,14 +243,19 @@ class TracePlan:
 
 
 def prepare_trace(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
-                  memo: dict | None = None) -> TracePlan:
+                  memo: dict | None = None, exchange=None) -> TracePlan:
     """Host half of compile_graph for many graphs: shapes, fuse, signatures,
-    integer descriptors (one H2D for all)."""
+    integer descriptors (one H2D for all).
+
+    ``exchange`` (dist.exchange_signatures) merges this rank's unmemoised
+    signatures with every other rank's in global first-seen order; the
+    resulting table is searched identically on every rank, so all memos stay
+    equal and every schedule is the one a single process would pick."""
     ctx = device()
     memo = _SCHEDULE_CACHE if memo is None else memo
-    sig_rows: dict[tuple, int] = {}
-    sig_src: list[tuple] = []
     compiled, per_kernel = [], []
+    hits: dict[tuple, Schedule] = {}
+    local_pending: dict[tuple, bytes] = {}
     for graph, limits, strategies in items:
         order = topo_order(graph)
         shapes = shape_map(graph, order)
@@ -263,41 +268,49 @@ def prepare_trace(items: list[tuple[Graph, dict | None, dict | None]], profile: 
         cg._shapes = shapes
         for k in kernels:
             sig = schedule_signature(annotated, shapes, k, profile)
-            row = sig_rows.get(sig)
-            if row is None:
-                row = sig_rows[sig] = len(sig_src)
-                sig_src.append((sig, annotated, shapes, k))
-            per_kernel.append((cg, k, row, strategies.get(k.anchor, 0)))
+            if sig not in hits and sig not in local_pending:
+                hit = memo.get(sig)
+                if hit is None and annotated.nodes[k.anchor].kind not in COMPLEX_KINDS:
+                    hit = memo[sig] = TRIVIAL_SCHEDULE
+                if hit is not None:
+                    hits[sig] = hit
+                else:
+                    d = N.KernDesc()
+                    kernel_desc(annotated, shapes, k, None, d)
+                    d.sig_index = -1
+                    local_pending[sig] = bytes(d)
+            per_kernel.append((cg, k, sig, strategies.get(k.anchor, 0)))
         compiled.append(cg)
-    nsig, nk = len(sig_src), len(per_kernel)
-    sig_arr = (N.KernDesc * max(nsig, 1))()
+    pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
+    rows: dict[tuple, int] = {}
+    sig_bytes = []
+    for sig, sch in hits.items():
+        d = N.KernDesc()
+        d.has_shape, d.resolved, d.sig_index = 1, 1, -1
+        d.ty[:], d.tx[:], d.unroll = list(sch.tile_y), list(sch.tile_x), sch.unroll
+        rows[sig] = len(sig_bytes)
+        sig_bytes.append(bytes(d))
     pending = []
-    for i, (sig, g, sh, k) in enumerate(sig_src):
-        d = sig_arr[i]
-        hit = memo.get(sig)
-        if hit is None and g.nodes[k.anchor].kind not in COMPLEX_KINDS:
-            hit = memo[sig] = TRIVIAL_SCHEDULE
-        kernel_desc(g, sh, k, hit, d)
-        d.sig_index = -1
-        if hit is not None:
-            d.resolved = 1
-        else:
-            pending.append((i, sig))
+    for sig, blob in pending_all.items():
+        rows[sig] = len(sig_bytes)
+        pending.append((rows[sig], sig))
+        sig_bytes.append(blob)
+    nsig, nk = len(sig_bytes), len(per_kernel)
     kern_arr = (N.KernDesc * max(nk, 1))()
-    for r, (cg, k, row, st) in enumerate(per_kernel):
+    for r, (cg, k, sig, st) in enumerate(per_kernel):
         d = kern_arr[r]
         kernel_desc(cg.graph, cg._shapes, k, None, d)
-        d.sig_index, d.strategy = row, st
+        d.sig_index, d.strategy = rows[sig], st
     offsets = np.zeros(len(compiled) + 1, np.int32)
     offsets[1:] = np.cumsum([len(cg.kernels) for cg in compiled])
-    blob = bytes(sig_arr) + bytes(kern_arr)
+    sig_blob = b"".join(sig_bytes) if sig_bytes else bytes(N.KernDesc())
+    blob = sig_blob + bytes(kern_arr)
     dev = ctx.upload_bytes(blob)
     offs = torch.from_numpy(offsets).to(ctx.device, non_blocking=True)
-    sig_dev = dev[:len(bytes(sig_arr))]
-    kern_dev = dev[len(bytes(sig_arr)):]
-    tp = TracePlan(compiled, kern_dev, sig_dev, nk, nsig, pending, offsets, offs, profile, memo)
+    tp = TracePlan(compiled, dev[len(sig_blob):], dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile,
+                   memo)
     tp._blob = dev
-    tp._sig_template = bytes(sig_arr)
+    tp._sig_template = sig_blob
     return tp
 
 
