@@ -196,7 +196,9 @@ def main_ours(args):
     steps_total = args.warmup + args.steps
     plans_all = population_plans(vanilla, P * world, args.seed)
     mine = plans_all[rank * P:(rank + 1) * P]
-    pe = PopulationEvaluator(vanilla, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed, memo={})
+    from paper_2107_09789_b200 import dist as tdist
+    pe = PopulationEvaluator(vanilla, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed, memo={},
+                             exchange=tdist.exchange_signatures if world > 1 else None)
 
     def barrier():
         if world > 1:

@@ -96,8 +96,12 @@ class DeviceContext:
         self.weight_cache_bytes += dev.numel() * 4
 
     def clear_cache(self) -> None:
+        """Drop every device copy of host arrays (weights, folded BatchNorm,
+        staged constants): the next run re-uploads everything it needs."""
         self.weight_cache.clear()
         self.weight_cache_bytes = 0
+        self.__dict__.pop("affine_cache", None)
+        self.__dict__.pop("const_cache", None)
 
     def sync(self) -> None:
         self.stream.synchronize()

@@ -28,8 +28,8 @@ import torch
 from .engine import device
 from .executor import PopulationRun, compare_outputs, lower, trial_inputs
 from .fitness import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
-from .ir import Graph, label_sequence
-from .knobs import ObfuscationPlan, TransformError, apply_plan
+from .ir import Graph, analyze, label_sequence
+from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
 from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,
                     run_trace, trace_population)
 
@@ -53,14 +53,16 @@ class Candidate:
     graph: Graph | None
     directives: object | None
     error: str | None = None
+    analysis: object | None = None
 
 
-def build_candidates(vanilla: Graph, plans: list[ObfuscationPlan]) -> list[Candidate]:
+def build_candidates(vanilla: Graph, plans: list[ObfuscationPlan], vanilla_analysis=None) -> list[Candidate]:
+    va = vanilla_analysis if vanilla_analysis is not None else analyze(vanilla)
     out = []
     for p in plans:
         try:
-            g, d = apply_plan(vanilla, p)
-            out.append(Candidate(p, g, d))
+            g, d, ana = apply_plan_analyzed(vanilla, p, va)
+            out.append(Candidate(p, g, d, analysis=ana))
         except TransformError as exc:
             out.append(Candidate(p, None, None, str(exc)))
     return out
@@ -85,14 +87,16 @@ class PopulationEvaluator:
     """
 
     def __init__(self, vanilla: Graph, evaluator: Evaluator | None = None, budget: float = 0.02, trials: int = 8,
-                 seed: int = 0, tol: float = 1e-5, eps: float = EPSILON, memo: dict | None = None):
+                 seed: int = 0, tol: float = 1e-5, eps: float = EPSILON, memo: dict | None = None, exchange=None):
         self.ctx = device()
+        self.exchange = exchange  # dist.exchange_signatures when the population is sharded
         self.vanilla = vanilla
         self.ev = evaluator or Evaluator()
         self.budget, self.trials, self.seed, self.tol, self.eps = budget, trials, seed, tol, eps
         self.memo = _SCHEDULE_CACHE if memo is None else memo
         self.truth = encode_labels(label_sequence(vanilla))
-        self.lowered_vanilla = lower(vanilla)
+        self.vanilla_analysis = analyze(vanilla)
+        self.lowered_vanilla = lower(vanilla, self.vanilla_analysis)
         self.x_host = torch.from_numpy(trial_inputs(vanilla.input_shape, trials, seed)).pin_memory()
         # T* = latency of the unobfuscated graph under the same profile (Eq. 10)
         pt = trace_population([(vanilla, None, None)], self.ev.profile, self.memo)
@@ -104,15 +108,16 @@ class PopulationEvaluator:
         descriptors, all staged into HBM. ``memo`` defaults to the
         process-global schedule memo; pass {} for a cold schedule search."""
         t0 = time.perf_counter()
-        cands = build_candidates(self.vanilla, plans)
+        cands = build_candidates(self.vanilla, plans, self.vanilla_analysis)
         t1 = time.perf_counter()
         feas = [i for i, c in enumerate(cands) if c.graph is not None]
-        run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph) for i in feas],
+        run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph, cands[i].analysis) for i in feas],
                             reps=self.trials)
         t2 = time.perf_counter()
-        items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies)
-                 for i in feas]
-        tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo) if items else None
+        items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies,
+                  cands[i].analysis) for i in feas]
+        tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo,
+                           exchange=self.exchange) if items else None
         idx = torch.tensor(feas, dtype=torch.long).to(self.ctx.device, non_blocking=True)
         t3 = time.perf_counter()
         return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,

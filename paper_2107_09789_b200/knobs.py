@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .ir import (COMPLEX_KINDS, Graph, Node, OperatorKind, TensorShape, shape_map, topo_order)
+from .ir import (COMPLEX_KINDS, Graph, Node, OperatorKind, TensorShape, analyze, shape_map, topo_order)
 
 BRANCH_MODES = ("none", "in2", "in4", "out2", "out4")            # transforms.py:19
 WIDEN_FACTORS = (1.0, 1.0625, 1.125, 1.25, 1.5)                  # transforms.py:20
@@ -60,10 +60,14 @@ def _round_half_up(x: float) -> int:
 class _Work:
     """Mutable view used by the knobs. ``nodes`` are private copies."""
 
-    def __init__(self, graph: Graph, own: bool = False):
+    def __init__(self, graph: Graph, own: bool = False, analysis=None):
         self.g = graph if own else graph.copy()
-        self.succ = self.g.successor_index()
-        self._shapes: dict[int, TensorShape] | None = None
+        if analysis is not None:  # reuse the input graph's structure (copied: we mutate)
+            self.succ = {k: list(v) for k, v in analysis.succ.items()}
+            self._shapes: dict[int, TensorShape] | None = dict(analysis.shapes)
+        else:
+            self.succ = self.g.successor_index()
+            self._shapes = None
 
     # -- structure ----------------------------------------------------------
     def sole_successor(self, nid: int) -> int | None:
@@ -313,6 +317,33 @@ def branch_layer(graph: Graph, layer_id: int, mode: str, parts: int) -> Graph:
 # Dummy addition / deepening / skipping / kernel widening (transforms.py:238-335)
 # ---------------------------------------------------------------------------
 
+# Knob-synthesised constants (zero skip kernels, zero dummy operands, identity
+# deepen kernels) depend only on their shape: one read-only array per shape is
+# shared by every candidate. Values equal the reference's fresh arrays, and
+# identical bases let the device weight cache upload each constant once.
+_CONSTS: dict[tuple, np.ndarray] = {}
+
+
+def _shared_zeros(shape: tuple) -> np.ndarray:
+    key = ("zeros",) + tuple(shape)
+    a = _CONSTS.get(key)
+    if a is None:
+        a = np.zeros(shape, dtype=np.float32)
+        a.flags.writeable = False
+        _CONSTS[key] = a
+    return a
+
+
+def _shared_identity(channels: int) -> np.ndarray:
+    key = ("eye", channels)
+    a = _CONSTS.get(key)
+    if a is None:
+        a = channel_identity_kernel(channels)
+        a.flags.writeable = False
+        _CONSTS[key] = a
+    return a
+
+
 def _insertion_point(w: _Work, layer_id: int) -> int:
     act = w.activation_site(layer_id)
     return layer_id if act is None else act
@@ -324,7 +355,7 @@ def _dummy(w: _Work, layer_id: int, count: int) -> None:
     shapes = w.shapes()
     site = _insertion_point(w, layer_id)
     s = shapes[site]
-    zeros = np.zeros(s.as_tuple(), dtype=np.float32)   # one constant shared by the whole chain
+    zeros = _shared_zeros(s.as_tuple())   # one constant shared by the whole chain
     prev, made = site, []
     for _ in range(count):
         nid = w.next_id()
@@ -360,7 +391,8 @@ def _deepen(w: _Work, layer_id: int, kernel_init) -> None:
     ch = s.channels
     conv_id = w.next_id()
     w.add_node(Node(conv_id, OperatorKind.Conv2D,
-                    {"k1": 1, "k2": 1, "c": ch, "j": ch, "stride": 1, "padding": 0}, kernel_init(ch), [act]))
+                    {"k1": 1, "k2": 1, "c": ch, "j": ch, "stride": 1, "padding": 0},
+                    _shared_identity(ch) if kernel_init is channel_identity_kernel else kernel_init(ch), [act]))
     w.add_node(Node(conv_id + 1, OperatorKind.ReLU, {}, None, [conv_id]))
     w.set_shape(conv_id, s)
     w.set_shape(conv_id + 1, s)
@@ -382,7 +414,7 @@ def _skip(w: _Work, layer_id: int) -> None:
     conv_id = w.next_id()
     w.add_node(Node(conv_id, OperatorKind.Conv2D,
                     {"k1": 1, "k2": 1, "c": ch, "j": ch, "stride": 1, "padding": 0},
-                    np.zeros((1, 1, ch, ch), dtype=np.float32), [site]))
+                    _shared_zeros((1, 1, ch, ch)), [site]))
     w.add_node(Node(conv_id + 1, OperatorKind.Add, {}, None, [site, conv_id]))
     w.set_shape(conv_id, s)
     w.set_shape(conv_id + 1, s)
@@ -480,7 +512,18 @@ class PlanApplicationError(TransformError):
 def apply_plan(graph: Graph, plan: ObfuscationPlan) -> tuple[Graph, BackendDirectives]:
     """Apply a whole plan: widen, kernel-widen, branch, deepen, skip, dummy —
     one pass per knob over the plan entries (transforms.py:400-474)."""
-    vanilla = graph.complex_layers()
+    out, directives, _ = apply_plan_analyzed(graph, plan)
+    return out, directives
+
+
+def apply_plan_analyzed(graph: Graph, plan: ObfuscationPlan, vanilla_analysis=None):
+    """``apply_plan`` that also returns the obfuscated graph's structural
+    analysis (order / successors / shapes), reusing the knobs' incremental
+    successor index and shape table instead of recomputing them."""
+    if vanilla_analysis is not None:
+        vanilla = [nid for nid in vanilla_analysis.order if graph.nodes[nid].kind in COMPLEX_KINDS]
+    else:
+        vanilla = graph.complex_layers()
     ids = [e.layer_id for e in plan.entries]
     if sorted(ids) != sorted(vanilla):
         raise PlanApplicationError([(-1, "plan", f"entries {sorted(ids)} != complex layers {sorted(vanilla)}")])
@@ -489,7 +532,7 @@ def apply_plan(graph: Graph, plan: ObfuscationPlan) -> tuple[Graph, BackendDirec
     # Fast exit: an all-identity plan returns the input graph object.
     touched = any(e.widen_factor != 1.0 or e.kernel_widen or e.branching != "none" or e.deepen or e.skip
                   or e.dummy_count for e in entries)
-    w = _Work(graph) if touched else None
+    w = _Work(graph, analysis=vanilla_analysis) if touched else None
     failures: list[tuple[int, str, str]] = []
     anchor = {lid: lid for lid in vanilla}
     carriers = {lid: [lid] for lid in vanilla}
@@ -534,5 +577,6 @@ def apply_plan(graph: Graph, plan: ObfuscationPlan) -> tuple[Graph, BackendDirec
                 directives.fusion_limits[nid] = e.fusion_limit
             if e.schedule_strategy:
                 directives.schedule_strategies[nid] = e.schedule_strategy
-    out = w.g if touched else graph
-    return out, directives
+    if touched:
+        return w.g, directives, analyze(w.g, w.succ, w._shapes)
+    return graph, directives, vanilla_analysis if vanilla_analysis is not None else analyze(graph)

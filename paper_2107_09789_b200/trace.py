@@ -26,7 +26,7 @@ import torch
 
 from . import _native as N
 from .engine import device
-from .ir import COMPLEX_KINDS, Graph, OperatorKind as K, TensorShape, infer_shapes, shape_map, topo_order
+from .ir import COMPLEX_KINDS, Graph, OperatorKind as K, TensorShape, analyze, infer_shapes, shape_map, topo_order
 from .kernels import DEFAULT_UNROLL, TRIVIAL_SCHEDULE, Kernel, Schedule, fuse, modify_schedule
 
 BYTES = 4            # costmodel.py:28
@@ -113,11 +113,31 @@ class Trace:
         return np.array([s.features(self.case) for s in self.steps], dtype=np.float64)
 
 
-@dataclass
 class CompiledGraph:
-    graph: Graph
-    kernels: list[Kernel]
-    schedules: list[Schedule]
+    """costmodel.py:259-263: shape-annotated graph, kernels, schedules. The
+    annotated copy is built lazily (the batched path never needs it)."""
+
+    def __init__(self, graph: Graph | None = None, kernels: list[Kernel] | None = None,
+                 schedules: list[Schedule] | None = None, *, source: Graph | None = None,
+                 shapes: dict | None = None):
+        self._graph = graph
+        self._source = source
+        self._shapes = shapes
+        self.kernels = kernels or []
+        self.schedules = schedules or []
+
+    @property
+    def graph(self) -> Graph:
+        if self._graph is None:
+            g = self._source.copy()
+            for nid, sh in self._shapes.items():
+                g.nodes[nid].out_shape = sh
+            self._graph = g
+        return self._graph
+
+    @property
+    def nodes_source(self) -> Graph:
+        return self._graph if self._graph is not None else self._source
 
 
 # process-global memo, first-seen semantics (costmodel.py:248)
@@ -155,39 +175,49 @@ def _work(graph: Graph, shapes: dict, nid: int) -> int:
     return _numel(s)
 
 
-def kernel_desc(graph: Graph, shapes: dict, kernel: Kernel, schedule: Schedule | None, d: N.KernDesc) -> None:
-    """Fill ``d`` with the integers profile_kernel reads (costmodel.py:166-232)."""
-    a = graph.nodes[kernel.anchor]
+KERN_DTYPE = np.dtype(N.KernDesc)
+
+
+def kernel_tuple(graph: Graph, shapes: dict, kernel: Kernel, schedule: Schedule | None = None, strategy: int = 0,
+                 sig_index: int = -1, resolved: int = 0) -> tuple:
+    """The integers profile_kernel reads (costmodel.py:166-232), as one
+    KERN_DTYPE record (field order of tobf_kern_desc)."""
+    nodes = graph.nodes
+    a = nodes[kernel.anchor]
     s = shapes[kernel.anchor]
-    d.has_shape = 1
-    d.work = _work(graph, shapes, kernel.anchor)
-    d.fused_work = sum(_work(graph, shapes, q) for q in kernel.node_ids[1:])
-    fb = 0
-    for q in kernel.node_ids[1:]:
-        nq = graph.nodes[q]
+    fused = kernel.node_ids[1:]
+    fw = fb = 0
+    for q in fused:
+        nq = nodes[q]
+        fw += _work(graph, shapes, q)
         if nq.weights is not None:
             fb += nq.weights.size * BYTES
         if nq.kind is K.Add and len(nq.inputs) > 1:
             fb += sum(_numel(shapes[p]) * BYTES for p in nq.inputs[1:])
-    d.fused_bytes = fb
-    d.in_bytes = (sum(_numel(shapes[p]) for p in a.inputs) if a.inputs else _numel(graph.input_shape)) * BYTES
-    d.w_bytes = a.weights.size * BYTES if a.weights is not None else 0
-    d.out_bytes = _numel(shapes[kernel.node_ids[-1]]) * BYTES
-    d.tiled = 1 if a.kind in (K.Conv2D, K.MaxPool) else 0
-    d.is_conv = 1 if a.kind is K.Conv2D else 0
-    d.H, d.W = s.height, s.width
-    if a.kind is K.Conv2D:
-        d.c, d.k1, d.k2, d.s = a.attrs["c"], a.attrs["k1"], a.attrs["k2"], a.attrs["stride"]
-    elif a.kind is K.MaxPool:
-        d.c, d.k1, d.k2, d.s = a.attrs.get("c", s.channels), a.attrs["window"], a.attrs["window"], a.attrs["stride"]
-    d.channel_like = a.attrs.get("j", s.channels)
-    d.reuse_x_stream = a.attrs["j"] if a.kind is K.Linear else 1
-    d.label = _LABEL_CODE.get(a.kind, -1)
-    d.unroll = DEFAULT_UNROLL
+    inb = (sum(_numel(shapes[p]) for p in a.inputs) if a.inputs else _numel(graph.input_shape)) * BYTES
+    wb = a.weights.size * BYTES if a.weights is not None else 0
+    ob = _numel(shapes[kernel.node_ids[-1]]) * BYTES
+    kind = a.kind
+    at = a.attrs
+    if kind is K.Conv2D:
+        geo = (1, 1, at["c"], at["k1"], at["k2"], at["stride"])
+    elif kind is K.MaxPool:
+        geo = (1, 0, at.get("c", s.channels), at["window"], at["window"], at["stride"])
+    else:
+        geo = (0, 0, 0, 0, 0, 0)
     if schedule is not None:
-        d.ty[:] = list(schedule.tile_y)
-        d.tx[:] = list(schedule.tile_x)
-        d.unroll = schedule.unroll
+        ty, tx, unroll = tuple(schedule.tile_y), tuple(schedule.tile_x), schedule.unroll
+    else:
+        ty, tx, unroll = (0, 0, 0), (0, 0, 0), DEFAULT_UNROLL
+    return (_work(graph, shapes, kernel.anchor), fw, fb, inb, wb, ob) + geo + (
+        s.height, s.width, at.get("j", s.channels), at["j"] if kind is K.Linear else 1, ty, tx, unroll,
+        _LABEL_CODE.get(kind, -1), 1, strategy, sig_index, resolved)
+
+
+def kernel_desc(graph: Graph, shapes: dict, kernel: Kernel, schedule: Schedule | None, d: N.KernDesc) -> None:
+    """Fill a ctypes KernDesc (single-kernel paths)."""
+    rec = np.array([kernel_tuple(graph, shapes, kernel, schedule)], dtype=KERN_DTYPE)
+    C.memmove(C.addressof(d), rec.ctypes.data, C.sizeof(d))
 
 
 def _to_step(row: np.ndarray, graph: Graph, kernel: Kernel) -> TraceStep:
@@ -242,10 +272,11 @@ class TracePlan:
         self.feats = self.totals = None
 
 
-def prepare_trace(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
-                  memo: dict | None = None, exchange=None) -> TracePlan:
-    """Host half of compile_graph for many graphs: shapes, fuse, signatures,
-    integer descriptors (one H2D for all).
+def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
+                  exchange=None) -> TracePlan:
+    """Host half of compile_graph for many graphs: fuse, signatures, integer
+    descriptors (one H2D for all). ``items``: (graph, fusion_limits,
+    strategies[, ir.Analysis]).
 
     ``exchange`` (dist.exchange_signatures) merges this rank's unmemoised
     signatures with every other rank's in global first-seen order; the
@@ -256,55 +287,48 @@ def prepare_trace(items: list[tuple[Graph, dict | None, dict | None]], profile: 
     compiled, per_kernel = [], []
     hits: dict[tuple, Schedule] = {}
     local_pending: dict[tuple, bytes] = {}
-    for graph, limits, strategies in items:
-        order = topo_order(graph)
-        shapes = shape_map(graph, order)
-        annotated = graph.copy()
-        for nid, sh in shapes.items():
-            annotated.nodes[nid].out_shape = sh
-        kernels = fuse(annotated, limits, order=order)
+    pname = profile.name
+    for item in items:
+        graph, limits, strategies = item[0], item[1], item[2]
+        ana = item[3] if len(item) > 3 and item[3] is not None else analyze(graph)
+        shapes = ana.shapes
+        kernels = fuse(graph, limits, order=ana.order, succ=ana.succ)
         strategies = strategies or {}
-        cg = CompiledGraph(annotated, kernels, [])
-        cg._shapes = shapes
+        cg = CompiledGraph(kernels=kernels, source=graph, shapes=shapes)
+        nodes = graph.nodes
         for k in kernels:
-            sig = schedule_signature(annotated, shapes, k, profile)
+            a = nodes[k.anchor]
+            ins = shapes[a.inputs[0]] if a.inputs else graph.input_shape
+            sig = (pname, a.kind.value, tuple(sorted(a.attrs.items())), ins.as_tuple(), shapes[k.anchor].as_tuple())
             if sig not in hits and sig not in local_pending:
                 hit = memo.get(sig)
-                if hit is None and annotated.nodes[k.anchor].kind not in COMPLEX_KINDS:
+                if hit is None and a.kind not in COMPLEX_KINDS:
                     hit = memo[sig] = TRIVIAL_SCHEDULE
                 if hit is not None:
                     hits[sig] = hit
                 else:
-                    d = N.KernDesc()
-                    kernel_desc(annotated, shapes, k, None, d)
-                    d.sig_index = -1
-                    local_pending[sig] = bytes(d)
+                    local_pending[sig] = np.array([kernel_tuple(graph, shapes, k)], dtype=KERN_DTYPE).tobytes()
             per_kernel.append((cg, k, sig, strategies.get(k.anchor, 0)))
         compiled.append(cg)
     pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
     rows: dict[tuple, int] = {}
-    sig_bytes = []
+    sig_recs = []
     for sig, sch in hits.items():
-        d = N.KernDesc()
-        d.has_shape, d.resolved, d.sig_index = 1, 1, -1
-        d.ty[:], d.tx[:], d.unroll = list(sch.tile_y), list(sch.tile_x), sch.unroll
-        rows[sig] = len(sig_bytes)
-        sig_bytes.append(bytes(d))
+        rows[sig] = len(sig_recs)
+        sig_recs.append(np.array([(0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, tuple(sch.tile_y), tuple(sch.tile_x),
+                                   sch.unroll, 0, 1, 0, -1, 1)], dtype=KERN_DTYPE).tobytes())
     pending = []
     for sig, blob in pending_all.items():
-        rows[sig] = len(sig_bytes)
+        rows[sig] = len(sig_recs)
         pending.append((rows[sig], sig))
-        sig_bytes.append(blob)
-    nsig, nk = len(sig_bytes), len(per_kernel)
-    kern_arr = (N.KernDesc * max(nk, 1))()
-    for r, (cg, k, sig, st) in enumerate(per_kernel):
-        d = kern_arr[r]
-        kernel_desc(cg.graph, cg._shapes, k, None, d)
-        d.sig_index, d.strategy = rows[sig], st
+        sig_recs.append(blob)
+    nsig, nk = len(sig_recs), len(per_kernel)
+    kern = np.array([kernel_tuple(cg.nodes_source, cg._shapes, k, None, st, rows[sig])
+                     for cg, k, sig, st in per_kernel], dtype=KERN_DTYPE) if nk else np.zeros(1, KERN_DTYPE)
     offsets = np.zeros(len(compiled) + 1, np.int32)
     offsets[1:] = np.cumsum([len(cg.kernels) for cg in compiled])
-    sig_blob = b"".join(sig_bytes) if sig_bytes else bytes(N.KernDesc())
-    blob = sig_blob + bytes(kern_arr)
+    sig_blob = b"".join(sig_recs) if sig_recs else np.zeros(1, KERN_DTYPE).tobytes()
+    blob = sig_blob + kern.tobytes()
     dev = ctx.upload_bytes(blob)
     offs = torch.from_numpy(offsets).to(ctx.device, non_blocking=True)
     tp = TracePlan(compiled, dev[len(sig_blob):], dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile,
@@ -380,7 +404,7 @@ class PopulationTrace:
         fh = feats_host if feats_host is not None else self.feats.cpu().numpy()
         cg = self.compiled[i]
         lo, hi = self.offsets_host[i], self.offsets_host[i + 1]
-        return Trace(tuple(_to_step(fh[r], cg.graph, k) for r, k in zip(range(lo, hi), cg.kernels)), case)
+        return Trace(tuple(_to_step(fh[r], cg.nodes_source, k) for r, k in zip(range(lo, hi), cg.kernels)), case)
 
 
 def trace_population(items: list[tuple[Graph, dict | None, dict | None]], profile: DeviceProfile,
