@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=1, help="cpu_baseline sample: rounds of one candidate per core")
+    ap.add_argument("--micro", type=int, default=8, help="e2e micro-batch (host prep overlaps device run)")
     return ap.parse_args()
 
 
@@ -266,18 +267,24 @@ def main_ours(args):
         plans_e2e = population_plans(vanilla, P * world * (steps_total + 1), args.seed + 1)
         per_step = P * world
 
+        host_ms = {}
+
         def e2e_step(s):
             ctx.clear_cache()
             shard = plans_e2e[s * per_step + rank * P: s * per_step + (rank + 1) * P]
-            p = pe.prepare(shard, memo={})
-            o = pe.run(p, cold_schedules=False)
-            rec = gather(o)
-            return rec.cpu()
+            rec = pe.evaluate_records(shard, micro=args.micro, memo={})
+            for k, v in pe.last_host_ms.items():
+                host_ms[k] = host_ms.get(k, 0.0) + v
+            if world > 1:
+                from paper_2107_09789_b200 import dist as tdist
+                rec = tdist.gather_records(rec, per_step)
+            return rec
 
         for s in range(args.warmup):
             e2e_step(s)
         torch.cuda.synchronize()
         barrier()
+        host_ms.clear()
         h0 = ctx.h2d_bytes
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
@@ -285,7 +292,7 @@ def main_ours(args):
         d2h = 0
         for s in range(args.warmup, steps_total):
             r = e2e_step(s)
-            d2h += r.numel() * r.element_size()
+            d2h += r.nbytes
         f1.record()
         torch.cuda.synchronize()
         barrier()
@@ -293,7 +300,9 @@ def main_ours(args):
         x_bytes = pe.x_host.numel() * 4
         e2e = {"value": world * P / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int((ctx.h2d_bytes - h0) / args.steps) + x_bytes,
-               "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms,
+               "host_ms_per_step": {k: round(v / args.steps, 2) for k, v in host_ms.items()},
+               "micro_batch": args.micro}
 
     # ---- cpu baseline (rank 0, N == 1 only)
     cpu = None

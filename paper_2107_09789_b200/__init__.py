@@ -1,0 +1,84 @@
+"""paper_2107_09789_b200 — B200-native drop-in for traceobf's candidate-evaluation path.
+
+Same public surface as the reference package (reference
+pkg/src/traceobf/__init__.py:8-49): graph IR, knobs + apply_plan, fusion and
+schedules, the analytical cost model and the reference executor — the last
+two now backed by sm_100a kernels in libtobf.so — plus the spec-level
+attacker / GA entry points the reference lacks (levenshtein, ler, fitness,
+run_ga, search_space) and the batched population evaluator.
+
+    import paper_2107_09789_b200 as traceobf      # drop-in
+"""
+
+from .ir import (
+    COMPLEX_KINDS,
+    INJECTIVE_KINDS,
+    CycleDetected,
+    Graph,
+    GraphError,
+    Node,
+    OperatorKind,
+    ShapeMismatch,
+    TensorShape,
+    Violation,
+    infer_shapes,
+    label_sequence,
+    topo_order,
+    validate,
+)
+from .knobs import (
+    BRANCH_MODES,
+    WIDEN_FACTORS,
+    BackendDirectives,
+    NoActivation,
+    NotDivisible,
+    NotWidenable,
+    ObfuscationPlan,
+    PlanApplicationError,
+    PlanEntry,
+    TransformError,
+    add_dummy,
+    apply_plan,
+    branch_layer,
+    channel_identity_kernel,
+    deepen_layer,
+    identity_plan,
+    skip_layer,
+    widen_kernel,
+    widen_layer,
+    widenable,
+)
+from .kernels import (
+    DEFAULT_UNROLL,
+    FUSION_SATURATION,
+    TILE_FACTORS,
+    TRIVIAL_SCHEDULE,
+    InvalidStrategy,
+    Kernel,
+    Schedule,
+    balanced_pair,
+    candidate_triples,
+    default_schedule,
+    fuse,
+    modify_schedule,
+)
+from .trace import (
+    BUILTIN_PROFILES,
+    CASE_FEATURES,
+    FEATURE_NAMES,
+    CompiledGraph,
+    DeviceProfile,
+    LeakageCase,
+    Trace,
+    TraceStep,
+    compile_graph,
+    profile_graph,
+    profile_kernel,
+    profile_pipeline,
+)
+from .executor import equivalence_check, evaluate_equivalence, execute
+from .fitness import FitnessReport, Predictor, bagged_predictors, init_predictor, ler, levenshtein
+from .evaluate import Evaluator, PopulationEvaluator, fitness
+from .ga import GaParams, GaResult, run_ga, search_space
+
+__version__ = "0.1.0"

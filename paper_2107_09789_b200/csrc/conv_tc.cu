@@ -46,44 +46,16 @@ struct ConvCfg {
 // fp32-faithful (error at OpenBLAS-sgemm level).
 constexpr int kChunkKB = 4;
 
-struct EpiRegs {
-  int nepi;
-  int op[TOBF_MAX_EPI];
-  int aux[TOBF_MAX_EPI];
-  const float* ptr[TOBF_MAX_EPI];
-};
+// Warp roles (384 threads = 3 warpgroups; registers rebalanced with setmaxnreg):
+//   WG0 warps 0-3   A producer (im2col gather, tf32 split, swizzled st.shared)
+//   WG1 warp 4      TMEM allocator + B producer (bulk copy of the packed weight image)
+//       warp 5      MMA issuer;  warps 6-7 idle
+//   WG2 warps 8-11  accumulator drain + epilogue (TMEM lanes 32*(warp%4) ...)
+constexpr int kThreads = 384;
+constexpr int kRegsProducer = 152, kRegsControl = 56, kRegsDrain = 256;
 
-__device__ __forceinline__ float epi_apply(float v, const EpiRegs& e, int64_t m, int c, int64_t cidx) {
-#pragma unroll
-  for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-    if (s >= e.nepi) break;
-    switch (e.op[s]) {
-      case TOBF_EPI_AFFINE:
-        v = v * __ldg(e.ptr[s] + c) + __ldg(e.ptr[s] + e.aux[s] + c);
-        break;
-      case TOBF_EPI_RELU:
-        v = fmaxf(v, 0.0f);
-        break;
-      case TOBF_EPI_ADD_TENSOR:
-        v = v + __ldg(e.ptr[s] + m * e.aux[s] + c);
-        break;
-      case TOBF_EPI_ADD_CONST:
-        v = v + __ldg(e.ptr[s] + cidx + c);
-        break;
-      default:
-        break;
-    }
-  }
-  return v;
-}
-
-// Warp roles (320 threads):
-//   0-3  A producer (im2col gather, tf32 split, swizzled st.shared)
-//   4    TMEM allocator + B producer (bulk copy of the packed weight image)
-//   5    MMA issuer
-//   6-9  accumulator drain + epilogue (TMEM lanes 32*(warp%4) ...)
 template <int BN>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     conv_tf32x3_kernel(const tobf_conv_desc* __restrict__ descs, int nprob) {
   using Cfg = ConvCfg<BN>;
   constexpr int STAGES = Cfg::kStages;
@@ -135,6 +107,7 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp < 4) {
     // ---------------------------------------------------------- A producer
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProducer));
     const int t = threadIdx.x;
     const int chunk = t & 7;
     const int rsub = t >> 3;
@@ -164,11 +137,9 @@ __global__ void __launch_bounds__(320, 1)
     }
     const float* __restrict__ x = d.x;
     const int H = d.H, W = d.W, ldx = d.ldx;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = 0; kb < kblocks; ++kb) {
+    // gather one K block (this thread: 8 rows x one 16-B chunk) and advance (u, v, c0)
+    auto gather = [&](float4 (&vals)[8]) {
       const bool kvalid = u < k1;
-      float4 vals[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int yi = ybase[i] + u;
@@ -179,6 +150,19 @@ __global__ void __launch_bounds__(320, 1)
           vals[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+      c0 += kBK;
+      while (c0 >= Cp) {
+        c0 -= Cp;
+        if (++v == k2) { v = 0; ++u; }
+      }
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    float4 cur[8], nxt[8];
+    gather(cur);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      // the next block's loads are in flight while this one is split and stored
+      if (kb + 1 < kblocks) gather(nxt);
       mbar_wait(&empty_bar[stage], phase ^ 1, 0x101);
       const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
       const uint32_t a_lo = a_hi + kABytes;
@@ -187,23 +171,23 @@ __global__ void __launch_bounds__(320, 1)
         const int r = rsub + 16 * i;
         const uint32_t off = sw128_off(r, chunk);
         float4 h, l;
-        h.x = __uint_as_float(to_tf32_rna(vals[i].x)); l.x = vals[i].x - h.x;
-        h.y = __uint_as_float(to_tf32_rna(vals[i].y)); l.y = vals[i].y - h.y;
-        h.z = __uint_as_float(to_tf32_rna(vals[i].z)); l.z = vals[i].z - h.z;
-        h.w = __uint_as_float(to_tf32_rna(vals[i].w)); l.w = vals[i].w - h.w;
+        h.x = __uint_as_float(to_tf32_rna(cur[i].x)); l.x = cur[i].x - h.x;
+        h.y = __uint_as_float(to_tf32_rna(cur[i].y)); l.y = cur[i].y - h.y;
+        h.z = __uint_as_float(to_tf32_rna(cur[i].z)); l.z = cur[i].z - h.z;
+        h.w = __uint_as_float(to_tf32_rna(cur[i].w)); l.w = cur[i].w - h.w;
         sts128(a_hi + off, h);
         sts128(a_lo + off, l);
       }
       fence_proxy_async_smem();
       mbar_arrive(&full_bar[stage]);
-      c0 += kBK;
-      while (c0 >= Cp) {
-        c0 -= Cp;
-        if (++v == k2) { v = 0; ++u; }
-      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == 4) {
+  } else if (warp < 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+  }
+  if (warp == 4) {
     // ---------------------------------------------------------- B producer
     if (lane == 0) {
       const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
@@ -254,8 +238,9 @@ __global__ void __launch_bounds__(320, 1)
         mma_commit(&acc_full[buf]);
       }
     }
-  } else {
+  } else if (warp >= 8) {
     // ---------------------------------------------------------- drain + epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsDrain));
     const int lq = warp & 3;  // TMEM lane quarter this warp may access
     float sum[BN];
 #pragma unroll
@@ -301,40 +286,119 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    EpiRegs e;
-    e.nepi = d.nepi;
+    const int nepi = d.nepi;
+    int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI], eslot[TOBF_MAX_EPI];
+    const float* eptr[TOBF_MAX_EPI];
+    int naff = 0, nld = 0, cperiod = 1;
 #pragma unroll
     for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-      e.op[s] = d.epi[s].op;
-      e.aux[s] = d.epi[s].aux;
-      e.ptr[s] = d.epi[s].ptr;
+      eop[s] = s < nepi ? d.epi[s].op : TOBF_EPI_NONE;
+      eaux[s] = d.epi[s].aux;
+      eptr[s] = d.epi[s].ptr;
+      eslot[s] = 0;
+      if (eop[s] == TOBF_EPI_AFFINE) eslot[s] = naff++;
+      if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) eslot[s] = nld++;
+      if (eop[s] == TOBF_EPI_ADD_CONST) cperiod = eaux[s];
     }
-    int cperiod = 1;
-    for (int s = 0; s < e.nepi; ++s)
-      if (e.op[s] == TOBF_EPI_ADD_CONST) cperiod = e.aux[s];
     // Row-per-warp-iteration epilogue: lanes cover 4 consecutive channels
     // each, so residual / constant reads and output writes are coalesced.
+    // Fast path: <= 2 affine steps and <= 2 tensor operands (every chain the
+    // lowering emits for the fixtures); longer chains take the generic path.
     constexpr int kLanesPerRow = BN / 4;            // 32 (BN=128) or 16 (BN=64)
     constexpr int kRowsPerIter = 32 / kLanesPerRow;  // 1 or 2
+    constexpr int kUnroll = 4;                       // independent rows in flight per lane
     const int sub = lane / kLanesPerRow;
     const int g = lane % kLanesPerRow;
     const int c = n_tile * BN + g * 4;
     const int Cpo = d.Cpo, j = d.j;
-    const int ew = warp - 6;  // 0..3
-#pragma unroll 1
-    for (int r0 = ew * kRowsPerIter; r0 < kBM; r0 += 4 * kRowsPerIter) {
-      const int row = r0 + sub;
-      const int m = m0 + row;
-      if (m >= M || c >= Cpo) continue;
-      const float* srow = reinterpret_cast<const float*>(smem) + row * BN;
-      const float4 a = *reinterpret_cast<const float4*>(srow + ((g ^ (row & (BN / 4 - 1))) * 4));
-      const int n_img = m / HWo;
-      const int pix = m - n_img * HWo;
-      const int64_t cidx = ((int64_t)(n_img % cperiod) * HWo + pix) * Cpo;
-      float o[4] = {a.x, a.y, a.z, a.w};
+    const bool cvalid = c < Cpo;
+    const bool fast = naff <= 2 && nld <= 2;
+    float4 sc[2], sh[2];  // per-channel affine parameters are row-invariant: load once
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = (c + q < j) ? epi_apply(o[q], e, m, c + q, cidx) : 0.0f;
-      *reinterpret_cast<float4*>(d.y + (int64_t)m * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
+    for (int a = 0; a < 2; ++a) sc[a] = sh[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+      if (fast && cvalid && eop[s] == TOBF_EPI_AFFINE) {
+        const float4 a4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + c));
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + c));
+        if (eslot[s] == 0) { sc[0] = a4; sh[0] = b4; } else { sc[1] = a4; sh[1] = b4; }
+      }
+    }
+    const int ew = warp - 8;  // 0..3
+    constexpr int kRowStep = 4 * kRowsPerIter;
+#pragma unroll 1
+    for (int r0 = ew * kRowsPerIter; r0 < kBM; r0 += kRowStep * kUnroll) {
+      float4 acc[kUnroll], opv[kUnroll][2];
+      int mrow[kUnroll];
+      int64_t cidx[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const int row = r0 + q * kRowStep + sub;
+        const int m = m0 + row;
+        mrow[q] = (row < kBM && m < M && cvalid) ? m : -1;
+        acc[q] = opv[q][0] = opv[q][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int n_img = mrow[q] >= 0 ? m / HWo : 0;
+        cidx[q] = ((int64_t)(n_img % cperiod) * HWo + (m - n_img * HWo)) * Cpo;
+        if (mrow[q] >= 0) {
+          const float* srow = reinterpret_cast<const float*>(smem) + row * BN;
+          acc[q] = *reinterpret_cast<const float4*>(srow + ((g ^ (row & (BN / 4 - 1))) * 4));
+          if (fast) {
+#pragma unroll
+            for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+              float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (eop[s] == TOBF_EPI_ADD_TENSOR)
+                t = __ldg(reinterpret_cast<const float4*>(eptr[s] + (int64_t)m * eaux[s] + c));
+              else if (eop[s] == TOBF_EPI_ADD_CONST)
+                t = __ldg(reinterpret_cast<const float4*>(eptr[s] + cidx[q] + c));
+              if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) {
+                if (eslot[s] == 0) opv[q][0] = t; else opv[q][1] = t;
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        if (mrow[q] < 0) continue;
+        float o[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
+#pragma unroll
+        for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+          const int op = eop[s];
+          if (op == TOBF_EPI_NONE) continue;
+          const int sl = eslot[s];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int ce = c + e;
+            if (op == TOBF_EPI_RELU) {
+              o[e] = fmaxf(o[e], 0.0f);
+            } else if (op == TOBF_EPI_AFFINE) {
+              if (fast) {
+                const float4 a4 = sl == 0 ? sc[0] : sc[1];
+                const float4 b4 = sl == 0 ? sh[0] : sh[1];
+                const float av = e == 0 ? a4.x : e == 1 ? a4.y : e == 2 ? a4.z : a4.w;
+                const float bv = e == 0 ? b4.x : e == 1 ? b4.y : e == 2 ? b4.z : b4.w;
+                o[e] = o[e] * av + bv;
+              } else {
+                o[e] = o[e] * __ldg(eptr[s] + ce) + __ldg(eptr[s] + eaux[s] + ce);
+              }
+            } else {
+              float tv;
+              if (fast) {
+                const float4 t4 = sl == 0 ? opv[q][0] : opv[q][1];
+                tv = e == 0 ? t4.x : e == 1 ? t4.y : e == 2 ? t4.z : t4.w;
+              } else {
+                tv = op == TOBF_EPI_ADD_TENSOR ? __ldg(eptr[s] + (int64_t)mrow[q] * eaux[s] + ce)
+                                               : __ldg(eptr[s] + cidx[q] + ce);
+              }
+              o[e] = o[e] + tv;
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c + e >= j) o[e] = 0.0f;
+        *reinterpret_cast<float4*>(d.y + (int64_t)mrow[q] * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
+      }
     }
   }
 
@@ -447,7 +511,7 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
     if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
-  conv_tf32x3_kernel<BN><<<(unsigned)total_tiles, 320, ConvCfg<BN>::kSmem, st>>>(d_descs, n);
+  conv_tf32x3_kernel<BN><<<(unsigned)total_tiles, kThreads, ConvCfg<BN>::kSmem, st>>>(d_descs, n);
   return tobf_cuda_check("tobf_conv_grouped");
 }
 

@@ -103,7 +103,7 @@ class PopulationEvaluator:
         self.t_star = float(pt.totals.cpu()[0])
 
     # ---------------------------------------------------------------- host
-    def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None) -> dict:
+    def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None) -> dict:
         """Host half: apply_plan, lowering, weight upload + packing, trace
         descriptors, all staged into HBM. ``memo`` defaults to the
         process-global schedule memo; pass {} for a cold schedule search."""
@@ -117,7 +117,7 @@ class PopulationEvaluator:
         items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies,
                   cands[i].analysis) for i in feas]
         tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo,
-                           exchange=self.exchange) if items else None
+                           exchange=self.exchange, first_seen=first_seen) if items else None
         idx = torch.tensor(feas, dtype=torch.long).to(self.ctx.device, non_blocking=True)
         t3 = time.perf_counter()
         return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
@@ -183,6 +183,24 @@ class PopulationEvaluator:
         rec["feasible"] = np.asarray(out["feasible"], dtype=np.int32)
         self.ctx.sync()
         return rec
+
+    def evaluate_records(self, plans: list[ObfuscationPlan], micro: int = 8, memo: dict | None = None) -> np.ndarray:
+        """Records for ``plans`` with host preparation of micro-batch i+1
+        overlapping the device pipeline of micro-batch i (launches are async;
+        the only host waits are the final read-backs). First-seen schedule
+        semantics hold across micro-batches: a signature pending in several of
+        them is searched from its first occurrence's descriptor everywhere."""
+        first_seen: dict = {}
+        jobs = []
+        for lo in range(0, len(plans), micro):
+            prep = self.prepare(plans[lo:lo + micro], memo=memo, first_seen=first_seen)
+            jobs.append((prep, self.run(prep, cold_schedules=False)))
+        recs = [self.collect(out) for _, out in jobs]
+        for prep, _ in jobs:
+            if prep["trace"] is not None:
+                finish_trace(prep["trace"])
+        self.last_host_ms = {k: sum(p["host_ms"][k] for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
+        return np.concatenate(recs)
 
     def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
         prep = self.prepare(plans)

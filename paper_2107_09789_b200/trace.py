@@ -273,7 +273,7 @@ class TracePlan:
 
 
 def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
-                  exchange=None) -> TracePlan:
+                  exchange=None, first_seen: dict | None = None) -> TracePlan:
     """Host half of compile_graph for many graphs: fuse, signatures, integer
     descriptors (one H2D for all). ``items``: (graph, fusion_limits,
     strategies[, ir.Analysis]).
@@ -281,7 +281,9 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
     ``exchange`` (dist.exchange_signatures) merges this rank's unmemoised
     signatures with every other rank's in global first-seen order; the
     resulting table is searched identically on every rank, so all memos stay
-    equal and every schedule is the one a single process would pick."""
+    equal and every schedule is the one a single process would pick.
+    ``first_seen`` (sig -> descriptor bytes) carries first occurrences across
+    batches whose searches have not been folded into the memo yet."""
     ctx = device()
     memo = _SCHEDULE_CACHE if memo is None else memo
     compiled, per_kernel = [], []
@@ -307,7 +309,12 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
                 if hit is not None:
                     hits[sig] = hit
                 else:
-                    local_pending[sig] = np.array([kernel_tuple(graph, shapes, k)], dtype=KERN_DTYPE).tobytes()
+                    blob = first_seen.get(sig) if first_seen is not None else None
+                    if blob is None:
+                        blob = np.array([kernel_tuple(graph, shapes, k)], dtype=KERN_DTYPE).tobytes()
+                        if first_seen is not None:
+                            first_seen[sig] = blob
+                    local_pending[sig] = blob
             per_kernel.append((cg, k, sig, strategies.get(k.anchor, 0)))
         compiled.append(cg)
     pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
