@@ -136,7 +136,7 @@ def cpu_step(pool, plans):
 
 def host_predictors():
     """Predictor weights without touching CUDA (same init as fitness.bagged_predictors)."""
-    from paper_2107_09789_b200 import fitness
+    from paper_2107_09789_b200 import attacker as fitness
     return fitness.bagged_predictors()
 
 

@@ -77,7 +77,7 @@ from .trace import (
     profile_pipeline,
 )
 from .executor import equivalence_check, evaluate_equivalence, execute
-from .fitness import FitnessReport, Predictor, bagged_predictors, init_predictor, ler, levenshtein
+from .attacker import FitnessReport, Predictor, bagged_predictors, init_predictor, ler, levenshtein
 from .evaluate import Evaluator, PopulationEvaluator, fitness
 from .ga import GaParams, GaResult, run_ga, search_space
 

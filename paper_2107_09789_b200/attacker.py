@@ -1,4 +1,4 @@
-"""Fitness stage on the GPU: bagged LSTM sequence predictors, greedy CTC,
+"""Attacker + fitness stage on the GPU: bagged LSTM sequence predictors, greedy CTC,
 Levenshtein / LER and the Eq. 10 reward.
 
 The reference package has no code for this stage (the attacker

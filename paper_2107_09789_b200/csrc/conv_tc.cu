@@ -31,10 +31,11 @@ template <int BN>
 struct ConvCfg {
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kStages = BN >= 128 ? 3 : 4;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  // [0,BN): correction terms (a_lo*b_hi + a_hi*b_lo), whole K;
-  // [BN,3BN): ping-pong main accumulators (a_hi*b_hi), one K chunk each
+  static constexpr int kStages = BN >= 128 ? 2 : 4;
+  static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
+  // [0,2BN): per-tile correction accumulators (a_lo*b_hi + a_hi*b_lo), 2 tile slots;
+  // [2BN,4BN): ping-pong main accumulators (a_hi*b_hi), one K chunk each
   static constexpr int kTmemCols = 4 * BN;
 };
 
@@ -46,39 +47,47 @@ struct ConvCfg {
 // fp32-faithful (error at OpenBLAS-sgemm level).
 constexpr int kChunkKB = 4;
 
+// Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ... of the
+// group (problems sorted by K descending, so long tiles go first). Every role
+// runs the same tile sequence; the operand ring, the chunk accumulators and
+// the tile-slot correction accumulators carry their phases across tiles, so
+// tile i+1's loads and MMAs overlap tile i's drain and epilogue.
 // Warp roles (384 threads = 3 warpgroups; registers rebalanced with setmaxnreg):
 //   WG0 warps 0-3   A producer (im2col gather, tf32 split, swizzled st.shared)
 //   WG1 warp 4      TMEM allocator + B producer (bulk copy of the packed weight image)
 //       warp 5      MMA issuer;  warps 6-7 idle
-//   WG2 warps 8-11  accumulator drain + epilogue (TMEM lanes 32*(warp%4) ...)
+//   WG2 warps 8-11  accumulator drain + fused epilogue (TMEM lanes 32*(warp%4) ...)
 constexpr int kThreads = 384;
 constexpr int kRegsProducer = 152, kRegsControl = 56, kRegsDrain = 256;
 
+__device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ descs, int nprob, int tile) {
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&descs[mid].tile_start) <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_tf32x3_kernel(const tobf_conv_desc* __restrict__ descs, int nprob) {
+    conv_tf32x3_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles) {
   using Cfg = ConvCfg<BN>;
   constexpr int STAGES = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
+  float* epi_buf = reinterpret_cast<float*>(smem + STAGES * Cfg::kStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes);
   uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain
+  uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain (one K chunk)
   uint64_t* acc_empty = acc_full + 2;        // [2] drain -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  int* s_prob = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* small_empty = acc_empty + 2;     // [2] drain -> MMA (tile-slot correction accumulator)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(small_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    int lo = 0, hi = nprob - 1;
-    const int b = blockIdx.x;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&descs[mid].tile_start) <= b) lo = mid; else hi = mid - 1;
-    }
-    *s_prob = lo;
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 128 + 1);
       mbar_init(&empty_bar[s], 1);
@@ -86,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
+      mbar_init(&small_empty[s], 128);
     }
     fence_mbar_init();
   }
@@ -94,16 +104,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const tobf_conv_desc& d = descs[*s_prob];
-
-  const int tile = blockIdx.x - d.tile_start;
-  const int m_tile = tile / d.ntiles;
-  const int n_tile = tile - m_tile * d.ntiles;
-  const int m0 = m_tile * kBM;
-  const int HWo = d.Ho * d.Wo;
-  const int M = d.batch * HWo;
-  const int kblocks = d.kblocks;
-  const int nchunks = (kblocks + kChunkKB - 1) / kChunkKB;
 
   if (warp < 4) {
     // ---------------------------------------------------------- A producer
@@ -111,78 +111,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t = threadIdx.x;
     const int chunk = t & 7;
     const int rsub = t >> 3;
-    int pixbase[8], ybase[8], xbase[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m0 + rsub + 16 * i;
-      if (m < M) {
-        const int n = m / HWo;
-        const int rem = m - n * HWo;
-        const int yo = rem / d.Wo;
-        const int xo = rem - yo * d.Wo;
-        pixbase[i] = n * d.H * d.W;
-        ybase[i] = yo * d.stride - d.pad;
-        xbase[i] = xo * d.stride - d.pad;
-      } else {
-        pixbase[i] = 0;
-        ybase[i] = -(1 << 28);  // forces the bounds test to fail
-        xbase[i] = -(1 << 28);
-      }
-    }
-    const int Cp = d.Cp, k1 = d.k1, k2 = d.k2;
-    int u = 0, v = 0, c0 = chunk * 4;
-    while (c0 >= Cp) {
-      c0 -= Cp;
-      if (++v == k2) { v = 0; ++u; }
-    }
-    const float* __restrict__ x = d.x;
-    const int H = d.H, W = d.W, ldx = d.ldx;
-    // gather one K block (this thread: 8 rows x one 16-B chunk) and advance (u, v, c0)
-    auto gather = [&](float4 (&vals)[8]) {
-      const bool kvalid = u < k1;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+      const int lt = tile - d.tile_start;
+      const int m0 = (lt / d.ntiles) * kBM;
+      const int HWo = d.Ho * d.Wo;
+      const int M = d.batch * HWo;
+      const int kblocks = d.kblocks;
+      int pixbase[8], ybase[8], xbase[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int yi = ybase[i] + u;
-        const int xi = xbase[i] + v;
-        if (kvalid && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W) {
-          vals[i] = ldg_nc4(x + (int64_t)(pixbase[i] + yi * W + xi) * ldx + c0);
+        const int m = m0 + rsub + 16 * i;
+        if (m < M) {
+          const int n = m / HWo;
+          const int rem = m - n * HWo;
+          const int yo = rem / d.Wo;
+          const int xo = rem - yo * d.Wo;
+          pixbase[i] = n * d.H * d.W;
+          ybase[i] = yo * d.stride - d.pad;
+          xbase[i] = xo * d.stride - d.pad;
         } else {
-          vals[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          pixbase[i] = 0;
+          ybase[i] = -(1 << 28);  // forces the bounds test to fail
+          xbase[i] = -(1 << 28);
         }
       }
-      c0 += kBK;
+      const int Cp = d.Cp, k1 = d.k1, k2 = d.k2;
+      int u = 0, v = 0, c0 = chunk * 4;
       while (c0 >= Cp) {
         c0 -= Cp;
         if (++v == k2) { v = 0; ++u; }
       }
-    };
-    int stage = 0;
-    uint32_t phase = 0;
-    float4 cur[8], nxt[8];
-    gather(cur);
-    for (int kb = 0; kb < kblocks; ++kb) {
-      // the next block's loads are in flight while this one is split and stored
-      if (kb + 1 < kblocks) gather(nxt);
-      mbar_wait(&empty_bar[stage], phase ^ 1, 0x101);
-      const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
-      const uint32_t a_lo = a_hi + kABytes;
+      const float* __restrict__ x = d.x;
+      const int H = d.H, W = d.W, ldx = d.ldx;
+      // gather one K block (this thread: 8 rows x one 16-B chunk) and advance (u, v, c0)
+      auto gather = [&](float4 (&vals)[8]) {
+        const bool kvalid = u < k1;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = rsub + 16 * i;
-        const uint32_t off = sw128_off(r, chunk);
-        float4 h, l;
-        h.x = __uint_as_float(to_tf32_rna(cur[i].x)); l.x = cur[i].x - h.x;
-        h.y = __uint_as_float(to_tf32_rna(cur[i].y)); l.y = cur[i].y - h.y;
-        h.z = __uint_as_float(to_tf32_rna(cur[i].z)); l.z = cur[i].z - h.z;
-        h.w = __uint_as_float(to_tf32_rna(cur[i].w)); l.w = cur[i].w - h.w;
-        sts128(a_hi + off, h);
-        sts128(a_lo + off, l);
+        for (int i = 0; i < 8; ++i) {
+          const int yi = ybase[i] + u;
+          const int xi = xbase[i] + v;
+          if (kvalid && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W) {
+            vals[i] = ldg_nc4(x + (int64_t)(pixbase[i] + yi * W + xi) * ldx + c0);
+          } else {
+            vals[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        if (Cp >= kBK) {          // Cp % 32 == 0 or a single wrap
+          c0 += kBK;
+          if (c0 >= Cp) {
+            c0 -= Cp;
+            if (++v == k2) { v = 0; ++u; }
+          }
+        } else {                  // Cp in {4, 8, 16, ...}: step 32/Cp filter taps
+          c0 += kBK;
+          const int adv = c0 / Cp;
+          c0 -= adv * Cp;
+          v += adv;
+          if (v >= k2) {
+            u += v / k2;
+            v -= (v / k2) * k2;
+          }
+        }
+      };
+      float4 cur[8], nxt[8];
+      gather(cur);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        // the next block's loads are in flight while this one is split and stored
+        if (kb + 1 < kblocks) gather(nxt);
+        mbar_wait(&empty_bar[stage], phase ^ 1, 0x101);
+        const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
+        const uint32_t a_lo = a_hi + kABytes;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = rsub + 16 * i;
+          const uint32_t off = sw128_off(r, chunk);
+          float4 h, l;
+          h.x = __uint_as_float(to_tf32_rna(cur[i].x)); l.x = cur[i].x - h.x;
+          h.y = __uint_as_float(to_tf32_rna(cur[i].y)); l.y = cur[i].y - h.y;
+          h.z = __uint_as_float(to_tf32_rna(cur[i].z)); l.z = cur[i].z - h.z;
+          h.w = __uint_as_float(to_tf32_rna(cur[i].w)); l.w = cur[i].w - h.w;
+          sts128(a_hi + off, h);
+          sts128(a_lo + off, l);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&full_bar[stage]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&full_bar[stage]);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp < 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
@@ -190,16 +209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4) {
     // ---------------------------------------------------------- B producer
     if (lane == 0) {
-      const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
-                            (int64_t)n_tile * kblocks * (2 * Cfg::kBBytes);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&empty_bar[stage], phase ^ 1, 0x104);
-        uint8_t* dst = smem + stage * Cfg::kStageBytes + 2 * kABytes;
-        mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
-        bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+        const int lt = tile - d.tile_start;
+        const int n_tile = lt - (lt / d.ntiles) * d.ntiles;
+        const int kblocks = d.kblocks;
+        const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
+                              (int64_t)n_tile * kblocks * (2 * Cfg::kBBytes);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1, 0x104);
+          uint8_t* dst = smem + stage * Cfg::kStageBytes + 2 * kABytes;
+          mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
+          bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 5) {
@@ -208,197 +233,242 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = idesc_make(2u /*tf32*/, kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int kb = 0;
-      const uint32_t acc_small = tmem_base;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        const int buf = ch & 1;
-        const uint32_t acc = tmem_base + BN + buf * BN;
-        mbar_wait(&acc_empty[buf], ((ch >> 1) & 1) ^ 1, 0x106);
+      int gc = 0;  // global chunk counter (main accumulator ping-pong)
+      int it = 0;  // local tile counter (correction accumulator slot)
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+        const int kblocks = descs[find_problem(descs, nprob, tile)].kblocks;
+        const int slot = it & 1;
+        const uint32_t acc_small = tmem_base + slot * BN;
+        mbar_wait(&small_empty[slot], ((it >> 1) & 1) ^ 1, 0x107);
         tc_fence_after();
-        const int kend = min(kblocks, kb + kChunkKB);
-        for (int kc = 0; kb < kend; ++kb, ++kc) {
-          mbar_wait(&full_bar[stage], phase, 0x105);
+        for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
+          const int buf = gc & 1;
+          const uint32_t acc = tmem_base + 2 * BN + buf * BN;
+          mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106);
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
-          const uint32_t a_lo = a_hi + kABytes;
-          const uint32_t b_hi = a_hi + 2 * kABytes;
-          const uint32_t b_lo = b_hi + Cfg::kBBytes;
+          const int kend = min(kblocks, kb0 + kChunkKB);
+          for (int kb = kb0; kb < kend; ++kb) {
+            mbar_wait(&full_bar[stage], phase, 0x105);
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
+            const uint32_t a_lo = a_hi + kABytes;
+            const uint32_t b_hi = a_hi + 2 * kABytes;
+            const uint32_t b_lo = b_hi + Cfg::kBBytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-            const uint64_t dah = sdesc_k128(a_hi + koff), dal = sdesc_k128(a_lo + koff);
-            const uint64_t dbh = sdesc_k128(b_hi + koff), dbl = sdesc_k128(b_lo + koff);
-            mma_tf32(acc_small, dal, dbh, idesc, (kb | kk) != 0);
-            mma_tf32(acc_small, dah, dbl, idesc, 1u);
-            mma_tf32(acc, dah, dbh, idesc, (kc | kk) != 0);
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+              const uint64_t dah = sdesc_k128(a_hi + koff), dal = sdesc_k128(a_lo + koff);
+              const uint64_t dbh = sdesc_k128(b_hi + koff), dbl = sdesc_k128(b_lo + koff);
+              mma_tf32(acc_small, dal, dbh, idesc, (kb | kk) != 0);
+              mma_tf32(acc_small, dah, dbl, idesc, 1u);
+              mma_tf32(acc, dah, dbh, idesc, (kb - kb0 | kk) != 0);
+            }
+            mma_commit(&empty_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          mma_commit(&acc_full[buf]);
         }
-        mma_commit(&acc_full[buf]);
       }
     }
   } else if (warp >= 8) {
     // ---------------------------------------------------------- drain + epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsDrain));
     const int lq = warp & 3;  // TMEM lane quarter this warp may access
-    float sum[BN];
-#pragma unroll
-    for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int buf = ch & 1;
-      mbar_wait(&acc_full[buf], (ch >> 1) & 1, 0x103);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + BN + buf * BN;
-#pragma unroll
-      for (int cc = 0; cc < BN / 16; ++cc) {
-        float part[16];
-        tmem_ld16(taddr + cc * 16, part);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
-    }
-    {
-      // the last acc_full commit covered every MMA, so the correction
-      // accumulator is complete as well
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16);
-#pragma unroll
-      for (int cc = 0; cc < BN / 16; ++cc) {
-        float part[16];
-        tmem_ld16(taddr + cc * 16, part);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
-      }
-    }
-    // Stage the tile's fp32 sums in shared memory (the operand ring is idle:
-    // every K block has been consumed), 16-B chunks XOR-swizzled by row so
-    // the row-per-thread writes are bank-conflict free.
-    {
-      const int row = lq * 32 + lane;
-      float* srow = reinterpret_cast<float*>(smem) + row * BN;
-#pragma unroll
-      for (int g = 0; g < BN / 4; ++g) {
-        const int gs = g ^ (row & (BN / 4 - 1));
-        *reinterpret_cast<float4*>(srow + gs * 4) =
-            make_float4(sum[g * 4], sum[g * 4 + 1], sum[g * 4 + 2], sum[g * 4 + 3]);
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const int nepi = d.nepi;
-    int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI], eslot[TOBF_MAX_EPI];
-    const float* eptr[TOBF_MAX_EPI];
-    int naff = 0, nld = 0, cperiod = 1;
-#pragma unroll
-    for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-      eop[s] = s < nepi ? d.epi[s].op : TOBF_EPI_NONE;
-      eaux[s] = d.epi[s].aux;
-      eptr[s] = d.epi[s].ptr;
-      eslot[s] = 0;
-      if (eop[s] == TOBF_EPI_AFFINE) eslot[s] = naff++;
-      if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) eslot[s] = nld++;
-      if (eop[s] == TOBF_EPI_ADD_CONST) cperiod = eaux[s];
-    }
-    // Row-per-warp-iteration epilogue: lanes cover 4 consecutive channels
-    // each, so residual / constant reads and output writes are coalesced.
-    // Fast path: <= 2 affine steps and <= 2 tensor operands (every chain the
-    // lowering emits for the fixtures); longer chains take the generic path.
-    constexpr int kLanesPerRow = BN / 4;            // 32 (BN=128) or 16 (BN=64)
-    constexpr int kRowsPerIter = 32 / kLanesPerRow;  // 1 or 2
-    constexpr int kUnroll = 4;                       // independent rows in flight per lane
-    const int sub = lane / kLanesPerRow;
-    const int g = lane % kLanesPerRow;
-    const int c = n_tile * BN + g * 4;
-    const int Cpo = d.Cpo, j = d.j;
-    const bool cvalid = c < Cpo;
-    const bool fast = naff <= 2 && nld <= 2;
-    float4 sc[2], sh[2];  // per-channel affine parameters are row-invariant: load once
-#pragma unroll
-    for (int a = 0; a < 2; ++a) sc[a] = sh[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-      if (fast && cvalid && eop[s] == TOBF_EPI_AFFINE) {
-        const float4 a4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + c));
-        const float4 b4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + c));
-        if (eslot[s] == 0) { sc[0] = a4; sh[0] = b4; } else { sc[1] = a4; sh[1] = b4; }
-      }
-    }
     const int ew = warp - 8;  // 0..3
-    constexpr int kRowStep = 4 * kRowsPerIter;
+    int gc = 0, it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+      const int lt = tile - d.tile_start;
+      const int m_tile = lt / d.ntiles;
+      const int n_tile = lt - m_tile * d.ntiles;
+      const int m0 = m_tile * kBM;
+      const int HWo = d.Ho * d.Wo;
+      const int M = d.batch * HWo;
+      const int kblocks = d.kblocks;
+      const int slot = it & 1;
+      float sum[BN];
+#pragma unroll
+      for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
+      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
+        const int buf = gc & 1;
+        mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + 2 * BN + buf * BN;
+#pragma unroll
+        for (int cc = 0; cc < BN / 16; ++cc) {
+          float part[16];
+          tmem_ld16(taddr + cc * 16, part);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+      }
+      {
+        // the tile's last acc_full commit covered every MMA of the tile, so the
+        // correction accumulator of this slot is complete as well
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + slot * BN;
+#pragma unroll
+        for (int cc = 0; cc < BN / 16; ++cc) {
+          float part[16];
+          tmem_ld16(taddr + cc * 16, part);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
+        }
+        tc_fence_before();
+        mbar_arrive(&small_empty[slot]);
+      }
+      // Stage the tile's fp32 sums in the epilogue buffer, 16-B chunks
+      // XOR-swizzled by row so the row-per-thread writes are conflict free.
+      {
+        const int row = lq * 32 + lane;
+        float* srow = epi_buf + row * BN;
+#pragma unroll
+        for (int g = 0; g < BN / 4; ++g) {
+          const int gs = g ^ (row & (BN / 4 - 1));
+          *reinterpret_cast<float4*>(srow + gs * 4) =
+              make_float4(sum[g * 4], sum[g * 4 + 1], sum[g * 4 + 2], sum[g * 4 + 3]);
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+
+      const int nepi = d.nepi;
+      int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI], eslot[TOBF_MAX_EPI];
+      const float* eptr[TOBF_MAX_EPI];
+      int naff = 0, nld = 0, cperiod = 1;
+#pragma unroll
+      for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+        eop[s] = s < nepi ? d.epi[s].op : TOBF_EPI_NONE;
+        eaux[s] = d.epi[s].aux;
+        eptr[s] = d.epi[s].ptr;
+        eslot[s] = 0;
+        if (eop[s] == TOBF_EPI_AFFINE) eslot[s] = naff++;
+        if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) eslot[s] = nld++;
+        if (eop[s] == TOBF_EPI_ADD_CONST) cperiod = eaux[s];
+      }
+      // Row-per-warp-iteration epilogue: lanes cover 4 consecutive channels
+      // each, so residual / constant reads and output writes are coalesced.
+      // Fast path: <= 2 affine steps and <= 2 tensor operands (every chain the
+      // lowering emits for the fixtures); longer chains take the generic path.
+      constexpr int kLanesPerRow = BN / 4;            // 32 (BN=128) or 16 (BN=64)
+      constexpr int kRowsPerIter = 32 / kLanesPerRow;  // 1 or 2
+      constexpr int kUnroll = 4;                       // independent rows in flight per lane
+      const int sub = lane / kLanesPerRow;
+      const int g = lane % kLanesPerRow;
+      const int c = n_tile * BN + g * 4;
+      const int Cpo = d.Cpo, j = d.j;
+      const bool cvalid = c < Cpo;
+      const bool fast = naff <= 2 && nld <= 2;
+      float4 sc[2], sh[2];  // per-channel affine parameters are row-invariant: load once
+#pragma unroll
+      for (int a = 0; a < 2; ++a) sc[a] = sh[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+        if (fast && cvalid && eop[s] == TOBF_EPI_AFFINE) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + c));
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + c));
+          if (eslot[s] == 0) { sc[0] = a4; sh[0] = b4; } else { sc[1] = a4; sh[1] = b4; }
+        }
+      }
+      constexpr int kRowStep = 4 * kRowsPerIter;
 #pragma unroll 1
-    for (int r0 = ew * kRowsPerIter; r0 < kBM; r0 += kRowStep * kUnroll) {
-      float4 acc[kUnroll], opv[kUnroll][2];
-      int mrow[kUnroll];
-      int64_t cidx[kUnroll];
+      for (int r0 = ew * kRowsPerIter; r0 < kBM; r0 += kRowStep * kUnroll) {
+        float4 acc[kUnroll], opv[kUnroll][2];
+        int mrow[kUnroll];
+        int64_t cidx[kUnroll];
 #pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const int row = r0 + q * kRowStep + sub;
-        const int m = m0 + row;
-        mrow[q] = (row < kBM && m < M && cvalid) ? m : -1;
-        acc[q] = opv[q][0] = opv[q][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int n_img = mrow[q] >= 0 ? m / HWo : 0;
-        cidx[q] = ((int64_t)(n_img % cperiod) * HWo + (m - n_img * HWo)) * Cpo;
-        if (mrow[q] >= 0) {
-          const float* srow = reinterpret_cast<const float*>(smem) + row * BN;
-          acc[q] = *reinterpret_cast<const float4*>(srow + ((g ^ (row & (BN / 4 - 1))) * 4));
-          if (fast) {
+        for (int q = 0; q < kUnroll; ++q) {
+          const int row = r0 + q * kRowStep + sub;
+          const int m = m0 + row;
+          mrow[q] = (row < kBM && m < M && cvalid) ? m : -1;
+          acc[q] = opv[q][0] = opv[q][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const int n_img = mrow[q] >= 0 ? m / HWo : 0;
+          cidx[q] = ((int64_t)(n_img % cperiod) * HWo + (m - n_img * HWo)) * Cpo;
+          if (mrow[q] >= 0) {
+            const float* srow = epi_buf + row * BN;
+            acc[q] = *reinterpret_cast<const float4*>(srow + ((g ^ (row & (BN / 4 - 1))) * 4));
+            if (fast) {
 #pragma unroll
-            for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-              float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (eop[s] == TOBF_EPI_ADD_TENSOR)
-                t = __ldg(reinterpret_cast<const float4*>(eptr[s] + (int64_t)m * eaux[s] + c));
-              else if (eop[s] == TOBF_EPI_ADD_CONST)
-                t = __ldg(reinterpret_cast<const float4*>(eptr[s] + cidx[q] + c));
-              if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) {
-                if (eslot[s] == 0) opv[q][0] = t; else opv[q][1] = t;
+              for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+                float4 tv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (eop[s] == TOBF_EPI_ADD_TENSOR)
+                  tv = __ldg(reinterpret_cast<const float4*>(eptr[s] + (int64_t)m * eaux[s] + c));
+                else if (eop[s] == TOBF_EPI_ADD_CONST)
+                  tv = __ldg(reinterpret_cast<const float4*>(eptr[s] + cidx[q] + c));
+                if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) {
+                  if (eslot[s] == 0) opv[q][0] = tv; else opv[q][1] = tv;
+                }
               }
             }
           }
         }
-      }
+        // apply the chain step by step: one warp-uniform branch per step per
+        // batch of rows, straight-line float math inside
+        float o[kUnroll][4];
 #pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        if (mrow[q] < 0) continue;
-        float o[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
-#pragma unroll
-        for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-          const int op = eop[s];
-          if (op == TOBF_EPI_NONE) continue;
-          const int sl = eslot[s];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int ce = c + e;
+        for (int q = 0; q < kUnroll; ++q) {
+          o[q][0] = acc[q].x; o[q][1] = acc[q].y; o[q][2] = acc[q].z; o[q][3] = acc[q].w;
+        }
+        if (fast) {
+#pragma unroll 1
+          for (int s = 0; s < nepi; ++s) {
+            const int op = d.epi[s].op;
+            const int sl = eslot[s < TOBF_MAX_EPI ? s : 0];
             if (op == TOBF_EPI_RELU) {
-              o[e] = fmaxf(o[e], 0.0f);
+#pragma unroll
+              for (int q = 0; q < kUnroll; ++q)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[q][e] = fmaxf(o[q][e], 0.0f);
             } else if (op == TOBF_EPI_AFFINE) {
-              if (fast) {
-                const float4 a4 = sl == 0 ? sc[0] : sc[1];
-                const float4 b4 = sl == 0 ? sh[0] : sh[1];
-                const float av = e == 0 ? a4.x : e == 1 ? a4.y : e == 2 ? a4.z : a4.w;
-                const float bv = e == 0 ? b4.x : e == 1 ? b4.y : e == 2 ? b4.z : b4.w;
-                o[e] = o[e] * av + bv;
-              } else {
-                o[e] = o[e] * __ldg(eptr[s] + ce) + __ldg(eptr[s] + eaux[s] + ce);
+              const float4 a4 = sl == 0 ? sc[0] : sc[1];
+              const float4 b4 = sl == 0 ? sh[0] : sh[1];
+#pragma unroll
+              for (int q = 0; q < kUnroll; ++q) {
+                o[q][0] = o[q][0] * a4.x + b4.x;
+                o[q][1] = o[q][1] * a4.y + b4.y;
+                o[q][2] = o[q][2] * a4.z + b4.z;
+                o[q][3] = o[q][3] * a4.w + b4.w;
               }
-            } else {
-              float tv;
-              if (fast) {
+            } else if (op == TOBF_EPI_ADD_TENSOR || op == TOBF_EPI_ADD_CONST) {
+#pragma unroll
+              for (int q = 0; q < kUnroll; ++q) {
                 const float4 t4 = sl == 0 ? opv[q][0] : opv[q][1];
-                tv = e == 0 ? t4.x : e == 1 ? t4.y : e == 2 ? t4.z : t4.w;
-              } else {
-                tv = op == TOBF_EPI_ADD_TENSOR ? __ldg(eptr[s] + (int64_t)mrow[q] * eaux[s] + ce)
-                                               : __ldg(eptr[s] + cidx[q] + ce);
+                o[q][0] += t4.x; o[q][1] += t4.y; o[q][2] += t4.z; o[q][3] += t4.w;
               }
-              o[e] = o[e] + tv;
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int s = 0; s < nepi; ++s) {
+            const tobf_epi_step st = d.epi[s];
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) {
+              if (mrow[q] < 0) continue;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int ce = c + e;
+                switch (st.op) {
+                  case TOBF_EPI_RELU: o[q][e] = fmaxf(o[q][e], 0.0f); break;
+                  case TOBF_EPI_AFFINE: o[q][e] = o[q][e] * __ldg(st.ptr + ce) + __ldg(st.ptr + st.aux + ce); break;
+                  case TOBF_EPI_ADD_TENSOR: o[q][e] += __ldg(st.ptr + (int64_t)mrow[q] * st.aux + ce); break;
+                  case TOBF_EPI_ADD_CONST: o[q][e] += __ldg(st.ptr + cidx[q] + ce); break;
+                  default: break;
+                }
+              }
             }
           }
         }
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (c + e >= j) o[e] = 0.0f;
-        *reinterpret_cast<float4*>(d.y + (int64_t)mrow[q] * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
+        for (int q = 0; q < kUnroll; ++q) {
+          if (mrow[q] < 0) continue;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (c + e >= j) o[q][e] = 0.0f;
+          *reinterpret_cast<float4*>(d.y + (int64_t)mrow[q] * d.ldy + c) =
+              make_float4(o[q][0], o[q][1], o[q][2], o[q][3]);
+        }
       }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue buffer free for the next tile
     }
   }
 
@@ -504,14 +574,20 @@ extern "C" int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t
 
 template <int BN>
 static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute(conv_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ConvCfg<BN>::kSmem);
-    if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
+    if (e != cudaSuccess) {
+      sms = 0;
+      return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
   }
-  conv_tf32x3_kernel<BN><<<(unsigned)total_tiles, kThreads, ConvCfg<BN>::kSmem, st>>>(d_descs, n);
+  const int grid = (int)std::min<int64_t>(total_tiles, sms);
+  conv_tf32x3_kernel<BN><<<grid, kThreads, ConvCfg<BN>::kSmem, st>>>(d_descs, n, (int)total_tiles);
   return tobf_cuda_check("tobf_conv_grouped");
 }
 

@@ -132,6 +132,175 @@ __global__ void lstm_ctc_kernel(const double* __restrict__ feats, const int32_t*
   if (j < TPC && b0 + j < B) ntok[b0 + j] = s_cnt[j];
 }
 
+// ------------------------------------------------------------------------
+// Cluster LSTM: one thread-block cluster per group of TPC traces; CTA rank r
+// owns hidden units [32r, 32r+32) (lane = unit, warp = trace), keeps its
+// 128 gate rows of [W_ih | W_hh] resident in shared memory as bf16 (exact:
+// predictor weights are bf16-representable by construction), and after every
+// step broadcasts its h slice into every CTA's h buffer through distributed
+// shared memory (st.shared::cluster), followed by one cluster barrier.
+// Rank 0 then computes the head logits and the greedy-CTC token. The gate
+// accumulation order (bias, x[0..F), h[0..H)) and every rounding are the
+// same as the single-CTA formulation and the CPU oracle.
+constexpr int kLstmUnits = 32;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t map_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+template <int TPC>
+__global__ void __launch_bounds__(TPC * 32, 1)
+    lstm_ctc_cluster_kernel(const double* __restrict__ feats, const int32_t* __restrict__ offsets, int B, int F,
+                            int H, int NC, const float* __restrict__ w_ihT, const float* __restrict__ w_hhT,
+                            const float* __restrict__ bias, const float* __restrict__ w_out,
+                            const float* __restrict__ b_out, int8_t* __restrict__ tokens, int T_max,
+                            int32_t* __restrict__ ntok) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int L = F + H;                 // input vector length: [x_t | h_{t-1}]
+  const int Lq = L >> 2;               // full quads
+  const int Lp = (L + 3) & ~3;         // padded row length of the h buffers
+  // wq[kq][g][u] : 4 consecutive k of gate row (g, u) as 4 bf16 (uint2)
+  uint2* wq = reinterpret_cast<uint2*>(sm);
+  uint16_t* wtail = reinterpret_cast<uint16_t*>(sm + (size_t)Lq * 4 * kLstmUnits * 8);  // [L%4][4][32]
+  float* hv = reinterpret_cast<float*>(sm + (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2);
+  float* bsm = hv + 2 * TPC * Lp;      // [4][32]
+  float* wo = bsm + 4 * kLstmUnits;    // [NC][H] (rank 0 uses it)
+  const int G = 4 * H;
+  const uint32_t rank = cluster_rank();
+  const int CS = H / kLstmUnits;
+  const int u = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int unit = rank * kLstmUnits + u;
+  const int b = blockIdx.y * TPC + q;
+
+  // ---- one-time staging of this CTA's gate rows (fp32 -> bf16, exact)
+  for (int i = threadIdx.x; i < Lq * 4 * kLstmUnits; i += blockDim.x) {
+    const int uu = i % kLstmUnits, g = (i / kLstmUnits) % 4, kq = i / (4 * kLstmUnits);
+    const int col = g * H + rank * kLstmUnits + uu;
+    uint32_t pk[2];
+    for (int h2 = 0; h2 < 2; ++h2) {
+      uint32_t lo16, hi16;
+      const int k0 = kq * 4 + 2 * h2;
+      const float w0 = k0 < F ? w_ihT[(int64_t)k0 * G + col] : w_hhT[(int64_t)(k0 - F) * G + col];
+      const float w1 = k0 + 1 < F ? w_ihT[(int64_t)(k0 + 1) * G + col] : w_hhT[(int64_t)(k0 + 1 - F) * G + col];
+      lo16 = __float_as_uint(w0) >> 16;
+      hi16 = __float_as_uint(w1) >> 16;
+      pk[h2] = lo16 | (hi16 << 16);
+    }
+    wq[i] = make_uint2(pk[0], pk[1]);
+  }
+  for (int i = threadIdx.x; i < (L & 3) * 4 * kLstmUnits; i += blockDim.x) {
+    const int uu = i % kLstmUnits, g = (i / kLstmUnits) % 4, e = i / (4 * kLstmUnits);
+    const int k = Lq * 4 + e;
+    const int col = g * H + rank * kLstmUnits + uu;
+    const float w = k < F ? w_ihT[(int64_t)k * G + col] : w_hhT[(int64_t)(k - F) * G + col];
+    wtail[i] = (uint16_t)(__float_as_uint(w) >> 16);
+  }
+  for (int i = threadIdx.x; i < 4 * kLstmUnits; i += blockDim.x)
+    bsm[i] = bias[(i / kLstmUnits) * H + rank * kLstmUnits + (i % kLstmUnits)];
+  if (rank == 0)
+    for (int i = threadIdx.x; i < NC * H; i += blockDim.x) wo[i] = w_out[i];
+  for (int i = threadIdx.x; i < 2 * TPC * Lp; i += blockDim.x) hv[i] = 0.0f;
+  const int len = b < B ? offsets[b + 1] - offsets[b] : 0;
+  const int row0 = b < B ? offsets[b] : 0;
+  int tmax = len;
+  for (int o = 16; o; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+  __shared__ int s_tmax[TPC];
+  if (u == 0) s_tmax[q] = tmax;
+  __syncthreads();
+  tmax = 0;
+  for (int i = 0; i < TPC; ++i) tmax = max(tmax, s_tmax[i]);
+  cluster_sync_all();  // every CTA's buffers are initialised before remote writes start
+
+  // remote addresses of this thread's h slot in every CTA, per buffer
+  const uint32_t hv_local = static_cast<uint32_t>(__cvta_generic_to_shared(hv));
+  float c = 0.0f;
+  int prev = 0, cnt = 0;
+  for (int t = 0; t < tmax; ++t) {
+    float* hcur = hv + (t & 1) * TPC * Lp + q * Lp;
+    const int nxt = (t + 1) & 1;
+    if (u < F) hcur[u] = t < len ? (float)tobf_log1p_d(feats[(int64_t)(row0 + t) * 9 + u]) : 0.0f;
+    __syncwarp();
+    float acc0 = bsm[u], acc1 = bsm[32 + u], acc2 = bsm[64 + u], acc3 = bsm[96 + u];
+    const uint2* wrow = wq + u;
+#pragma unroll 4
+    for (int kq = 0; kq < Lq; ++kq) {
+      const float4 v = *reinterpret_cast<const float4*>(hcur + kq * 4);
+      const uint2 w0 = wrow[(kq * 4 + 0) * kLstmUnits], w1 = wrow[(kq * 4 + 1) * kLstmUnits];
+      const uint2 w2 = wrow[(kq * 4 + 2) * kLstmUnits], w3 = wrow[(kq * 4 + 3) * kLstmUnits];
+      acc0 = fmaf(bf16lo(w0.x), v.x, acc0); acc1 = fmaf(bf16lo(w1.x), v.x, acc1);
+      acc2 = fmaf(bf16lo(w2.x), v.x, acc2); acc3 = fmaf(bf16lo(w3.x), v.x, acc3);
+      acc0 = fmaf(bf16hi(w0.x), v.y, acc0); acc1 = fmaf(bf16hi(w1.x), v.y, acc1);
+      acc2 = fmaf(bf16hi(w2.x), v.y, acc2); acc3 = fmaf(bf16hi(w3.x), v.y, acc3);
+      acc0 = fmaf(bf16lo(w0.y), v.z, acc0); acc1 = fmaf(bf16lo(w1.y), v.z, acc1);
+      acc2 = fmaf(bf16lo(w2.y), v.z, acc2); acc3 = fmaf(bf16lo(w3.y), v.z, acc3);
+      acc0 = fmaf(bf16hi(w0.y), v.w, acc0); acc1 = fmaf(bf16hi(w1.y), v.w, acc1);
+      acc2 = fmaf(bf16hi(w2.y), v.w, acc2); acc3 = fmaf(bf16hi(w3.y), v.w, acc3);
+    }
+    for (int e = 0; e < (L & 3); ++e) {
+      const float xv = hcur[Lq * 4 + e];
+      const uint16_t* wt = wtail + e * 4 * kLstmUnits + u;
+      acc0 = fmaf(__uint_as_float((uint32_t)wt[0] << 16), xv, acc0);
+      acc1 = fmaf(__uint_as_float((uint32_t)wt[32] << 16), xv, acc1);
+      acc2 = fmaf(__uint_as_float((uint32_t)wt[64] << 16), xv, acc2);
+      acc3 = fmaf(__uint_as_float((uint32_t)wt[96] << 16), xv, acc3);
+    }
+    float hval = hcur[F + unit];
+    if (t < len) {
+      const float ig = tobf_sigmoid(acc0);
+      const float fg = tobf_sigmoid(acc1);
+      const float gg = tobf_tanh(acc2);
+      const float og = tobf_sigmoid(acc3);
+      c = fmaf(fg, c, ig * gg);
+      hval = og * tobf_tanh(c);
+    }
+    const uint32_t slot = hv_local + 4u * (uint32_t)(nxt * TPC * Lp + q * Lp + F + unit);
+    for (int rr = 0; rr < CS; ++rr) st_cluster_f32(map_shared(slot, rr), hval);
+    cluster_sync_all();
+    if (rank == 0 && t < len) {
+      const float* hn = hv + nxt * TPC * Lp + q * Lp + F;
+      int best = 0;
+      float bestv = 0.0f;
+      for (int cls = 0; cls < NC; ++cls) {
+        float p = 0.0f;
+        for (int k = u; k < H; k += 32) p = fmaf(wo[cls * H + k], hn[k], p);
+        for (int off = 16; off; off >>= 1) p = p + __shfl_xor_sync(0xffffffffu, p, off);
+        const float lg = b_out[cls] + p;
+        if (cls == 0 || lg > bestv) {
+          best = cls;
+          bestv = lg;
+        }
+      }
+      if (u == 0) {
+        if (best != 0 && best != prev) {
+          tokens[(int64_t)b * T_max + cnt] = (int8_t)best;
+          ++cnt;
+        }
+        prev = best;
+      }
+    }
+  }
+  if (rank == 0 && u == 0 && b < B) ntok[b] = cnt;
+}
+
 // One warp per prediction; strips of 32 truth columns, anti-diagonal sweep.
 __global__ void levenshtein_kernel(const int8_t* __restrict__ pred, const int32_t* __restrict__ ntok, int B,
                                    int T_max, const int8_t* __restrict__ truth, int m, int32_t* __restrict__ ed,
@@ -243,6 +412,35 @@ static int launch_lstm(const double* feats, const int32_t* offsets, int32_t B, i
   return tobf_cuda_check("tobf_lstm_ctc");
 }
 
+static int launch_lstm_cluster(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H,
+                               int32_t NC, const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
+                               const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, cudaStream_t st) {
+  constexpr int TPC = 8;
+  const int L = F + H, Lq = L / 4, Lp = (L + 3) & ~3, CS = H / kLstmUnits;
+  const size_t smem = (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2 +
+                      sizeof(float) * (2 * TPC * Lp + 4 * kLstmUnits + NC * H);
+  auto kern = lstm_ctc_cluster_kernel<TPC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm cluster attrs: %s", cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, (B + TPC - 1) / TPC, 1);
+  cfg.blockDim = dim3(TPC * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, feats, offsets, (int)B, (int)F, (int)H, (int)NC, w_ihT, w_hhT, b, w_out, b_out,
+                         tokens, (int)T_max, ntok);
+  if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm cluster launch: %s", cudaGetErrorString(e));
+  return tobf_cuda_check("tobf_lstm_ctc");
+}
+
 extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H,
                              int32_t NC, const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
                              const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, void* stream) {
@@ -251,6 +449,8 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
       NC < 2 || NC > kMaxNC || H < 32 || H > 1024 || H % 32 || T_max < 1)
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
+  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16)
+    return launch_lstm_cluster(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   if (B >= 148 * 8) return launch_lstm<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   return launch_lstm<2>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
 }

@@ -27,7 +27,7 @@ import torch
 
 from .engine import device
 from .executor import PopulationRun, compare_outputs, lower, trial_inputs
-from .fitness import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
+from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
 from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,

@@ -7,7 +7,7 @@ import pytest
 from oracle import fitness_ref as FR
 from paper_2107_09789_b200 import fixtures, ga, knobs
 from paper_2107_09789_b200.evaluate import RECORD_DTYPE
-from paper_2107_09789_b200.fitness import eq10
+from paper_2107_09789_b200.attacker import eq10
 
 
 def fake_eval(plans):

@@ -15,7 +15,8 @@ from oracle import costmodel_ref as CM
 from oracle import fitness_ref as FR
 from oracle import interp_ref as IR
 from paper_2107_09789_b200 import _native as N
-from paper_2107_09789_b200 import executor, fitness, fixtures, ga, knobs, trace
+from paper_2107_09789_b200 import attacker as fitness
+from paper_2107_09789_b200 import executor, fixtures, ga, knobs, trace
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
 from paper_2107_09789_b200.ir import label_sequence
 
