@@ -102,6 +102,7 @@ class DeviceContext:
         self.weight_cache_bytes = 0
         self.__dict__.pop("affine_cache", None)
         self.__dict__.pop("const_cache", None)
+        self.__dict__.pop("wimg_cache", None)
 
     def sync(self) -> None:
         self.stream.synchronize()

@@ -37,6 +37,18 @@ def _rup4(c: int) -> int:
     return (c + 3) // 4 * 4
 
 
+def ctx_arena(ctx: DeviceContext, floats: int) -> Arena:
+    """The context's activation arena, grown on demand and reused: every run
+    is ordered on the engine stream, so a later run's writes cannot overtake
+    an earlier run's reads."""
+    ar = ctx.__dict__.get("arena")
+    if ar is None or ar.buf.numel() < floats:
+        ar = Arena(ctx, int(floats * 1.1) + 4096)
+        ctx.arena = ar
+    ar.used = 0
+    return ar
+
+
 @dataclass
 class Step:
     """One epilogue step: ('affine', node) | ('relu',) | ('add', value_node) | ('const', node)."""
@@ -172,8 +184,22 @@ def lower(graph: Graph, analysis=None) -> Lowered:
 # Population run: allocate, pack, describe, launch
 # ---------------------------------------------------------------------------
 
+CONV_DTYPE = np.dtype(N.ConvDesc)
+EW_DTYPE = np.dtype(N.EwDesc)
+_NO_EPI = (0, 0, 0)
+
+
 class PopulationRun:
-    """Runs the forward of several lowered graphs on the same stacked input."""
+    """Runs the forward of several lowered graphs on the same stacked input.
+
+    Host preparation is table-driven: descriptor rows are numpy records
+    (one H2D for all levels), packed weight images are cached per weight
+    view (every candidate that reuses a vanilla layer — or a branch slice of
+    it, or a shared knob constant — shares one image), activations live in
+    one arena reused across runs on the engine stream.
+    """
+
+    conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
 
     def __init__(self, ctx: DeviceContext, lowered: list[Lowered], reps: int):
         self.ctx = ctx
@@ -186,28 +212,21 @@ class PopulationRun:
                 raise ShapeMismatch(-1, "population graphs disagree on the input shape")
         ishape = g0.input_shape
         self.batch = ishape.batch * reps
-        # ---- sizes -> one arena for activations, constants and weight images
-        act_floats = Arena.round(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
-        wimg_floats = 0
+        act = Arena.round(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
         for lw in lowered:
             for v in lw.values:
-                s = lw.shapes[v]
-                act_floats += Arena.round(self.batch * s.height * s.width * _rup4(s.channels))
-            for op in lw.ops:
-                if op.kind == "gemm":
-                    k1, k2, cp, j = self._gemm_geom(lw, op)
-                    bn = 128 if j > 64 else 64
-                    wimg_floats += Arena.round(self.ctx.lib.tobf_wimg_bytes(k1, k2, cp, j, bn) // 4)
-        self.arena = Arena(ctx, act_floats + wimg_floats + 4096)
-        self._stage_affines()
+                sh = lw.shapes[v]
+                act += Arena.round(self.batch * sh.height * sh.width * _rup4(sh.channels))
+        self.arena = ctx_arena(ctx, act + 4096)
         self.x_ptr = self.arena.take(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
         self.bufs: list[dict[int, int]] = []
         for lw in lowered:
             b = {-1: self.x_ptr}
             for v in sorted(lw.values):
-                s = lw.shapes[v]
-                b[v] = self.arena.take(self.batch * s.height * s.width * _rup4(s.channels))
+                sh = lw.shapes[v]
+                b[v] = self.arena.take(self.batch * sh.height * sh.width * _rup4(sh.channels))
             self.bufs.append(b)
+        self._stage_affines()
         self._prepare()
 
     # -------------------------------------------------------------- helpers
@@ -270,30 +289,54 @@ class PopulationRun:
         hit = cache.get(id(node.weights))
         if hit is not None and hit[0] is node.weights:
             return hit[1].data_ptr()
-        s = lw.shapes[nid]
+        sh = lw.shapes[nid]
         b0 = lw.graph.input_shape.batch
-        cp = _rup4(s.channels)
+        cp = _rup4(sh.channels)
         src_ptr, _ = self.ctx.cached_view(np.ascontiguousarray(node.weights, dtype=np.float32))
-        dev = torch.empty(b0 * s.height * s.width * cp, dtype=torch.float32, device=self.ctx.device)
+        dev = torch.empty(b0 * sh.height * sh.width * cp, dtype=torch.float32, device=self.ctx.device)
         self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(src_ptr), C.c_void_p(dev.data_ptr()), b0,
-                                                      s.channels, s.height, s.width, cp, C.c_void_p(self.ctx.sp)),
+                                                      sh.channels, sh.height, sh.width, cp, C.c_void_p(self.ctx.sp)),
                        "const staging")
+        self.ctx.launches += 1
         cache[id(node.weights)] = (node.weights, dev)
         return dev.data_ptr()
 
-    def _epi_fill(self, lw: Lowered, bufs: dict, steps: list, epi_arr) -> int:
-        for i, st in enumerate(steps):
-            e = epi_arr[i]
+    def _wimg(self, n, s_in: TensorShape, k1: int, k2: int, cp: int, j: int, bn: int) -> int:
+        """Packed tf32 hi/lo operand image of a conv/linear weight view, cached
+        by (device view, geometry): one pack per distinct view per cache life."""
+        ctx, lib = self.ctx, self.ctx.lib
+        wptr, st = ctx.cached_view(n.weights)
+        if n.kind is K.Conv2D:
+            su, sv, sc, sn = st
+        else:
+            r, cstride = st
+            su, sv, sc, sn = s_in.width * r, r, s_in.height * s_in.width * r, cstride
+        key = (wptr, su, sv, sc, sn, k1, k2, s_in.channels, cp, j, bn)
+        cache = ctx.__dict__.setdefault("wimg_cache", {})
+        hit = cache.get(key)
+        if hit is not None:
+            return hit.data_ptr()
+        nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
+        img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
+        ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, s_in.channels, cp, j, su, sv, sc, sn, bn,
+                                        C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
+        ctx.launches += 1
+        cache[key] = img
+        return img.data_ptr()
+
+    def _epi_rows(self, lw: Lowered, bufs: dict, steps: list) -> list:
+        out = []
+        for st in steps:
             if st.op == "affine":
-                e.op, e.aux, e.ptr = N.EPI_AFFINE, _rup4(lw.shapes[st.ref].channels), self._affine(lw, st.ref)
+                out.append((N.EPI_AFFINE, _rup4(lw.shapes[st.ref].channels), self._affine(lw, st.ref)))
             elif st.op == "relu":
-                e.op, e.aux, e.ptr = N.EPI_RELU, 0, None
+                out.append((N.EPI_RELU, 0, 0))
             elif st.op == "add":
-                s = lw.shapes[st.ref] if st.ref >= 0 else lw.graph.input_shape
-                e.op, e.aux, e.ptr = N.EPI_ADD_TENSOR, _rup4(s.channels), bufs[st.ref]
+                sh = lw.shapes[st.ref] if st.ref >= 0 else lw.graph.input_shape
+                out.append((N.EPI_ADD_TENSOR, _rup4(sh.channels), bufs[st.ref]))
             elif st.op == "const":
-                e.op, e.aux, e.ptr = N.EPI_ADD_CONST, lw.graph.input_shape.batch, self._const(lw, st.ref)
-        return len(steps)
+                out.append((N.EPI_ADD_CONST, lw.graph.input_shape.batch, self._const(lw, st.ref)))
+        return out
 
     # -------------------------------------------------------------- prepare
     def _prepare(self) -> None:
@@ -301,79 +344,70 @@ class PopulationRun:
         levels: dict[int, dict[str, list]] = {}
         for gi, lw in enumerate(self.lowered):
             bufs = self.bufs[gi]
+            nodes = lw.graph.nodes
             for op in lw.ops:
-                lvl = levels.setdefault(op.level, {"g64": [], "g128": [], "ew": []})
+                lvl = levels.get(op.level)
+                if lvl is None:
+                    lvl = levels[op.level] = {"g64": [], "g128": [], "ew": []}
                 s_in = self._in_shape(lw, op)
                 s_out = lw.shapes[op.out]
                 if op.kind == "gemm":
-                    n = lw.graph.nodes[op.node]
+                    n = nodes[op.node]
                     k1, k2, cp, j = self._gemm_geom(lw, op)
                     bn = 128 if j > 64 else 64
-                    # weight view -> strides over (u, v, c, n)
-                    wptr, st = ctx.cached_view(n.weights)
                     if n.kind is K.Conv2D:
-                        su, sv, sc, sn = st
                         stride, pad = n.attrs["stride"], n.attrs["padding"]
                     else:
-                        r, cstride = st
-                        H, W = s_in.height, s_in.width
-                        su, sv, sc, sn = W * r, r, H * W * r, cstride
                         stride, pad = 1, 0
-                    nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
-                    wimg = self.arena.take(nbytes // 4)
-                    ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, s_in.channels, cp, j, su, sv, sc, sn,
-                                                    bn, C.c_void_p(wimg), C.c_void_p(ctx.sp)), "pack weights")
-                    d = N.ConvDesc()
-                    d.x, d.wimg, d.y = bufs[op.src], wimg, bufs[op.out]
-                    d.batch, d.H, d.W, d.Cp = self.batch, s_in.height, s_in.width, cp
-                    d.Ho, d.Wo, d.Cpo, d.j = s_out.height, s_out.width, _rup4(j), j
-                    d.k1, d.k2, d.stride, d.pad = k1, k2, stride, pad
-                    d.ldx, d.ldy = cp, _rup4(j)
-                    d.nepi = self._epi_fill(lw, bufs, op.steps, d.epi)
-                    lvl["g128" if bn == 128 else "g64"].append(d)
+                    epi = self._epi_rows(lw, bufs, op.steps)
+                    row = (bufs[op.src], self._wimg(n, s_in, k1, k2, cp, j, bn), bufs[op.out],
+                           self.batch, s_in.height, s_in.width, cp, s_out.height, s_out.width, _rup4(j), j,
+                           k1, k2, stride, pad, 0, 0, 0, 0, 0, len(epi), cp, _rup4(j),
+                           epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi)))
+                    lvl["g128" if bn == 128 else "g64"].append((k1 * k2 * cp, row))
                     continue
-                e = N.EwDesc()
-                e.x, e.y = bufs[op.src], bufs[op.out]
-                e.batch, e.H, e.W = self.batch, s_in.height, s_in.width
-                e.ldx = _rup4(s_in.channels)
-                e.ldy = _rup4(s_out.channels)
+                ldx, ldy = _rup4(s_in.channels), _rup4(s_out.channels)
+                epi = []
                 if op.kind == "pool":
-                    n = lw.graph.nodes[op.node]
-                    e.op, e.C, e.Cpo = N.OP_MAXPOOL, s_in.channels, _rup4(s_in.channels)
-                    e.Ho, e.Wo, e.a0, e.a1 = s_out.height, s_out.width, n.attrs["window"], n.attrs["stride"]
+                    n = nodes[op.node]
+                    head = (N.OP_MAXPOOL, self.batch, s_in.height, s_in.width, s_in.channels, ldx, s_out.height,
+                            s_out.width, ldy, n.attrs["window"], n.attrs["stride"])
+                    cpo = _rup4(s_in.channels)
                 elif op.kind == "epi":
-                    e.op, e.C, e.Cpo = N.OP_EPI, s_out.channels, _rup4(s_out.channels)
-                    e.Ho, e.Wo = s_out.height, s_out.width
-                    e.nepi = self._epi_fill(lw, bufs, op.steps, e.epi)
+                    epi = self._epi_rows(lw, bufs, op.steps)
+                    head = (N.OP_EPI, self.batch, s_in.height, s_in.width, s_out.channels, ldx, s_out.height,
+                            s_out.width, ldy, 0, 0)
+                    cpo = _rup4(s_out.channels)
                 elif op.kind == "copy":
                     total = s_out.channels
-                    last = op.a0 + op.cc == total
-                    e.op, e.C, e.a0, e.a1 = N.OP_COPYCH, op.cc, op.a0, op.a1
-                    e.Cpo = _rup4(total) if last else op.a0 + op.cc
-                elif op.kind == "softmax":
-                    e.op, e.C, e.Cpo = N.OP_SOFTMAX, s_in.channels, _rup4(s_in.channels)
-                lvl["ew"].append(e)
-        # sort GEMM problems by descending K so long tiles are scheduled first
+                    head = (N.OP_COPYCH, self.batch, s_in.height, s_in.width, op.cc, ldx, 0, 0, ldy, op.a0, op.a1)
+                    cpo = _rup4(total) if op.a0 + op.cc == total else op.a0 + op.cc
+                else:  # softmax
+                    head = (N.OP_SOFTMAX, self.batch, s_in.height, s_in.width, s_in.channels, ldx, 0, 0, ldy, 0, 0)
+                    cpo = _rup4(s_in.channels)
+                lvl["ew"].append((bufs[op.src], bufs[op.out]) + head +
+                                 (len(epi), 0, cpo, 0, epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi))))
         self.launches = []
         blobs = []
         for lv in sorted(levels):
             grp = levels[lv]
             for key, bn in (("g128", 128), ("g64", 64)):
-                lst = sorted(grp[key], key=lambda d: -(d.k1 * d.k2 * d.Cp))
-                if not lst:
+                if not grp[key]:
                     continue
-                arr = (N.ConvDesc * len(lst))(*lst)
+                # long-K problems first so their tiles start earliest
+                rows = [r for _, r in sorted(grp[key], key=lambda t: -t[0])]
+                arr = np.array(rows, dtype=CONV_DTYPE)
                 tot = C.c_int64()
-                ctx.check(lib.tobf_conv_prepare(arr, len(lst), bn, C.byref(tot)), "conv prepare")
-                blobs.append(bytes(arr))
-                self.launches.append(("conv", len(blobs) - 1, len(lst), tot.value, bn))
+                ctx.check(lib.tobf_conv_prepare(C.c_void_p(arr.ctypes.data), len(rows), bn, C.byref(tot)),
+                          "conv prepare")
+                blobs.append(arr.tobytes())
+                self.launches.append(("conv", len(blobs) - 1, len(rows), tot.value, bn))
             if grp["ew"]:
-                arr = (N.EwDesc * len(grp["ew"]))(*grp["ew"])
+                arr = np.array(grp["ew"], dtype=EW_DTYPE)
                 tot = C.c_int64()
-                ctx.check(lib.tobf_ew_prepare(arr, len(grp["ew"]), C.byref(tot)), "ew prepare")
-                blobs.append(bytes(arr))
-                self.launches.append(("ew", len(blobs) - 1, len(grp["ew"]), tot.value, 0))
-        # one H2D copy for every descriptor table
+                ctx.check(lib.tobf_ew_prepare(C.c_void_p(arr.ctypes.data), len(arr), C.byref(tot)), "ew prepare")
+                blobs.append(arr.tobytes())
+                self.launches.append(("ew", len(blobs) - 1, len(arr), tot.value, 0))
         offs, total = [], 0
         for b in blobs:
             offs.append(total)
@@ -397,8 +431,6 @@ class PopulationRun:
                                                       s.channels, s.height, s.width, _rup4(s.channels),
                                                       C.c_void_p(self.ctx.sp)), "input staging")
         self.ctx.launches += 1
-
-    conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
 
     def run(self) -> None:
         lib, sp = self.ctx.lib, C.c_void_p(self.ctx.sp)
