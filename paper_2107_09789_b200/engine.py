@@ -59,6 +59,14 @@ class DeviceContext:
         self.h2d_bytes += host.numel()
         return host.pin_memory().to(self.device, non_blocking=True)
 
+    def upload_array(self, a: np.ndarray) -> torch.Tensor:
+        """Pinned, stream-ordered H2D of a small host array (never a hidden
+        synchronising pageable copy)."""
+        a = np.ascontiguousarray(a)
+        host = torch.from_numpy(a).pin_memory()
+        self.h2d_bytes += a.nbytes
+        return host.to(self.device, non_blocking=True)
+
     def upload_struct_array(self, arr) -> torch.Tensor:
         return self.upload_bytes(memoryview(arr).cast("B"))
 

@@ -118,7 +118,7 @@ class PopulationEvaluator:
                   cands[i].analysis) for i in feas]
         tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo,
                            exchange=self.exchange, first_seen=first_seen) if items else None
-        idx = torch.tensor(feas, dtype=torch.long).to(self.ctx.device, non_blocking=True)
+        idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t3 = time.perf_counter()
         return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
                 "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
@@ -156,7 +156,7 @@ class PopulationEvaluator:
         if ncf:
             idx = prep["idx"]
             if not hasattr(self, "_truth_dev"):
-                self._truth_dev = torch.from_numpy(self.truth).to(ctx.device)
+                self._truth_dev = ctx.upload_array(self.truth)
             for p, pred in enumerate(self.ev.predictors):
                 toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred)
                 _, lr, _ = edit_distances(toks, ntok, self._truth_dev)

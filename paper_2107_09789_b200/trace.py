@@ -337,7 +337,7 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
     sig_blob = b"".join(sig_recs) if sig_recs else np.zeros(1, KERN_DTYPE).tobytes()
     blob = sig_blob + kern.tobytes()
     dev = ctx.upload_bytes(blob)
-    offs = torch.from_numpy(offsets).to(ctx.device, non_blocking=True)
+    offs = ctx.upload_array(offsets)
     tp = TracePlan(compiled, dev[len(sig_blob):], dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile,
                    memo)
     tp._blob = dev
