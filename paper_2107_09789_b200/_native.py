@@ -116,7 +116,7 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("TOBF_LIB", LIB_PATH))  # TOBF_LIB: debug builds
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is missing: build it with `python -m paper_2107_09789_b200.build_native` "

@@ -33,7 +33,8 @@ struct ConvCfg {
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStages = BN >= 128 ? 2 : 4;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
-  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kInfoBytes + 1024 /*align*/ + 512 /*barriers*/;
   // [0,2BN): per-tile correction accumulators (a_lo*b_hi + a_hi*b_lo), 2 tile slots;
   // [2BN,4BN): ping-pong main accumulators (a_hi*b_hi), one K chunk each
   static constexpr int kTmemCols = 4 * BN;
@@ -46,6 +47,7 @@ struct ConvCfg {
 // own accumulator, and round-to-nearest fp32 adds keep the conv
 // fp32-faithful (error at OpenBLAS-sgemm level).
 constexpr int kChunkKB = 4;
+constexpr int kPrefetchKB = 4;  // L2 prefetch distance of the A gather (K blocks)
 
 // Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ... of the
 // group (problems sorted by K descending, so long tiles go first). Every role
@@ -55,13 +57,35 @@ constexpr int kChunkKB = 4;
 // Warp roles (384 threads = 3 warpgroups; registers rebalanced with setmaxnreg):
 //   WG0 warps 0-3   A producer (im2col gather, tf32 split, swizzled st.shared)
 //   WG1 warp 4      TMEM allocator + B producer (bulk copy of the packed weight image)
-//       warp 5      MMA issuer;  warps 6-7 idle
+//       warp 5      MMA issuer
+//       warp 6      tile scheduler: resolves tile -> problem and copies the
+//                   descriptor into a 4-slot shared-memory ring ahead of use
+//       warp 7      idle
 //   WG2 warps 8-11  accumulator drain + fused epilogue (TMEM lanes 32*(warp%4) ...)
 constexpr int kThreads = 384;
 constexpr int kRegsProducer = 152, kRegsControl = 56, kRegsDrain = 256;
 
-__device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ descs, int nprob, int tile) {
-  int lo = 0, hi = nprob - 1;
+#ifdef TOBF_CONV_PROF
+// Debug-only role timing: per-role wait / busy cycle counters summed over CTAs.
+__device__ unsigned long long g_conv_prof[32];
+#define PROF_T0() const long long _p0 = clock64()
+#define PROF_ADD(slot) atomicAdd(&g_conv_prof[slot], (unsigned long long)(clock64() - _p0))
+#define PROF_WAIT(slot, expr) do { const long long _w0 = clock64(); expr; _pacc[slot] += clock64() - _w0; } while (0)
+#define PROF_DECL long long _pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define PROF_FLUSH(base) do { for (int _i = 0; _i < 8; ++_i) atomicAdd(&g_conv_prof[(base) + _i], (unsigned long long)_pacc[_i]); } while (0)
+#else
+#define PROF_T0()
+#define PROF_ADD(slot)
+#define PROF_WAIT(slot, expr) expr
+#define PROF_DECL
+#define PROF_FLUSH(base)
+#endif
+
+constexpr int kInfoSlots = 4;
+constexpr int kInfoConsumers = 4 /*A warps*/ + 1 /*B*/ + 1 /*MMA*/ + 4 /*drain warps*/;
+
+__device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ descs, int lo, int nprob, int tile) {
+  int hi = nprob - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (__ldg(&descs[mid].tile_start) <= tile) lo = mid; else hi = mid - 1;
@@ -77,12 +101,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_buf = reinterpret_cast<float*>(smem + STAGES * Cfg::kStageBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes);
+  tobf_conv_desc* info = reinterpret_cast<tobf_conv_desc*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes +
+                                                   Cfg::kInfoBytes);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain (one K chunk)
   uint64_t* acc_empty = acc_full + 2;        // [2] drain -> MMA
   uint64_t* small_empty = acc_empty + 2;     // [2] drain -> MMA (tile-slot correction accumulator)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(small_empty + 2);
+  uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
+  uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + kInfoSlots);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -96,6 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
       mbar_init(&small_empty[s], 128);
+    }
+    for (int s = 0; s < kInfoSlots; ++s) {
+      mbar_init(&info_full[s], 1);
+      mbar_init(&info_empty[s], kInfoConsumers);
     }
     fence_mbar_init();
   }
@@ -113,8 +145,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rsub = t >> 3;
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+    int it = 0;
+    PROF_DECL;
+    PROF_T0();
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      const int islot = it % kInfoSlots;
+      PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x110));
+      const tobf_conv_desc& d = info[islot];
       const int lt = tile - d.tile_start;
       const int m0 = (lt / d.ntiles) * kBM;
       const int HWo = d.Ho * d.Wo;
@@ -146,6 +183,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float* __restrict__ x = d.x;
       const int H = d.H, W = d.W, ldx = d.ldx;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
+      // L2 prefetch stream kPrefetchKB blocks ahead of the register gather:
+      // the activations of a level (all candidates) exceed L2, so the first
+      // touch of each row is a DRAM round trip. Each thread prefetches the
+      // 128-B line of one of the tile's rows (row rsub + 16*chunk) per block.
+      int pf_pix = 0, pf_y = -(1 << 28), pf_x = -(1 << 28);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i == chunk) { pf_pix = pixbase[i]; pf_y = ybase[i]; pf_x = xbase[i]; }
+      int pu = u, pv = v, pc = c0;
+      auto advance = [&](int& uu, int& vv, int& cc) {
+        cc += kBK;
+        if (cc >= Cp) {
+          const int adv = cc / Cp;
+          cc -= adv * Cp;
+          vv += adv;
+          if (vv >= k2) {
+            uu += vv / k2;
+            vv -= (vv / k2) * k2;
+          }
+        }
+      };
+      auto prefetch = [&]() {
+        const int yi = pf_y + pu, xi = pf_x + pv;
+        if (pu < k1 && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W) {
+          const float* a = x + (int64_t)(pf_pix + yi * W + xi) * ldx + pc;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        }
+        advance(pu, pv, pc);
+      };
+#pragma unroll 1
+      for (int q = 0; q < kPrefetchKB && q < kblocks; ++q) prefetch();
       // gather one K block (this thread: 8 rows x one 16-B chunk) and advance (u, v, c0)
       auto gather = [&](float4 (&vals)[8]) {
         const bool kvalid = u < k1;
@@ -179,9 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 cur[8], nxt[8];
       gather(cur);
       for (int kb = 0; kb < kblocks; ++kb) {
+        if (kb + kPrefetchKB < kblocks) prefetch();
         // the next block's loads are in flight while this one is split and stored
         if (kb + 1 < kblocks) gather(nxt);
-        mbar_wait(&empty_bar[stage], phase ^ 1, 0x101);
+        PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
         const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
         const uint32_t a_lo = a_hi + kABytes;
 #pragma unroll
@@ -203,6 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+#ifdef TOBF_CONV_PROF
+    if (t == 0) { PROF_FLUSH(0); PROF_ADD(7); }
+#endif
   } else if (warp < 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
   }
@@ -211,21 +285,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+      int it = 0;
+      PROF_DECL;
+      PROF_T0();
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+        const int islot = it % kInfoSlots;
+        PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x111));
+        const tobf_conv_desc& d = info[islot];
         const int lt = tile - d.tile_start;
         const int n_tile = lt - (lt / d.ntiles) * d.ntiles;
         const int kblocks = d.kblocks;
         const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
                               (int64_t)n_tile * kblocks * (2 * Cfg::kBBytes);
+        mbar_arrive(&info_empty[islot]);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1, 0x104);
+          PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x104));
           uint8_t* dst = smem + stage * Cfg::kStageBytes + 2 * kABytes;
           mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
           bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+#ifdef TOBF_CONV_PROF
+      PROF_FLUSH(24); PROF_ADD(31);
+#endif
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------- MMA issuer
@@ -235,20 +318,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int gc = 0;  // global chunk counter (main accumulator ping-pong)
       int it = 0;  // local tile counter (correction accumulator slot)
+      PROF_DECL;
+      PROF_T0();
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-        const int kblocks = descs[find_problem(descs, nprob, tile)].kblocks;
+        const int islot = it % kInfoSlots;
+        PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x112));
+        const int kblocks = info[islot].kblocks;
+        mbar_arrive(&info_empty[islot]);
         const int slot = it & 1;
         const uint32_t acc_small = tmem_base + slot * BN;
-        mbar_wait(&small_empty[slot], ((it >> 1) & 1) ^ 1, 0x107);
+        PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it >> 1) & 1) ^ 1, 0x107));
         tc_fence_after();
         for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
           const int buf = gc & 1;
           const uint32_t acc = tmem_base + 2 * BN + buf * BN;
-          mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106);
+          PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106));
           tc_fence_after();
           const int kend = min(kblocks, kb0 + kChunkKB);
           for (int kb = kb0; kb < kend; ++kb) {
-            mbar_wait(&full_bar[stage], phase, 0x105);
+            PROF_WAIT(3, mbar_wait(&full_bar[stage], phase, 0x105));
             tc_fence_after();
             const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
             const uint32_t a_lo = a_hi + kABytes;
@@ -269,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&acc_full[buf]);
         }
       }
+#ifdef TOBF_CONV_PROF
+      PROF_FLUSH(8); PROF_ADD(15);
+#endif
     }
   } else if (warp >= 8) {
     // ---------------------------------------------------------- drain + epilogue
@@ -276,8 +367,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lq = warp & 3;  // TMEM lane quarter this warp may access
     const int ew = warp - 8;  // 0..3
     int gc = 0, it = 0;
+    PROF_DECL;
+    PROF_T0();
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-      const tobf_conv_desc& d = descs[find_problem(descs, nprob, tile)];
+      const int islot = it % kInfoSlots;
+      PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
+      const tobf_conv_desc& d = info[islot];
       const int lt = tile - d.tile_start;
       const int m_tile = lt / d.ntiles;
       const int n_tile = lt - m_tile * d.ntiles;
@@ -291,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
       for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
         const int buf = gc & 1;
-        mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103);
+        PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103));
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + 2 * BN + buf * BN;
 #pragma unroll
@@ -330,6 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               make_float4(sum[g * 4], sum[g * 4 + 1], sum[g * 4 + 2], sum[g * 4 + 3]);
         }
       }
+#ifdef TOBF_CONV_PROF
+      const long long _e0 = clock64();
+#endif
       asm volatile("bar.sync 1, 128;" ::: "memory");
 
       const int nepi = d.nepi;
@@ -469,6 +567,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue buffer free for the next tile
+      if (lane == 0) mbar_arrive(&info_empty[islot]);
+#ifdef TOBF_CONV_PROF
+      _pacc[2] += clock64() - _e0;
+#endif
+    }
+#ifdef TOBF_CONV_PROF
+    if (ew == 0 && lane == 0) { PROF_FLUSH(16); PROF_ADD(23); }
+#endif
+  } else if (warp == 6) {
+    // ---------------------------------------------------------- tile scheduler
+    int prob = 0, it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      const int islot = it % kInfoSlots;
+      mbar_wait(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
+      prob = find_problem(descs, prob, nprob, tile);  // tiles only increase: search forward
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(info + islot);
+      constexpr int kWords = sizeof(tobf_conv_desc) / 8;
+      if (lane < kWords) dst[lane] = __ldg(src + lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&info_full[islot]);
     }
   }
 
@@ -600,6 +719,17 @@ extern "C" int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t t
   if (block_n == 64) return launch_conv<64>(d_descs, n, total_tiles, st);
   return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: block_n must be 64 or 128");
 }
+
+#ifdef TOBF_CONV_PROF
+extern "C" int tobf_conv_prof_read(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_conv_prof, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_conv_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" int tobf_check_fault(void* stream) {
   int h = 0;
