@@ -93,6 +93,152 @@ __device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ d
   return lo;
 }
 
+
+// ---------------------------------------------------------------- epilogue
+struct EpiArgs {
+  uint32_t epi_s;          // shared address of the staged fp32 tile
+  int m0, M, c, j, ldy, ldr;
+  bool cvalid;
+  float* y;
+  const float* res0;       // tensor operands of a simple chain (<= 2)
+  const float* res1;
+  int ldr1;
+  float4 sc, sh;           // the (single) folded BatchNorm of a simple chain
+};
+
+__device__ __forceinline__ float4 lds_tile(uint32_t epi_s, int row, int g, int bn) {
+  return lds128(epi_s + row * bn * 4 + ((g ^ (row & (bn / 4 - 1))) * 16));
+}
+
+// Compile-time specialised chain: PROG packs one TOBF_EPI op per nibble.
+// Lanes own 4 consecutive channels; a warp covers 32/(BN/4) rows per step,
+// kEpiUnroll steps are issued before any is consumed (loads in flight),
+// row addresses are linear in the row index (no divisions).
+constexpr int kEpiUnroll = 4;
+
+template <int BN>
+__device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt, int ew, int lane) {
+  constexpr int kLanesPerRow = BN / 4;
+  constexpr int kRowsPerIter = 32 / kLanesPerRow;
+  constexpr int kRowStep = 4 * kRowsPerIter;
+  const int sub = lane / kLanesPerRow;
+  const int g = lane % kLanesPerRow;
+  const int c = ea.c;
+  if (!ea.cvalid) return;
+  const bool cfull = c + 3 < ea.j;
+#pragma unroll 1
+  for (int r0 = ew * kRowsPerIter + sub; r0 < kBM; r0 += kRowStep * kEpiUnroll) {
+    float o[kEpiUnroll][4], ta[kEpiUnroll][4], tb[kEpiUnroll][4];
+    int mrow[kEpiUnroll];
+#pragma unroll
+    for (int q = 0; q < kEpiUnroll; ++q) {
+      const int row = r0 + q * kRowStep;
+      mrow[q] = ea.m0 + row;
+      const bool ok = row < kBM && mrow[q] < ea.M;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f), t0 = v, t1 = v;
+      if (ok) {
+        v = lds_tile(ea.epi_s, row, g, BN);
+        if (nt > 0) t0 = ldg_nc4(ea.res0 + (int64_t)mrow[q] * ea.ldr + c);
+        if (nt > 1) t1 = ldg_nc4(ea.res1 + (int64_t)mrow[q] * ea.ldr1 + c);
+      } else {
+        mrow[q] = -1;
+      }
+      o[q][0] = v.x; o[q][1] = v.y; o[q][2] = v.z; o[q][3] = v.w;
+      ta[q][0] = t0.x; ta[q][1] = t0.y; ta[q][2] = t0.z; ta[q][3] = t0.w;
+      tb[q][0] = t1.x; tb[q][1] = t1.y; tb[q][2] = t1.z; tb[q][3] = t1.w;
+    }
+    const float av[4] = {ea.sc.x, ea.sc.y, ea.sc.z, ea.sc.w};
+    const float bv[4] = {ea.sh.x, ea.sh.y, ea.sh.z, ea.sh.w};
+    // one warp-uniform branch per step for the whole batch of rows
+    int ti = 0;
+#pragma unroll 1
+    for (int s = 0; s < nsteps; ++s) {
+      const uint32_t op = (prog >> (4 * s)) & 7u;
+      if (op == TOBF_EPI_AFFINE) {
+#pragma unroll
+        for (int q = 0; q < kEpiUnroll; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[q][e] = o[q][e] * av[e] + bv[e];
+      } else if (op == TOBF_EPI_RELU) {
+#pragma unroll
+        for (int q = 0; q < kEpiUnroll; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[q][e] = fmaxf(o[q][e], 0.0f);
+      } else if (op == TOBF_EPI_ADD_TENSOR) {
+        if (ti == 0) {
+#pragma unroll
+          for (int q = 0; q < kEpiUnroll; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[q][e] += ta[q][e];
+        } else {
+#pragma unroll
+          for (int q = 0; q < kEpiUnroll; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[q][e] += tb[q][e];
+        }
+        ++ti;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kEpiUnroll; ++q) {
+      if (mrow[q] < 0) continue;
+      if (!cfull) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c + e >= ea.j) o[q][e] = 0.0f;
+      }
+      stg128(ea.y + (int64_t)mrow[q] * ea.ldy + c, make_float4(o[q][0], o[q][1], o[q][2], o[q][3]));
+    }
+  }
+}
+
+// Any other chain (several affines / operands, dummy-add constants): a
+// per-element interpreter of the descriptor's steps.
+template <int BN>
+__device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_conv_desc& d, int ew, int lane,
+                                              int HWo) {
+  constexpr int kLanesPerRow = BN / 4;
+  constexpr int kRowsPerIter = 32 / kLanesPerRow;
+  constexpr int kRowStep = 4 * kRowsPerIter;
+  const int sub = lane / kLanesPerRow;
+  const int g = lane % kLanesPerRow;
+  const int c = ea.c;
+  if (!ea.cvalid) return;
+  const int nepi = d.nepi;
+#pragma unroll 1
+  for (int row = ew * kRowsPerIter + sub; row < kBM; row += kRowStep) {
+    const int m = ea.m0 + row;
+    if (m >= ea.M) break;
+    const float4 v = lds_tile(ea.epi_s, row, g, BN);
+    float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll 1
+    for (int s = 0; s < nepi; ++s) {
+      const tobf_epi_step st = d.epi[s];
+      int64_t base = 0;
+      if (st.op == TOBF_EPI_ADD_TENSOR) base = (int64_t)m * st.aux;
+      if (st.op == TOBF_EPI_ADD_CONST) {
+        const int n_img = m / HWo;
+        base = ((int64_t)(n_img % st.aux) * HWo + (m - n_img * HWo)) * d.Cpo;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int ce = c + e;
+        switch (st.op) {
+          case TOBF_EPI_RELU: o[e] = fmaxf(o[e], 0.0f); break;
+          case TOBF_EPI_AFFINE: o[e] = o[e] * __ldg(st.ptr + ce) + __ldg(st.ptr + st.aux + ce); break;
+          case TOBF_EPI_ADD_TENSOR:
+          case TOBF_EPI_ADD_CONST: o[e] += __ldg(st.ptr + base + ce); break;
+          default: break;
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (c + e >= ea.j) o[e] = 0.0f;
+    stg128(ea.y + (int64_t)m * ea.ldy + c, make_float4(o[0], o[1], o[2], o[3]));
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tf32x3_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles) {
@@ -415,158 +561,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // Stage the tile's fp32 sums in the epilogue buffer, 16-B chunks
       // XOR-swizzled by row so the row-per-thread writes are conflict free.
+      const uint32_t epi_s = smem_u32(epi_buf);  // explicit shared-space addressing
       {
         const int row = lq * 32 + lane;
-        float* srow = epi_buf + row * BN;
+        const uint32_t srow = epi_s + row * BN * 4;
 #pragma unroll
         for (int g = 0; g < BN / 4; ++g) {
           const int gs = g ^ (row & (BN / 4 - 1));
-          *reinterpret_cast<float4*>(srow + gs * 4) =
-              make_float4(sum[g * 4], sum[g * 4 + 1], sum[g * 4 + 2], sum[g * 4 + 3]);
+          sts128(srow + gs * 16, make_float4(sum[g * 4], sum[g * 4 + 1], sum[g * 4 + 2], sum[g * 4 + 3]));
         }
       }
 #ifdef TOBF_CONV_PROF
       const long long _e0 = clock64();
 #endif
       asm volatile("bar.sync 1, 128;" ::: "memory");
+#ifdef TOBF_CONV_PROF
+      const long long _e1 = clock64();
+      _pacc[3] += _e1 - _e0;
+#endif
 
+      // ---- fused epilogue over the staged tile -----------------------------
       const int nepi = d.nepi;
-      int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI], eslot[TOBF_MAX_EPI];
+      int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI];
       const float* eptr[TOBF_MAX_EPI];
-      int naff = 0, nld = 0, cperiod = 1;
+      int naff = 0, nld = 0, nconst = 0;
+      uint32_t prog = 0;
 #pragma unroll
       for (int s = 0; s < TOBF_MAX_EPI; ++s) {
         eop[s] = s < nepi ? d.epi[s].op : TOBF_EPI_NONE;
         eaux[s] = d.epi[s].aux;
         eptr[s] = d.epi[s].ptr;
-        eslot[s] = 0;
-        if (eop[s] == TOBF_EPI_AFFINE) eslot[s] = naff++;
-        if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) eslot[s] = nld++;
-        if (eop[s] == TOBF_EPI_ADD_CONST) cperiod = eaux[s];
+        int slot = 0;
+        if (eop[s] == TOBF_EPI_AFFINE) slot = naff++;
+        if (eop[s] == TOBF_EPI_ADD_TENSOR) slot = nld++;
+        if (eop[s] == TOBF_EPI_ADD_CONST) ++nconst;
+        prog |= (uint32_t)((eop[s] & 7) | ((slot & 1) << 3)) << (4 * s);
       }
-      // Row-per-warp-iteration epilogue: lanes cover 4 consecutive channels
-      // each, so residual / constant reads and output writes are coalesced.
-      // Fast path: <= 2 affine steps and <= 2 tensor operands (every chain the
-      // lowering emits for the fixtures); longer chains take the generic path.
-      constexpr int kLanesPerRow = BN / 4;            // 32 (BN=128) or 16 (BN=64)
-      constexpr int kRowsPerIter = 32 / kLanesPerRow;  // 1 or 2
-      constexpr int kUnroll = 4;                       // independent rows in flight per lane
-      const int sub = lane / kLanesPerRow;
-      const int g = lane % kLanesPerRow;
-      const int c = n_tile * BN + g * 4;
-      const int Cpo = d.Cpo, j = d.j;
-      const bool cvalid = c < Cpo;
-      const bool fast = naff <= 2 && nld <= 2;
-      float4 sc[2], sh[2];  // per-channel affine parameters are row-invariant: load once
+      EpiArgs ea;
+      ea.epi_s = epi_s;
+      ea.m0 = m0;
+      ea.M = M;
+      ea.c = n_tile * BN + (lane % (BN / 4)) * 4;
+      ea.cvalid = ea.c < d.Cpo;
+      ea.j = d.j;
+      ea.y = d.y;
+      ea.ldy = d.ldy;
+      ea.sc = ea.sh = make_float4(0.f, 0.f, 0.f, 0.f);
+      ea.res0 = ea.res1 = nullptr;
+      ea.ldr = ea.ldr1 = 0;
+      {
+        int ti = 0;
 #pragma unroll
-      for (int a = 0; a < 2; ++a) sc[a] = sh[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-        if (fast && cvalid && eop[s] == TOBF_EPI_AFFINE) {
-          const float4 a4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + c));
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + c));
-          if (eslot[s] == 0) { sc[0] = a4; sh[0] = b4; } else { sc[1] = a4; sh[1] = b4; }
-        }
-      }
-      constexpr int kRowStep = 4 * kRowsPerIter;
-#pragma unroll 1
-      for (int r0 = ew * kRowsPerIter; r0 < kBM; r0 += kRowStep * kUnroll) {
-        float4 acc[kUnroll], opv[kUnroll][2];
-        int mrow[kUnroll];
-        int64_t cidx[kUnroll];
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          const int row = r0 + q * kRowStep + sub;
-          const int m = m0 + row;
-          mrow[q] = (row < kBM && m < M && cvalid) ? m : -1;
-          acc[q] = opv[q][0] = opv[q][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          const int n_img = mrow[q] >= 0 ? m / HWo : 0;
-          cidx[q] = ((int64_t)(n_img % cperiod) * HWo + (m - n_img * HWo)) * Cpo;
-          if (mrow[q] >= 0) {
-            const float* srow = epi_buf + row * BN;
-            acc[q] = *reinterpret_cast<const float4*>(srow + ((g ^ (row & (BN / 4 - 1))) * 4));
-            if (fast) {
-#pragma unroll
-              for (int s = 0; s < TOBF_MAX_EPI; ++s) {
-                float4 tv = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (eop[s] == TOBF_EPI_ADD_TENSOR)
-                  tv = __ldg(reinterpret_cast<const float4*>(eptr[s] + (int64_t)m * eaux[s] + c));
-                else if (eop[s] == TOBF_EPI_ADD_CONST)
-                  tv = __ldg(reinterpret_cast<const float4*>(eptr[s] + cidx[q] + c));
-                if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) {
-                  if (eslot[s] == 0) opv[q][0] = tv; else opv[q][1] = tv;
-                }
-              }
-            }
+        for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+          if (eop[s] == TOBF_EPI_AFFINE && ea.cvalid) {
+            ea.sc = __ldg(reinterpret_cast<const float4*>(eptr[s] + ea.c));
+            ea.sh = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + ea.c));
+          }
+          if (eop[s] == TOBF_EPI_ADD_TENSOR) {
+            if (ti == 0) { ea.res0 = eptr[s]; ea.ldr = eaux[s]; } else { ea.res1 = eptr[s]; ea.ldr1 = eaux[s]; }
+            ++ti;
           }
         }
-        // apply the chain step by step: one warp-uniform branch per step per
-        // batch of rows, straight-line float math inside
-        float o[kUnroll][4];
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          o[q][0] = acc[q].x; o[q][1] = acc[q].y; o[q][2] = acc[q].z; o[q][3] = acc[q].w;
-        }
-        if (fast) {
-#pragma unroll 1
-          for (int s = 0; s < nepi; ++s) {
-            const int op = d.epi[s].op;
-            const int sl = eslot[s < TOBF_MAX_EPI ? s : 0];
-            if (op == TOBF_EPI_RELU) {
-#pragma unroll
-              for (int q = 0; q < kUnroll; ++q)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) o[q][e] = fmaxf(o[q][e], 0.0f);
-            } else if (op == TOBF_EPI_AFFINE) {
-              const float4 a4 = sl == 0 ? sc[0] : sc[1];
-              const float4 b4 = sl == 0 ? sh[0] : sh[1];
-#pragma unroll
-              for (int q = 0; q < kUnroll; ++q) {
-                o[q][0] = o[q][0] * a4.x + b4.x;
-                o[q][1] = o[q][1] * a4.y + b4.y;
-                o[q][2] = o[q][2] * a4.z + b4.z;
-                o[q][3] = o[q][3] * a4.w + b4.w;
-              }
-            } else if (op == TOBF_EPI_ADD_TENSOR || op == TOBF_EPI_ADD_CONST) {
-#pragma unroll
-              for (int q = 0; q < kUnroll; ++q) {
-                const float4 t4 = sl == 0 ? opv[q][0] : opv[q][1];
-                o[q][0] += t4.x; o[q][1] += t4.y; o[q][2] += t4.z; o[q][3] += t4.w;
-              }
-            }
-          }
-        } else {
-#pragma unroll 1
-          for (int s = 0; s < nepi; ++s) {
-            const tobf_epi_step st = d.epi[s];
-#pragma unroll
-            for (int q = 0; q < kUnroll; ++q) {
-              if (mrow[q] < 0) continue;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int ce = c + e;
-                switch (st.op) {
-                  case TOBF_EPI_RELU: o[q][e] = fmaxf(o[q][e], 0.0f); break;
-                  case TOBF_EPI_AFFINE: o[q][e] = o[q][e] * __ldg(st.ptr + ce) + __ldg(st.ptr + st.aux + ce); break;
-                  case TOBF_EPI_ADD_TENSOR: o[q][e] += __ldg(st.ptr + (int64_t)mrow[q] * st.aux + ce); break;
-                  case TOBF_EPI_ADD_CONST: o[q][e] += __ldg(st.ptr + cidx[q] + ce); break;
-                  default: break;
-                }
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          if (mrow[q] < 0) continue;
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (c + e >= j) o[q][e] = 0.0f;
-          *reinterpret_cast<float4*>(d.y + (int64_t)mrow[q] * d.ldy + c) =
-              make_float4(o[q][0], o[q][1], o[q][2], o[q][3]);
-        }
       }
+#ifdef TOBF_CONV_PROF
+      const long long _e2 = clock64();
+      _pacc[4] += _e2 - _e1;
+#endif
+      // Simple chains (<= 1 folded BN, <= 2 tensor operands, no dummy
+      // constant) cover > 95% of the output volume the lowering emits for
+      // RN18 sequence candidates; anything else runs the per-element interpreter.
+      if (naff <= 1 && nld <= 2 && nconst == 0) {
+        epi_rows<BN>(ea, prog, nepi, nld, ew, lane);
+      } else {
+        epi_rows_generic<BN>(ea, d, ew, lane, HWo);
+      }
+#ifdef TOBF_CONV_PROF
+      const long long _e3 = clock64();
+      _pacc[5] += _e3 - _e2;
+#endif
       asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue buffer free for the next tile
+#ifdef TOBF_CONV_PROF
+      _pacc[6] += clock64() - _e3;
+#endif
       if (lane == 0) mbar_arrive(&info_empty[islot]);
 #ifdef TOBF_CONV_PROF
       _pacc[2] += clock64() - _e0;

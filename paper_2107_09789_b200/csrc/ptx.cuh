@@ -34,22 +34,27 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+// until the phase completes (or the hint expires) instead of spinning, so a
+// waiting role does not steal issue slots from the working warps of its SMSP.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "r"(0x989680u)
       : "memory");
   return ok != 0;
 }
 
-// Bounded wait: ~2^26 hardware-suspended try_waits is several seconds.
+// Bounded wait: each try_wait suspends up to ~10 ms, so 2^9 expiries is
+// seconds; on timeout the fault word records `code` and the kernel proceeds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int code) {
   const uint32_t addr = smem_u32(bar);
-  for (uint32_t i = 0; i < (1u << 26); ++i) {
+#pragma unroll 1
+  for (uint32_t i = 0; i < (1u << 9); ++i) {
     if (mbar_try_wait(addr, parity)) return;
   }
   atomicExch(&g_tobf_fault, code);
@@ -153,6 +158,19 @@ __device__ __forceinline__ uint32_t to_tf32_rna(float x) {
 
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+// Streaming global store (st.global, L2 only): never a generic store, so the
+// compiler and the LSU can keep shared-memory loads in flight around it.
+__device__ __forceinline__ void stg128(float* p, float4 v) {
+  asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
 

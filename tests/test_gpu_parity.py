@@ -223,3 +223,19 @@ def test_population_evaluation_matches_oracles(ctx):
         R, mean = FR.eq10(lers, T, ok, t_star, 0.02)
         assert rec["mean_ler"][i] == mean
         assert rec["reward"][i] == R
+
+
+def test_micro_batched_records_match_single_batch(ctx):
+    """evaluate_records overlaps host prep of micro-batch i+1 with the device
+    run of micro-batch i; records (incl. first-seen schedules) are identical."""
+    g = fixtures.resnet18(size=64)
+    plans = _plans(g, "sequence", 7, seed=12)
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
+    one = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=len(plans), memo={})
+    many = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=3, memo={})
+    assert one.tobytes() == many.tobytes()
+    # and the trace totals follow the reference's process-global first-seen memo order
+    memo = CM.ScheduleMemo()
+    for i, p in enumerate(plans):
+        og, d = knobs.apply_plan(g, p)
+        assert many["latency"][i] == CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)[3]
