@@ -74,9 +74,7 @@ class DeviceContext:
         """Device address of ``a[0, ..., 0]`` and ``a``'s element strides, with
         views sharing one upload of their base buffer (cached by identity;
         the base array is held so its id cannot be recycled while cached)."""
-        base = a
-        while isinstance(base.base, np.ndarray):
-            base = base.base
+        base = _root(a)
         if base.dtype == np.float32 and base.flags.c_contiguous and a.dtype == np.float32:
             key = id(base)
             hit = self.weight_cache.get(key)
@@ -115,6 +113,20 @@ class DeviceContext:
     def sync(self) -> None:
         self.stream.synchronize()
         self.check(self.lib.tobf_check_fault(C.c_void_p(self.sp)), "device pipeline")
+
+
+def _root(a: np.ndarray) -> np.ndarray:
+    """The ndarray owning ``a``'s memory, also through as_strided views (whose
+    ``.base`` is numpy's DummyArray holding the source array)."""
+    base = a
+    while True:
+        b = base.base
+        if isinstance(b, np.ndarray):
+            base = b
+        elif isinstance(getattr(b, "base", None), np.ndarray):
+            base = b.base
+        else:
+            return base
 
 
 def device(index: int | None = None) -> DeviceContext:

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .engine import Arena, DeviceContext, device
+from .engine import Arena, DeviceContext, _root, device
 from .ir import BN_EPS, Graph, OperatorKind as K, ShapeMismatch, TensorShape, analyze, shape_map, topo_order
 
 
@@ -68,6 +68,8 @@ class Op:
     a1: int = 0                # copy: src channel offset
     cc: int = 0                # copy: channel count
     level: int = 0
+    w: object = None           # gemm: fused sibling weight view (overrides node.weights)
+    j: int = 0                 # gemm: fused output channels (overrides attrs["j"])
 
 
 @dataclass
@@ -82,7 +84,86 @@ class Lowered:
 _CHAIN_KINDS = (K.BatchNorm, K.ReLU, K.Add)
 
 
-def lower(graph: Graph, analysis=None) -> Lowered:
+def _consecutive_views(ws: list, axis: int):
+    """If the arrays are consecutive slices of one buffer along ``axis`` (same
+    dtype / strides / other extents), return the merged view, else None."""
+    w0 = ws[0]
+    if not all(isinstance(w, np.ndarray) and w.dtype == np.float32 and w.ndim == w0.ndim and
+               w.strides == w0.strides for w in ws):
+        return None
+    ax = axis % w0.ndim
+    shape = list(w0.shape)
+    expect = w0.__array_interface__["data"][0]
+    total = 0
+    for w in ws:
+        if w.__array_interface__["data"][0] != expect:
+            return None
+        if any(a != b for i, (a, b) in enumerate(zip(w.shape, w0.shape)) if i != ax):
+            return None
+        expect += w.shape[ax] * w0.strides[ax]
+        total += w.shape[ax]
+    base = _root(w0)
+    if base is w0 or _root(ws[-1]) is not base:
+        return None
+    shape[ax] = total
+    return np.lib.stride_tricks.as_strided(w0, shape=tuple(shape), strides=w0.strides, writeable=False)
+
+
+def _sibling_groups(graph: Graph, order, shapes, succ) -> dict:
+    """Branch-layer siblings that one GEMM can compute (transforms.py:173-231):
+
+    out-branch  Concat of conv/linear parts reading the same input, same
+                geometry, weights = consecutive slices of one array along j
+                -> one GEMM with N = sum(j) written into the Concat buffer;
+    in-branch   Add of conv/linear parts, each reading its own channel Slice of
+                one input (consecutive, covering all channels), weights =
+                consecutive slices along c -> one GEMM with K = all channels
+                written into the Add buffer.
+    Same FLOPs as the emitted parts; returns combiner id -> (kind, parts, slices, view)."""
+    nodes = graph.nodes
+    groups = {}
+    for nid in order:
+        n = nodes[nid]
+        if len(n.inputs) < 2 or n.kind not in (K.Concat, K.Add) or (n.kind is K.Add and n.weights is not None):
+            continue
+        parts = [nodes[p] for p in n.inputs]
+        if len(set(n.inputs)) != len(n.inputs):
+            continue
+        if any(p.kind not in (K.Conv2D, K.Linear) or p.kind is not parts[0].kind or succ[p.id] != [nid]
+               for p in parts):
+            continue
+        a0 = parts[0].attrs
+        if parts[0].kind is K.Conv2D and any(
+                (p.attrs["k1"], p.attrs["k2"], p.attrs["stride"], p.attrs["padding"]) !=
+                (a0["k1"], a0["k2"], a0["stride"], a0["padding"]) for p in parts):
+            continue
+        if n.kind is K.Concat:
+            src = parts[0].inputs
+            if any(p.inputs != src for p in parts):
+                continue
+            view = _consecutive_views([p.weights for p in parts], -1)
+            if view is not None:
+                groups[nid] = ("out", [p.id for p in parts], [], view)
+        else:
+            slices = [nodes[p.inputs[0]] if len(p.inputs) == 1 else None for p in parts]
+            if any(sl is None or sl.kind is not K.Slice or succ[sl.id] != [p.id] for sl, p in zip(slices, parts)):
+                continue
+            src = slices[0].inputs
+            if any(sl.inputs != src for sl in slices):
+                continue
+            src_c = shapes[src[0]].channels if src else graph.input_shape.channels
+            bounds = [(sl.attrs["start"], sl.attrs["stop"]) for sl in slices]
+            if bounds[0][0] != 0 or bounds[-1][1] != src_c or any(bounds[i][1] != bounds[i + 1][0]
+                                                                    for i in range(len(bounds) - 1)):
+                continue
+            axis = 2 if parts[0].kind is K.Conv2D else 0
+            view = _consecutive_views([p.weights for p in parts], axis)
+            if view is not None:
+                groups[nid] = ("in", [p.id for p in parts], [sl.id for sl in slices], view)
+    return groups
+
+
+def lower(graph: Graph, analysis=None, fuse_siblings: bool = True) -> Lowered:
     """Partition a graph into device ops (host-only; no device needed)."""
     if analysis is None:
         analysis = analyze(graph)
@@ -91,6 +172,11 @@ def lower(graph: Graph, analysis=None) -> Lowered:
     covered: set[int] = set()
     ops: list[Op] = []
     produced: set[int] = set()  # value nodes already produced by an earlier op
+    groups = _sibling_groups(graph, order, shapes, succ) if fuse_siblings else {}
+    member = {}  # part / slice node -> combiner
+    for comb, (_, parts, slices, _) in groups.items():
+        for m in parts + slices:
+            member[m] = comb
 
     def absorb(op: Op, tail: int) -> int:
         """Extend op's epilogue along sole-consumer injective successors."""
@@ -127,6 +213,21 @@ def lower(graph: Graph, analysis=None) -> Lowered:
         if nid in covered:
             continue
         n = nodes[nid]
+        comb = member.get(nid)
+        if comb is not None:
+            kind, parts, slices, view = groups[comb]
+            covered.update(parts + slices + [comb])
+            head = nodes[parts[0]]
+            if kind == "out":
+                src = head.inputs[0] if head.inputs else -1
+            else:
+                sl = nodes[slices[0]]
+                src = sl.inputs[0] if sl.inputs else -1
+            op = Op("gemm", comb, src, node=parts[0], deps=[src], w=view, j=shapes[comb].channels)
+            op.out = absorb(op, comb)
+            ops.append(op)
+            produced.add(op.out)
+            continue
         src = n.inputs[0] if n.inputs else -1
         if n.kind in (K.Conv2D, K.Linear):
             op = Op("gemm", nid, src, node=nid, deps=[src])
@@ -237,9 +338,10 @@ class PopulationRun:
     def _gemm_geom(self, lw: Lowered, op: Op):
         n = lw.graph.nodes[op.node]
         s_in = self._in_shape(lw, op)
+        j = op.j or n.attrs["j"]
         if n.kind is K.Conv2D:
-            return n.attrs["k1"], n.attrs["k2"], _rup4(s_in.channels), n.attrs["j"]
-        return s_in.height, s_in.width, _rup4(s_in.channels), n.attrs["j"]
+            return n.attrs["k1"], n.attrs["k2"], _rup4(s_in.channels), j
+        return s_in.height, s_in.width, _rup4(s_in.channels), j
 
     def _stage_affines(self) -> None:
         """Fold every BatchNorm the population's epilogues use into (a, b) with
@@ -272,8 +374,7 @@ class PopulationRun:
         host = np.zeros(total, np.float32)
         for o, blk in zip(offs, blocks):
             host[o:o + blk.size] = blk
-        dev = torch.from_numpy(host).pin_memory().to(self.ctx.device, non_blocking=True)
-        self.ctx.h2d_bytes += host.nbytes
+        dev = self.ctx.upload_array(host)
         if len(cache) > 200000:
             cache.clear()
         for (key, w), o in zip(misses.items(), offs):
@@ -301,11 +402,11 @@ class PopulationRun:
         cache[id(node.weights)] = (node.weights, dev)
         return dev.data_ptr()
 
-    def _wimg(self, n, s_in: TensorShape, k1: int, k2: int, cp: int, j: int, bn: int) -> int:
+    def _wimg(self, n, s_in: TensorShape, k1: int, k2: int, cp: int, j: int, bn: int, w=None) -> int:
         """Packed tf32 hi/lo operand image of a conv/linear weight view, cached
         by (device view, geometry): one pack per distinct view per cache life."""
         ctx, lib = self.ctx, self.ctx.lib
-        wptr, st = ctx.cached_view(n.weights)
+        wptr, st = ctx.cached_view(n.weights if w is None else w)
         if n.kind is K.Conv2D:
             su, sv, sc, sn = st
         else:
@@ -360,7 +461,7 @@ class PopulationRun:
                     else:
                         stride, pad = 1, 0
                     epi = self._epi_rows(lw, bufs, op.steps)
-                    row = (bufs[op.src], self._wimg(n, s_in, k1, k2, cp, j, bn), bufs[op.out],
+                    row = (bufs[op.src], self._wimg(n, s_in, k1, k2, cp, j, bn, op.w), bufs[op.out],
                            self.batch, s_in.height, s_in.width, cp, s_out.height, s_out.width, _rup4(j), j,
                            k1, k2, stride, pad, 0, 0, 0, 0, 0, len(epi), cp, _rup4(j),
                            epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi)))
@@ -387,37 +488,41 @@ class PopulationRun:
                     cpo = _rup4(s_in.channels)
                 lvl["ew"].append((bufs[op.src], bufs[op.out]) + head +
                                  (len(epi), 0, cpo, 0, epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi))))
-        self.launches = []
-        blobs = []
+        # one structured array per op class for the whole population (numpy's
+        # nested-sequence parsing is the dominant host cost per call), then
+        # one contiguous slice per launch
+        conv_rows, conv_keys, ew_rows, ew_keys = [], [], [], []
         for lv in sorted(levels):
             grp = levels[lv]
             for key, bn in (("g128", 128), ("g64", 64)):
-                if not grp[key]:
-                    continue
-                # long-K problems first so their tiles start earliest
-                rows = [r for _, r in sorted(grp[key], key=lambda t: -t[0])]
-                arr = np.array(rows, dtype=CONV_DTYPE)
-                tot = C.c_int64()
-                ctx.check(lib.tobf_conv_prepare(C.c_void_p(arr.ctypes.data), len(rows), bn, C.byref(tot)),
-                          "conv prepare")
-                blobs.append(arr.tobytes())
-                self.launches.append(("conv", len(blobs) - 1, len(rows), tot.value, bn))
+                if grp[key]:
+                    rows = [r for _, r in sorted(grp[key], key=lambda t: -t[0])]  # long K first
+                    conv_keys.append((lv, bn, len(conv_rows), len(rows)))
+                    conv_rows += rows
             if grp["ew"]:
-                arr = np.array(grp["ew"], dtype=EW_DTYPE)
-                tot = C.c_int64()
-                ctx.check(lib.tobf_ew_prepare(C.c_void_p(arr.ctypes.data), len(arr), C.byref(tot)), "ew prepare")
-                blobs.append(arr.tobytes())
-                self.launches.append(("ew", len(blobs) - 1, len(arr), tot.value, 0))
-        offs, total = [], 0
-        for b in blobs:
-            offs.append(total)
-            total += (len(b) + 255) // 256 * 256
-        host = bytearray(total)
-        for o, b in zip(offs, blobs):
-            host[o:o + len(b)] = b
-        self.desc_dev = ctx.upload_bytes(host) if total else None
-        base = self.desc_dev.data_ptr() if total else 0
-        self.launches = [(k, base + offs[i], n, tot, bn) for (k, i, n, tot, bn) in self.launches]
+                ew_keys.append((lv, len(ew_rows), len(grp["ew"])))
+                ew_rows += grp["ew"]
+        conv_arr = np.array(conv_rows, dtype=CONV_DTYPE) if conv_rows else np.zeros(0, CONV_DTYPE)
+        ew_arr = np.array(ew_rows, dtype=EW_DTYPE) if ew_rows else np.zeros(0, EW_DTYPE)
+        launches = []
+        for lv, bn, lo, n in conv_keys:
+            tot = C.c_int64()
+            ctx.check(lib.tobf_conv_prepare(C.c_void_p(conv_arr[lo:].ctypes.data), n, bn, C.byref(tot)),
+                      "conv prepare")
+            launches.append((lv, 0, "conv", lo, n, tot.value, bn))
+        for lv, lo, n in ew_keys:
+            tot = C.c_int64()
+            ctx.check(lib.tobf_ew_prepare(C.c_void_p(ew_arr[lo:].ctypes.data), n, C.byref(tot)), "ew prepare")
+            launches.append((lv, 1, "ew", lo, n, tot.value, 0))
+        launches.sort(key=lambda t: (t[0], t[1]))
+        conv_bytes = conv_arr.tobytes()
+        pad = (-len(conv_bytes)) % 256
+        host = conv_bytes + bytes(pad) + ew_arr.tobytes()
+        self.desc_dev = ctx.upload_bytes(host) if host else None
+        base = self.desc_dev.data_ptr() if host else 0
+        ew_base = base + len(conv_bytes) + pad
+        self.launches = [(k, (base + lo * CONV_DTYPE.itemsize) if k == "conv" else (ew_base + lo * EW_DTYPE.itemsize),
+                          n, tot, bn) for (_, _, k, lo, n, tot, bn) in launches]
 
     # -------------------------------------------------------------- run
     def set_input(self, x_nchw: torch.Tensor) -> None:
@@ -462,7 +567,9 @@ class PopulationRun:
         return out
 
     def gemm_flops(self) -> int:
-        """Algorithmic conv/linear FLOPs of one run (all graphs, all reps)."""
+        """Algorithmic conv/linear FLOPs of one run (all graphs, all reps): the
+        emitted (obfuscated) layers, 2*M*N*K each; a fused sibling group counts
+        exactly the sum of its parts."""
         total = 0
         for lw in self.lowered:
             for op in lw.ops:
@@ -470,8 +577,12 @@ class PopulationRun:
                     n = lw.graph.nodes[op.node]
                     s = lw.shapes[op.node]
                     s_in = self._in_shape(lw, op)
-                    kk = (n.attrs["k1"] * n.attrs["k2"] * n.attrs["c"]) if n.kind is K.Conv2D else n.attrs["c"]
-                    total += 2 * self.batch * s.height * s.width * s.channels * kk
+                    j = op.j or n.attrs["j"]
+                    if n.kind is K.Conv2D:
+                        kk = n.attrs["k1"] * n.attrs["k2"] * s_in.channels
+                        total += 2 * self.batch * s.height * s.width * j * kk
+                    else:
+                        total += 2 * self.batch * j * s_in.channels * s_in.height * s_in.width
         return total
 
 

@@ -155,7 +155,19 @@ def schedule_signature(graph: Graph, shapes: dict, kernel: Kernel, profile: Devi
 
 
 def _numel(s: TensorShape) -> int:
-    return s.batch * s.channels * s.height * s.width
+    return s._n
+
+
+_ATTR_CANON: dict[tuple, tuple] = {}
+
+
+def canonical_attrs(attrs: dict) -> tuple:
+    """tuple(sorted(attrs.items())) (the signature's attrs part), memoised."""
+    items = tuple(attrs.items())
+    hit = _ATTR_CANON.get(items)
+    if hit is None:
+        hit = _ATTR_CANON[items] = tuple(sorted(items))
+    return hit
 
 
 def _work(graph: Graph, shapes: dict, nid: int) -> int:
@@ -301,7 +313,7 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
         for k in kernels:
             a = nodes[k.anchor]
             ins = shapes[a.inputs[0]] if a.inputs else graph.input_shape
-            sig = (pname, a.kind.value, tuple(sorted(a.attrs.items())), ins.as_tuple(), shapes[k.anchor].as_tuple())
+            sig = (pname, a.kind.value, canonical_attrs(a.attrs), ins._t, shapes[k.anchor]._t)
             if sig not in hits and sig not in local_pending:
                 hit = memo.get(sig)
                 if hit is None and a.kind not in COMPLEX_KINDS:
