@@ -1,7 +1,7 @@
 // Thin inline-PTX wrappers for the sm_100a primitives the kernels use:
 // mbarriers, bulk async copies (UBLKCP), tcgen05 MMA / TMEM traffic.
-// Every wait is bounded: on timeout the kernel records an error code in
-// g_tobf_fault and proceeds, so a protocol bug surfaces as a host-side
+// Every wait is bounded (wall time): on timeout the kernel records an error
+// code in g_tobf_fault and drains, so a protocol bug surfaces as a host-side
 // error instead of a hung GPU.
 #pragma once
 #include <cstdint>
@@ -49,13 +49,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
-// Bounded wait: each try_wait suspends up to ~10 ms, so 2^9 expiries is
-// seconds; on timeout the fault word records `code` and the kernel proceeds.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded wait. A try_wait expiry returns after ~4 us on B200 whatever the
+// suspend hint (scripts/mbar_timeout_probe.cu), so the bound is wall time:
+// kWaitLimitNs of %globaltimer (generous: profiler replay slows a kernel by
+// 100x). On timeout the fault word records `code` and the wait returns; once
+// any wait has faulted every later wait returns at once, so a broken pipeline
+// drains in microseconds instead of hanging the GPU.
+constexpr uint64_t kWaitLimitNs = 4000000000ull;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int code) {
   const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
 #pragma unroll 1
-  for (uint32_t i = 0; i < (1u << 9); ++i) {
-    if (mbar_try_wait(addr, parity)) return;
+  while (true) {
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i)
+      if (mbar_try_wait(addr, parity)) return;
+    if (*(volatile int*)&g_tobf_fault != 0) return;
+    if (globaltimer_ns() - t0 > kWaitLimitNs) break;
   }
   atomicExch(&g_tobf_fault, code);
 }

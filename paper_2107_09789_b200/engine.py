@@ -79,7 +79,7 @@ class DeviceContext:
             key = id(base)
             hit = self.weight_cache.get(key)
             if hit is None or hit[0] is not base:
-                dev = torch.from_numpy(base.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+                dev = self._pinned_copy(base)
                 self.h2d_bytes += base.nbytes
                 self._remember(key, base, dev)
             dev = self.weight_cache[key][1]
@@ -89,10 +89,17 @@ class DeviceContext:
         key = id(a)
         hit = self.weight_cache.get(key)
         if hit is None or hit[0] is not a:
-            dev = torch.from_numpy(own.reshape(-1)).pin_memory().to(self.device, non_blocking=True)
+            dev = self._pinned_copy(own)
             self.h2d_bytes += own.nbytes
             self._remember(key, a, dev)
         return self.weight_cache[key][1].data_ptr(), tuple(st // 4 for st in own.strides)
+
+    def _pinned_copy(self, a: np.ndarray) -> torch.Tensor:
+        """Stage ``a`` (possibly read-only) in pinned memory and copy it to the
+        device, stream-ordered."""
+        host = torch.empty(a.size, dtype=torch.float32, pin_memory=True)
+        host.numpy()[:] = a.reshape(-1)
+        return host.to(self.device, non_blocking=True)
 
     def _remember(self, key, base, dev) -> None:
         if self.weight_cache_bytes > self.weight_cache_limit:

@@ -46,14 +46,19 @@ def main(pop=32, reps=5):
         arr = (N.ConvDesc * n).from_buffer_copy(host[dptr - base:dptr - base + n * C.sizeof(N.ConvDesc)])
         fl = sum(2.0 * d.batch * d.Ho * d.Wo * d.j * d.k1 * d.k2 * d.Cp for d in arr)
         kmax = max(d.kblocks for d in arr)
-        rows.append((times[ci], n, tot, bn, fl, kmax, arr[0].Ho, arr[0].j))
+        kavg = sum(d.kblocks * d.mtiles * d.ntiles for d in arr) / max(tot, 1)
+        geo = sorted({(d.k1, d.Cp, d.j, d.Ho) for d in arr})
+        rows.append((times[ci], n, tot, bn, fl, kmax, arr[0].Ho, arr[0].j, ci, kavg, geo))
         ci += 1
     tot_t = sum(r[0] for r in rows)
     tot_f = sum(r[4] for r in rows)
     print(f"conv launches {len(rows)}  total {tot_t:.2f} ms  {tot_f/1e12:.3f} TFLOP(padded K)  {tot_f/tot_t/1e9:.1f} TF/s")
-    for t, n, tot, bn, fl, kmax, ho, j in sorted(rows, key=lambda r: -r[0])[:25]:
-        print(f"{t:7.3f} ms  probs {n:3d} tiles {tot:5d} BN {bn:3d} kblk_max {kmax:4d} Ho {ho:3d} j {j:4d}  "
-              f"{fl/1e9:8.1f} GF  {fl/t/1e9:6.1f} TF/s")
+    by_order = "--order" in sys.argv
+    for t, n, tot, bn, fl, kmax, ho, j, ci, kavg, geo in (rows if by_order else
+                                                          sorted(rows, key=lambda r: -r[0])[:25]):
+        print(f"#{ci:2d} {t:7.3f} ms  probs {n:3d} tiles {tot:5d} BN {bn:3d} kblk_max {kmax:4d} avg {kavg:6.1f} "
+              f"Ho {ho:3d} j {j:4d}  {fl/1e9:8.1f} GF  {fl/t/1e9:6.1f} TF/s  us/tile/SM {t * 1e3 / (tot / 148):6.2f}"
+              + (f"  (k1,Cp,j,Ho) {geo[:6]}" if by_order else ""))
 
 
 if __name__ == "__main__":
