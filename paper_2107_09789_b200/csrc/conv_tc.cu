@@ -7,16 +7,12 @@
 // into the epilogue (BatchNorm interpreter.py:54-56 folded to an affine,
 // ReLU :52, Add :59-65 incl. residual operands and dummy constants).
 //
-// One CTA computes a 128 x BN output tile of one problem of the group:
-//   warps 0-3 : im2col gather of the A tile (NHWC fp32, float4 per lane,
-//               8 lanes per 128-B row => coalesced), tf32 hi/lo split,
-//               128B-swizzled st.shared; then the epilogue (TMEM -> regs ->
-//               fused BN/ReLU/Add chain -> NHWC float4 stores)
-//   warp 4    : TMEM allocator + bulk-copy producer of the pre-packed,
-//               pre-split, pre-swizzled weight image (one UBLKCP per stage)
-//   warp 5    : single-thread tcgen05.mma issuer (M=128, N=BN, K=8 per MMA)
-// Stages are a ring of {A_hi, A_lo, B_hi, B_lo} guarded by full/empty
-// mbarriers; MMA completion frees a stage through tcgen05.commit.
+// One CTA computes 128 x BN output tiles of the group's problems (persistent,
+// warp-specialised; roles below). Operands: A (im2col of the NHWC fp32
+// activations) is gathered by cp.async into a shared staging ring, split
+// hi/lo per row and written to tensor memory; B (weights) is a pre-packed,
+// pre-split, 128B-swizzled image bulk-copied into shared memory. Each K step
+// issues three tcgen05.mma kind::tf32 with A from TMEM and B from SMEM.
 #include "ptx.cuh"
 #include "tobf_internal.h"
 
@@ -29,15 +25,32 @@ constexpr int kABytes = kBM * kRowBytes;  // 16 KB
 
 template <int BN>
 struct ConvCfg {
+  // The A tile (hi/lo) lives in tensor memory (tcgen05.st by the producer, A
+  // operand read from TMEM by the MMA); shared memory carries only B, whose
+  // three MMA reads per K step are what the tensor pipe pulls from it.
   static constexpr int kBBytes = BN * kRowBytes;
-  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kStageBytes = 2 * kBBytes;  // B hi, B lo
   static constexpr int kStages = BN >= 128 ? 2 : 4;
+  // fp32 A blocks land here by cp.async (coalesced, zero-filled padding)
+  // kStagingKB blocks ahead of the split into TMEM
+  static constexpr int kStagingKB = 4;
+  static constexpr int kStagingOff = kStages * kStageBytes;
+  static constexpr int kEpiOff = kStagingOff + kStagingKB * kABytes;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
   static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
-  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + kInfoBytes + 1024 /*align*/ + 512 /*barriers*/;
-  // [0,2BN): per-tile correction accumulators (a_lo*b_hi + a_hi*b_lo), 2 tile slots;
-  // [2BN,4BN): ping-pong main accumulators (a_hi*b_hi), one K chunk each
-  static constexpr int kTmemCols = 4 * BN;
+  static constexpr int kSmem = kEpiOff + kEpiBytes + kInfoBytes + 1024 /*align*/ + 512 /*barriers*/;
+  // TMEM columns (512 allocated):
+  //   [0, kCorrSlots*BN)           correction accumulators (a_lo*b_hi + a_hi*b_lo), per tile
+  //   next 2*BN                    ping-pong main accumulators (a_hi*b_hi), one K chunk each
+  //   kTmemACol + 64*s             A stage s: 32 hi + 32 lo columns
+  // BN=128 has room for one correction slot only: a tile's first MMA waits
+  // until the drain has read the previous tile's correction.
+  static constexpr int kCorrSlots = BN >= 128 ? 1 : 2;
+  static constexpr int kTmemMainCol = kCorrSlots * BN;
+  static constexpr int kTmemACol = kTmemMainCol + 2 * BN;
+  static constexpr int kTmemCols = 512;
+  static_assert(kTmemACol + 64 * kStages <= 512, "TMEM budget");
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
 // K blocks accumulated in TMEM before the main partial sum is drained into
@@ -47,7 +60,6 @@ struct ConvCfg {
 // own accumulator, and round-to-nearest fp32 adds keep the conv
 // fp32-faithful (error at OpenBLAS-sgemm level).
 constexpr int kChunkKB = 4;
-constexpr int kPrefetchKB = 4;  // L2 prefetch distance of the A gather (K blocks)
 
 // Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ... of the
 // group (problems sorted by K descending, so long tiles go first). Every role
@@ -55,7 +67,8 @@ constexpr int kPrefetchKB = 4;  // L2 prefetch distance of the A gather (K block
 // the tile-slot correction accumulators carry their phases across tiles, so
 // tile i+1's loads and MMAs overlap tile i's drain and epilogue.
 // Warp roles (384 threads = 3 warpgroups; registers rebalanced with setmaxnreg):
-//   WG0 warps 0-3   A producer (im2col gather, tf32 split, swizzled st.shared)
+//   WG0 warps 0-3   A producer (cp.async im2col gather into the staging ring,
+//                   tf32 hi/lo split, tcgen05.st into the TMEM A stage)
 //   WG1 warp 4      TMEM allocator + B producer (bulk copy of the packed weight image)
 //       warp 5      MMA issuer
 //       warp 6      tile scheduler: resolves tile -> problem and copies the
@@ -246,10 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int STAGES = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* epi_buf = reinterpret_cast<float*>(smem + STAGES * Cfg::kStageBytes);
-  tobf_conv_desc* info = reinterpret_cast<tobf_conv_desc*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes + Cfg::kEpiBytes +
-                                                   Cfg::kInfoBytes);
+  float* epi_buf = reinterpret_cast<float*>(smem + Cfg::kEpiOff);
+  tobf_conv_desc* info = reinterpret_cast<tobf_conv_desc*>(smem + Cfg::kEpiOff + Cfg::kEpiBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kEpiOff + Cfg::kEpiBytes + Cfg::kInfoBytes);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain (one K chunk)
   uint64_t* acc_empty = acc_full + 2;        // [2] drain -> MMA
@@ -284,142 +296,145 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp < 4) {
-    // ---------------------------------------------------------- A producer
+    // ------------------------------------------ A producer (A in tensor memory)
+    // Two cursors over this CTA's sequence of K blocks (across tiles):
+    //  issue:   lane (chunk = lane&7, rsub = lane>>3) cp.async's 16-B chunk
+    //           `chunk` of rows 32*warp + rsub + 4i (i < 8) into staging slot
+    //           (block % kStagingKB), zero-filling padding taps — 4 rows x
+    //           128 B per instruction, coalesced; kStagingKB-1 blocks ahead;
+    //  consume: thread t reads its row t (= TMEM lane t) from the slot,
+    //           splits hi/lo and tcgen05.st's 32 + 32 columns of the stage.
+    // A warp only reads rows it copied itself, so __syncwarp orders the two.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProducer));
+    constexpr int SD = Cfg::kStagingKB;
     const int t = threadIdx.x;
-    const int chunk = t & 7;
-    const int rsub = t >> 3;
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
+    const int chunk = lane & 7;
+    const int rsub = lane >> 3;
+    const uint32_t stg_s = smem_u32(smem + Cfg::kStagingOff);
     PROF_DECL;
     PROF_T0();
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-      const int islot = it % kInfoSlots;
-      PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x110));
-      const tobf_conv_desc& d = info[islot];
-      const int lt = tile - d.tile_start;
-      const int m0 = (lt / d.ntiles) * kBM;
-      const int HWo = d.Ho * d.Wo;
-      const int M = d.batch * HWo;
-      const int kblocks = d.kblocks;
-      int pixbase[8], ybase[8], xbase[8];
+    // ---- issue cursor state (current tile of the issue side)
+    int itile = blockIdx.x, iit = 0, ikb = 0, ikblocks = 0;
+    const float* x = nullptr;
+    const float* rowp[8];
+    int yb[8], xb[8];
+    int Cp = 32, k1 = 1, k2 = 1, H = 1, W = 1, ldx = 0;
+    int u = 0, v = 0, c0 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { rowp[i] = nullptr; yb[i] = xb[i] = -(1 << 28); }
+    auto ensure = [&]() -> bool {  // a K block is ready to issue (fetches the next tile's descriptor)
+      while (ikb == ikblocks) {
+        if (itile >= total_tiles) return false;
+        const int islot = iit % kInfoSlots;
+        PROF_WAIT(0, mbar_wait(&info_full[islot], (iit / kInfoSlots) & 1, 0x110));
+        const tobf_conv_desc& d = info[islot];
+        const int lt = itile - d.tile_start;
+        const int m0 = (lt / d.ntiles) * kBM + 32 * warp + rsub;
+        const int HWo = d.Ho * d.Wo;
+        const int M = d.batch * HWo;
+        ikblocks = d.kblocks;
+        Cp = d.Cp; k1 = d.k1; k2 = d.k2; H = d.H; W = d.W; ldx = d.ldx;
+        x = d.x;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + 4 * i;
+          if (m < M) {
+            const int n = m / HWo;
+            const int rem = m - n * HWo;
+            const int yo = rem / d.Wo;
+            const int xo = rem - yo * d.Wo;
+            yb[i] = yo * d.stride - d.pad;
+            xb[i] = xo * d.stride - d.pad;
+            rowp[i] = x + (int64_t)(n * H * W + yb[i] * W + xb[i]) * ldx;
+          } else {
+            yb[i] = xb[i] = -(1 << 28);  // fails every bounds test
+            rowp[i] = x;
+          }
+        }
+        u = 0; v = 0; c0 = chunk * 4;
+        while (c0 >= Cp) {
+          c0 -= Cp;
+          if (++v == k2) { v = 0; ++u; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
+        ikb = 0;
+        ++iit;
+        itile += gridDim.x;
+      }
+      return true;
+    };
+    int issued = 0;
+    auto issue = [&]() {
+      const uint32_t slot = stg_s + (issued % SD) * kABytes;
+      const int uq = u < k1 ? u : (1 << 28);  // K tail beyond k1*k2*Cp reads zeros
+      const int toff = (u * W + v) * ldx + c0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int m = m0 + rsub + 16 * i;
-        if (m < M) {
-          const int n = m / HWo;
-          const int rem = m - n * HWo;
-          const int yo = rem / d.Wo;
-          const int xo = rem - yo * d.Wo;
-          pixbase[i] = n * d.H * d.W;
-          ybase[i] = yo * d.stride - d.pad;
-          xbase[i] = xo * d.stride - d.pad;
-        } else {
-          pixbase[i] = 0;
-          ybase[i] = -(1 << 28);  // forces the bounds test to fail
-          xbase[i] = -(1 << 28);
+        const int r = 32 * warp + rsub + 4 * i;
+        const bool ok = (unsigned)(yb[i] + uq) < (unsigned)H && (unsigned)(xb[i] + v) < (unsigned)W;
+        cp_async16(slot + r * kRowBytes + ((chunk ^ (r & 7)) << 4), ok ? rowp[i] + toff : x, ok ? 16u : 0u);
+      }
+      if (Cp >= kBK) {          // Cp % 32 == 0 or a single wrap
+        c0 += kBK;
+        if (c0 >= Cp) {
+          c0 -= Cp;
+          if (++v == k2) { v = 0; ++u; }
+        }
+      } else {                  // Cp in {4, 8, 16, ...}: step 32/Cp filter taps
+        c0 += kBK;
+        const int adv = c0 / Cp;
+        c0 -= adv * Cp;
+        v += adv;
+        if (v >= k2) {
+          u += v / k2;
+          v -= (v / k2) * k2;
         }
       }
-      const int Cp = d.Cp, k1 = d.k1, k2 = d.k2;
-      int u = 0, v = 0, c0 = chunk * 4;
-      while (c0 >= Cp) {
-        c0 -= Cp;
-        if (++v == k2) { v = 0; ++u; }
-      }
-      const float* __restrict__ x = d.x;
-      const int H = d.H, W = d.W, ldx = d.ldx;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
-      // L2 prefetch stream kPrefetchKB blocks ahead of the register gather:
-      // the activations of a level (all candidates) exceed L2, so the first
-      // touch of each row is a DRAM round trip. Each thread prefetches the
-      // 128-B line of one of the tile's rows (row rsub + 16*chunk) per block.
-      int pf_pix = 0, pf_y = -(1 << 28), pf_x = -(1 << 28);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i == chunk) { pf_pix = pixbase[i]; pf_y = ybase[i]; pf_x = xbase[i]; }
-      int pu = u, pv = v, pc = c0;
-      auto advance = [&](int& uu, int& vv, int& cc) {
-        cc += kBK;
-        if (cc >= Cp) {
-          const int adv = cc / Cp;
-          cc -= adv * Cp;
-          vv += adv;
-          if (vv >= k2) {
-            uu += vv / k2;
-            vv -= (vv / k2) * k2;
-          }
-        }
-      };
-      auto prefetch = [&]() {
-        const int yi = pf_y + pu, xi = pf_x + pv;
-        if (pu < k1 && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W) {
-          const float* a = x + (int64_t)(pf_pix + yi * W + xi) * ldx + pc;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-        }
-        advance(pu, pv, pc);
-      };
+      ++ikb;
+      ++issued;
+    };
 #pragma unroll 1
-      for (int q = 0; q < kPrefetchKB && q < kblocks; ++q) prefetch();
-      // gather one K block (this thread: 8 rows x one 16-B chunk) and advance (u, v, c0)
-      auto gather = [&](float4 (&vals)[8]) {
-        const bool kvalid = u < k1;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int yi = ybase[i] + u;
-          const int xi = xbase[i] + v;
-          if (kvalid && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W) {
-            vals[i] = ldg_nc4(x + (int64_t)(pixbase[i] + yi * W + xi) * ldx + c0);
-          } else {
-            vals[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-        if (Cp >= kBK) {          // Cp % 32 == 0 or a single wrap
-          c0 += kBK;
-          if (c0 >= Cp) {
-            c0 -= Cp;
-            if (++v == k2) { v = 0; ++u; }
-          }
-        } else {                  // Cp in {4, 8, 16, ...}: step 32/Cp filter taps
-          c0 += kBK;
-          const int adv = c0 / Cp;
-          c0 -= adv * Cp;
-          v += adv;
-          if (v >= k2) {
-            u += v / k2;
-            v -= (v / k2) * k2;
-          }
-        }
-      };
-      float4 cur[8], nxt[8];
-      gather(cur);
-      for (int kb = 0; kb < kblocks; ++kb) {
-        if (kb + kPrefetchKB < kblocks) prefetch();
-        // the next block's loads are in flight while this one is split and stored
-        if (kb + 1 < kblocks) gather(nxt);
-        PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
-        const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
-        const uint32_t a_lo = a_hi + kABytes;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = rsub + 16 * i;
-          const uint32_t off = sw128_off(r, chunk);
-          float4 h, l;
-          h.x = __uint_as_float(to_tf32_rna(cur[i].x)); l.x = cur[i].x - h.x;
-          h.y = __uint_as_float(to_tf32_rna(cur[i].y)); l.y = cur[i].y - h.y;
-          h.z = __uint_as_float(to_tf32_rna(cur[i].z)); l.z = cur[i].z - h.z;
-          h.w = __uint_as_float(to_tf32_rna(cur[i].w)); l.w = cur[i].w - h.w;
-          sts128(a_hi + off, h);
-          sts128(a_lo + off, l);
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&full_bar[stage]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
+    for (int q = 0; q < SD - 1; ++q) {
+      if (ensure()) issue();
+      cp_async_commit();
     }
+    int stage = 0;
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int g = 0;; ++g) {
+      __syncwarp();  // every lane is done reading the slot about to be refilled
+      if (ensure()) issue();
+      cp_async_commit();  // one group per block (empty past the end): group g holds block g
+      if (g >= issued) break;
+      PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
+      const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
+      float4 row[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
+      tc_fence_after();
+      const uint32_t ta = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + Cfg::kTmemACol + stage * 64;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float hh[16], ll[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a = row[half * 4 + q];
+          hh[4 * q + 0] = tf32_rna_finite(a.x); ll[4 * q + 0] = a.x - hh[4 * q + 0];
+          hh[4 * q + 1] = tf32_rna_finite(a.y); ll[4 * q + 1] = a.y - hh[4 * q + 1];
+          hh[4 * q + 2] = tf32_rna_finite(a.z); ll[4 * q + 2] = a.z - hh[4 * q + 2];
+          hh[4 * q + 3] = tf32_rna_finite(a.w); ll[4 * q + 3] = a.w - hh[4 * q + 3];
+        }
+        tmem_st16(ta + half * 16, hh);
+        tmem_st16(ta + 32 + half * 16, ll);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&full_bar[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF
     if (t == 0) { PROF_FLUSH(0); PROF_ADD(7); }
 #endif
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&info_empty[islot]);
         for (int kb = 0; kb < kblocks; ++kb) {
           PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x104));
-          uint8_t* dst = smem + stage * Cfg::kStageBytes + 2 * kABytes;
+          uint8_t* dst = smem + stage * Cfg::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
           bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -458,55 +473,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_make(2u /*tf32*/, kBM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int gc = 0;  // global chunk counter (main accumulator ping-pong)
-      int it = 0;  // local tile counter (correction accumulator slot)
-      PROF_DECL;
-      PROF_T0();
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-        const int islot = it % kInfoSlots;
-        PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x112));
-        const int kblocks = info[islot].kblocks;
-        mbar_arrive(&info_empty[islot]);
-        const int slot = it & 1;
-        const uint32_t acc_small = tmem_base + slot * BN;
-        PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it >> 1) & 1) ^ 1, 0x107));
+    // The whole warp runs the schedule so stage addresses, descriptors and
+    // TMEM addresses are warp-uniform (uniform registers: no per-MMA
+    // register->uniform broadcast loop); one elected lane issues.
+    constexpr uint32_t idesc = idesc_make(2u /*tf32*/, kBM, BN);
+    const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int gc = 0;  // global chunk counter (main accumulator ping-pong)
+    int it = 0;  // local tile counter (correction accumulator slot)
+    PROF_DECL;
+    PROF_T0();
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      const int islot = it % kInfoSlots;
+      PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x112));
+      const int kblocks = __shfl_sync(0xffffffffu, info[islot].kblocks, 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&info_empty[islot]);
+      const int slot = it % Cfg::kCorrSlots;
+      const uint32_t acc_small = tb + slot * BN;
+      PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it / Cfg::kCorrSlots) & 1) ^ 1, 0x107));
+      tc_fence_after();
+      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
+        const int buf = gc & 1;
+        const uint32_t acc = tb + Cfg::kTmemMainCol + buf * BN;
+        PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106));
         tc_fence_after();
-        for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
-          const int buf = gc & 1;
-          const uint32_t acc = tmem_base + 2 * BN + buf * BN;
-          PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106));
+        const int kend = min(kblocks, kb0 + kChunkKB);
+        for (int kb = kb0; kb < kend; ++kb) {
+          PROF_WAIT(3, mbar_wait(&full_bar[stage], phase, 0x105));
           tc_fence_after();
-          const int kend = min(kblocks, kb0 + kChunkKB);
-          for (int kb = kb0; kb < kend; ++kb) {
-            PROF_WAIT(3, mbar_wait(&full_bar[stage], phase, 0x105));
-            tc_fence_after();
-            const uint32_t a_hi = smem_u32(smem + stage * Cfg::kStageBytes);
-            const uint32_t a_lo = a_hi + kABytes;
-            const uint32_t b_hi = a_hi + 2 * kABytes;
-            const uint32_t b_lo = b_hi + Cfg::kBBytes;
+          const uint32_t b_hi = sbase + stage * Cfg::kStageBytes;
+          const uint32_t b_lo = b_hi + Cfg::kBBytes;
+          const uint32_t ta = tb + Cfg::kTmemACol + stage * 64;  // A hi columns, lo at +32
+          if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 8; ++kk) {
               const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-              const uint64_t dah = sdesc_k128(a_hi + koff), dal = sdesc_k128(a_lo + koff);
               const uint64_t dbh = sdesc_k128(b_hi + koff), dbl = sdesc_k128(b_lo + koff);
-              mma_tf32(acc_small, dal, dbh, idesc, (kb | kk) != 0);
-              mma_tf32(acc_small, dah, dbl, idesc, 1u);
-              mma_tf32(acc, dah, dbh, idesc, (kb - kb0 | kk) != 0);
+              mma_tf32_ts(acc_small, ta + 32 + kk * 8, dbh, idesc, (kb | kk) != 0);
+              mma_tf32_ts(acc_small, ta + kk * 8, dbl, idesc, 1u);
+              mma_tf32_ts(acc, ta + kk * 8, dbh, idesc, (kb - kb0 | kk) != 0);
             }
             mma_commit(&empty_bar[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&acc_full[buf]);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (elect_one()) mma_commit(&acc_full[buf]);
+        __syncwarp();
       }
-#ifdef TOBF_CONV_PROF
-      PROF_FLUSH(8); PROF_ADD(15);
-#endif
     }
+#ifdef TOBF_CONV_PROF
+    if (lane == 0) { PROF_FLUSH(8); PROF_ADD(15); }
+#endif
   } else if (warp >= 8) {
     // ---------------------------------------------------------- drain + epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsDrain));
@@ -517,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     PROF_T0();
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       const int islot = it % kInfoSlots;
-      PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
+      PROF_WAIT(0, mbar_wait_backoff(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
       const tobf_conv_desc& d = info[islot];
       const int lt = tile - d.tile_start;
       const int m_tile = lt / d.ntiles;
@@ -526,15 +547,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int HWo = d.Ho * d.Wo;
       const int M = d.batch * HWo;
       const int kblocks = d.kblocks;
-      const int slot = it & 1;
+      const int slot = it % Cfg::kCorrSlots;
       float sum[BN];
 #pragma unroll
       for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
       for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
         const int buf = gc & 1;
-        PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103));
+        PROF_WAIT(1, mbar_wait_backoff(&acc_full[buf], (gc >> 1) & 1, 0x103));
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + 2 * BN + buf * BN;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + Cfg::kTmemMainCol + buf * BN;
 #pragma unroll
         for (int cc = 0; cc < BN / 16; ++cc) {
           float part[16];
@@ -656,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int prob = 0, it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       const int islot = it % kInfoSlots;
-      mbar_wait(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
+      mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
       prob = find_problem(descs, prob, nprob, tile);  // tiles only increase: search forward
       const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
       uint64_t* dst = reinterpret_cast<uint64_t*>(info + islot);

@@ -77,6 +77,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int co
   atomicExch(&g_tobf_fault, code);
 }
 
+// Bounded wait with exponential nanosleep backoff (64 ns .. 1 us) between
+// polls: for roles whose waits are long and off the critical path (drain
+// warps waiting for a K chunk, the tile scheduler waiting for a free slot),
+// so that spinning does not steal issue slots from the producer warps that
+// share their SM sub-partitions.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int code) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 64;
+#pragma unroll 1
+  while (true) {
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+      __nanosleep(ns);
+      if (mbar_try_wait(addr, parity)) return;
+      ns = ns < 1024 ? 2 * ns : 1024;
+    }
+    if (*(volatile int*)&g_tobf_fault != 0) return;
+    if (globaltimer_ns() - t0 > kWaitLimitNs) break;
+  }
+  atomicExch(&g_tobf_fault, code);
+}
+
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -137,6 +172,31 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// A operand from tensor memory (M=128: row i = TMEM lane i, one tf32 per
+// 32-bit column), B from shared memory.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 16 consecutive 32-bit columns of this thread's TMEM lane (warp w may
+// address lanes 32*(w%4) .. +31). Asynchronous: tmem_wait_st() before the
+// data is signalled to the MMA issuer.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::
+          "r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -171,6 +231,23 @@ __device__ __forceinline__ uint32_t to_tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
+}
+
+// cvt.rna.tf32.f32 for finite inputs in two integer ops (ptxas expands the
+// cvt with an Inf/NaN guard): round the magnitude half-up at bit 13, clear
+// the 13 low mantissa bits. x - result is exact in fp32.
+__device__ __forceinline__ float tf32_rna_finite(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// 16-B global -> shared async copy (L2 only); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
