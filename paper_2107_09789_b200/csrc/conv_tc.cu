@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int g = 0;; ++g) {
       __syncwarp();  // every lane is done reading the slot about to be refilled
-      if (ensure()) issue();
+      PROF_WAIT(4, if (ensure()) issue());
       cp_async_commit();  // one group per block (empty past the end): group g holds block g
       if (g >= issued) break;
       PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st16(ta + half * 16, hh);
         tmem_st16(ta + 32 + half * 16, ll);
       }
-      tmem_wait_st();
+      PROF_WAIT(3, tmem_wait_st());
       tc_fence_before();
       mbar_arrive(&full_bar[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -538,7 +538,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     PROF_T0();
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       const int islot = it % kInfoSlots;
-      PROF_WAIT(0, mbar_wait_backoff(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
+      // one drain warp polls, the other three sleep in the named barrier
+      // (polling warps take issue slots from the producers on their SMSPs)
+      if (ew == 0) PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
+      asm volatile("bar.sync 2, 128;" ::: "memory");
       const tobf_conv_desc& d = info[islot];
       const int lt = tile - d.tile_start;
       const int m_tile = lt / d.ntiles;
@@ -553,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
       for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
         const int buf = gc & 1;
-        PROF_WAIT(1, mbar_wait_backoff(&acc_full[buf], (gc >> 1) & 1, 0x103));
+        if (ew == 0) PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103));
+        asm volatile("bar.sync 2, 128;" ::: "memory");
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + Cfg::kTmemMainCol + buf * BN;
 #pragma unroll

@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2107_09789_b200 import fixtures, ga  # noqa: E402
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator  # noqa: E402
 
-NAMES = {0: "A.info", 1: "A.empty", 2: "A.cpw", 7: "A.total", 8: "M.info", 9: "M.small", 10: "M.accE", 11: "M.full",
+NAMES = {0: "A.info", 1: "A.empty", 2: "A.cpw", 3: "A.stw", 4: "A.issue", 7: "A.total", 8: "M.info", 9: "M.small", 10: "M.accE", 11: "M.full",
          15: "M.total", 16: "D.info", 17: "D.accF", 18: "D.epi", 19: "D.bar1", 20: "D.setup", 21: "D.rows",
          22: "D.bar2", 23: "D.total", 24: "B.info", 25: "B.empty",
          31: "B.total"}
@@ -35,7 +35,7 @@ def main():
     lib.tobf_conv_prof_read(buf.ctypes.data, 1)
     sp = C.c_void_p(pe.ctx.sp)
     convs = [L for L in run.launches if L[0] == "conv"]
-    for idx in (0, 1, 2, 3, 5, 10, 20, 40, 60, 80):
+    for idx in (0, 1, 4, 14, 20, 22, 29, 34, 38, 44):
         if idx >= len(convs):
             break
         _, dptr, n, tot, bn = convs[idx]
