@@ -282,242 +282,400 @@ def lower(graph: Graph, analysis=None, fuse_siblings: bool = True) -> Lowered:
 
 
 # ---------------------------------------------------------------------------
-# Population run: allocate, pack, describe, launch
+# Forward plans: one graph's forward as descriptor rows with SYMBOLIC
+# pointers (host only, picklable — built in worker processes for a
+# population), linked to device memory and launched by PopulationRun
 # ---------------------------------------------------------------------------
 
 CONV_DTYPE = np.dtype(N.ConvDesc)
 EW_DTYPE = np.dtype(N.EwDesc)
 _NO_EPI = (0, 0, 0)
 
+# A symbolic pointer is (space << 56) | value: value = byte offset into the
+# graph's activation block (SP_ARENA) or an index into one of the plan's
+# requirement tables (packed weight images, folded BatchNorms, constants).
+SP_INPUT, SP_ARENA, SP_WIMG, SP_AFFINE, SP_CONST = 1, 2, 3, 4, 5
+_SP_SHIFT = 56
+_SP_LOW = (1 << _SP_SHIFT) - 1
+
+
+def _sym(space: int, value: int) -> int:
+    return (space << _SP_SHIFT) | value
+
+
+class ArrayRefs:
+    """Host arrays <-> hashable references ``(root_key, byte_offset, shape,
+    strides)``. In process a root is keyed by identity; the worker-side
+    registry (hostpipe.py) names roots its parent can rebuild instead."""
+
+    def __init__(self):
+        self._roots: dict = {}
+
+    def root_key(self, root: np.ndarray):
+        key = ("id", id(root))
+        self._roots[key] = root
+        return key
+
+    def root(self, key) -> np.ndarray:
+        return self._roots[key]
+
+    def ref(self, a: np.ndarray) -> tuple:
+        r = _root(a)
+        off = a.__array_interface__["data"][0] - r.__array_interface__["data"][0]
+        return (self.root_key(r), off, a.shape, a.strides)
+
+    def resolve(self, ref: tuple) -> np.ndarray:
+        key, off, shape, strides = ref
+        r = self.root(key)
+        if off == 0 and shape == r.shape and strides == r.strides:
+            return r
+        return np.ndarray(shape, r.dtype, buffer=r, offset=off, strides=strides)
+
+
+@dataclass
+class ForwardPlan:
+    """conv/ew: descriptor rows (symbolic pointers) with their launch keys
+    (dependency level, BN, K); wimg/affine/const: requirement tables;
+    arena_bytes: the graph's activation block; out_off: its output value."""
+
+    conv: np.ndarray
+    conv_level: np.ndarray
+    conv_bn: np.ndarray
+    conv_k: np.ndarray
+    ew: np.ndarray
+    ew_level: np.ndarray
+    wimg: list      # (weight ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn)
+    affine: list    # BatchNorm weight ref
+    const: list     # (constant ref, b0, channels, h, w, cp)
+    arena_bytes: int
+    out_off: int
+    out_shape: TensorShape
+    input_shape: TensorShape
+    flops_per_image: int
+
+
+def _gemm_geom(lw: Lowered, op: Op, s_in: TensorShape):
+    n = lw.graph.nodes[op.node]
+    j = op.j or n.attrs["j"]
+    if n.kind is K.Conv2D:
+        return n.attrs["k1"], n.attrs["k2"], _rup4(s_in.channels), j
+    return s_in.height, s_in.width, _rup4(s_in.channels), j
+
+
+def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
+    """Descriptor rows of one lowered graph for ``reps`` stacked trials."""
+    graph, shapes, nodes = lw.graph, lw.shapes, lw.graph.nodes
+    ishape = graph.input_shape
+    batch = ishape.batch * reps
+    offs: dict[int, int] = {}
+    used = 0
+    for v in sorted(lw.values):
+        sh = shapes[v]
+        offs[v] = used
+        used += 4 * Arena.round(batch * sh.height * sh.width * _rup4(sh.channels))
+
+    def buf(v: int) -> int:
+        return _sym(SP_INPUT, 0) if v < 0 else _sym(SP_ARENA, offs[v])
+
+    tables: dict[str, tuple[dict, list]] = {"wimg": ({}, []), "affine": ({}, []), "const": ({}, [])}
+
+    def index(table: str, entry) -> int:
+        idx, lst = tables[table]
+        i = idx.get(entry)
+        if i is None:
+            i = idx[entry] = len(lst)
+            lst.append(entry)
+        return i
+
+    def epi_rows(steps: list) -> list:
+        out = []
+        for st in steps:
+            if st.op == "affine":
+                out.append((N.EPI_AFFINE, _rup4(shapes[st.ref].channels),
+                            _sym(SP_AFFINE, index("affine", refs.ref(nodes[st.ref].weights)))))
+            elif st.op == "relu":
+                out.append((N.EPI_RELU, 0, 0))
+            elif st.op == "add":
+                sh = shapes[st.ref] if st.ref >= 0 else ishape
+                out.append((N.EPI_ADD_TENSOR, _rup4(sh.channels), buf(st.ref)))
+            elif st.op == "const":
+                sh = shapes[st.ref]
+                entry = (refs.ref(nodes[st.ref].weights), ishape.batch, sh.channels, sh.height, sh.width,
+                         _rup4(sh.channels))
+                out.append((N.EPI_ADD_CONST, ishape.batch, _sym(SP_CONST, index("const", entry))))
+        return out + [_NO_EPI] * (N.TOBF_MAX_EPI - len(out))
+
+    conv_rows, conv_lv, conv_bn, conv_k = [], [], [], []
+    ew_rows, ew_lv = [], []
+    flops = 0
+    for op in lw.ops:
+        s_in = shapes[op.src] if op.src >= 0 else ishape
+        s_out = shapes[op.out]
+        if op.kind == "gemm":
+            n = nodes[op.node]
+            k1, k2, cp, j = _gemm_geom(lw, op, s_in)
+            bn = 128 if j > 64 else 64
+            if n.kind is K.Conv2D:
+                stride, pad = n.attrs["stride"], n.attrs["padding"]
+                flops += 2 * ishape.batch * shapes[op.node].height * shapes[op.node].width * j * k1 * k2 * s_in.channels
+            else:
+                stride, pad = 1, 0
+                flops += 2 * ishape.batch * j * s_in.channels * s_in.height * s_in.width
+            w = n.weights if op.w is None else op.w
+            wi = index("wimg", (refs.ref(w), n.kind is K.Conv2D, s_in.height, s_in.width, s_in.channels,
+                                k1, k2, cp, j, bn))
+            epi = epi_rows(op.steps)
+            conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
+                              s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
+                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi))
+            conv_lv.append(op.level)
+            conv_bn.append(bn)
+            conv_k.append(k1 * k2 * cp)
+            continue
+        ldx, ldy = _rup4(s_in.channels), _rup4(s_out.channels)
+        epi = [_NO_EPI] * N.TOBF_MAX_EPI
+        nepi = 0
+        if op.kind == "pool":
+            n = nodes[op.node]
+            head = (N.OP_MAXPOOL, batch, s_in.height, s_in.width, s_in.channels, ldx, s_out.height,
+                    s_out.width, ldy, n.attrs["window"], n.attrs["stride"])
+            cpo = _rup4(s_in.channels)
+        elif op.kind == "epi":
+            epi = epi_rows(op.steps)
+            nepi = sum(1 for e in epi if e[0])
+            head = (N.OP_EPI, batch, s_in.height, s_in.width, s_out.channels, ldx, s_out.height,
+                    s_out.width, ldy, 0, 0)
+            cpo = _rup4(s_out.channels)
+        elif op.kind == "copy":
+            total = s_out.channels
+            head = (N.OP_COPYCH, batch, s_in.height, s_in.width, op.cc, ldx, 0, 0, ldy, op.a0, op.a1)
+            cpo = _rup4(total) if op.a0 + op.cc == total else op.a0 + op.cc
+        else:  # softmax
+            head = (N.OP_SOFTMAX, batch, s_in.height, s_in.width, s_in.channels, ldx, 0, 0, ldy, 0, 0)
+            cpo = _rup4(s_in.channels)
+        ew_rows.append((buf(op.src), buf(op.out)) + head + (nepi, 0, cpo, 0, epi))
+        ew_lv.append(op.level)
+    return ForwardPlan(
+        conv=np.array(conv_rows, dtype=CONV_DTYPE) if conv_rows else np.zeros(0, CONV_DTYPE),
+        conv_level=np.array(conv_lv, np.int32), conv_bn=np.array(conv_bn, np.int32),
+        conv_k=np.array(conv_k, np.int64),
+        ew=np.array(ew_rows, dtype=EW_DTYPE) if ew_rows else np.zeros(0, EW_DTYPE),
+        ew_level=np.array(ew_lv, np.int32),
+        wimg=tables["wimg"][1], affine=tables["affine"][1], const=tables["const"][1],
+        arena_bytes=used, out_off=offs[lw.out_node], out_shape=shapes[lw.out_node], input_shape=ishape,
+        flops_per_image=flops)
+
+
+def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, tables: dict) -> np.ndarray:
+    """Symbolic -> device pointers for one pointer column (rows x k), rows of
+    several plans at once (row_plan = plan index of each row)."""
+    col = col.astype(np.uint64, copy=False)
+    space = (col >> np.uint64(_SP_SHIFT)).astype(np.int64)
+    val = (col & np.uint64(_SP_LOW)).astype(np.int64)
+    rp = row_plan.reshape((-1,) + (1,) * (col.ndim - 1))
+    rp = np.broadcast_to(rp, col.shape)
+    out = np.zeros(col.shape, np.uint64)
+    m = space == SP_INPUT
+    out[m] = np.uint64(x_ptr)
+    m = space == SP_ARENA
+    out[m] = (arena[rp[m]] + val[m]).astype(np.uint64)
+    for sp, (ptrs, offsets) in tables.items():
+        m = space == sp
+        if m.any():
+            out[m] = ptrs[offsets[rp[m]] + val[m]]
+    return out
+
 
 class PopulationRun:
-    """Runs the forward of several lowered graphs on the same stacked input.
+    """Runs the forward of several graphs on the same stacked input.
 
-    Host preparation is table-driven: descriptor rows are numpy records
-    (one H2D for all levels), packed weight images are cached per weight
-    view (every candidate that reuses a vanilla layer — or a branch slice of
-    it, or a shared knob constant — shares one image), activations live in
-    one arena reused across runs on the engine stream.
+    Each graph is a ForwardPlan (built here, or in host worker processes);
+    linking resolves the plans' requirement tables — packed weight images
+    cached per weight view (every candidate that reuses a vanilla layer, a
+    branch slice of it or a shared knob constant shares one image), folded
+    BatchNorms, staged constants — lays the activation blocks out in one
+    arena reused across runs, rewrites every symbolic pointer with
+    vectorised numpy, groups rows into one launch per (level, BN) / level,
+    and uploads all descriptors in one H2D.
     """
 
     conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
 
-    def __init__(self, ctx: DeviceContext, lowered: list[Lowered], reps: int):
+    def __init__(self, ctx: DeviceContext, lowered: list[Lowered] | None, reps: int,
+                 plans: list[ForwardPlan] | None = None, refs: ArrayRefs | None = None):
         self.ctx = ctx
-        self.lowered = lowered
         self.reps = reps
-        self._keep: list = []
-        g0 = lowered[0].graph
-        for lw in lowered:
-            if lw.graph.input_shape != g0.input_shape:
+        if plans is None:
+            refs = ArrayRefs()
+            plans = [plan_forward(lw, reps, refs) for lw in lowered]
+        self.plans, self.refs = plans, refs
+        ishape = plans[0].input_shape
+        for p in plans:
+            if p.input_shape != ishape:
                 raise ShapeMismatch(-1, "population graphs disagree on the input shape")
-        ishape = g0.input_shape
+        self.input_shape = ishape
         self.batch = ishape.batch * reps
-        act = Arena.round(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
-        for lw in lowered:
-            for v in lw.values:
-                sh = lw.shapes[v]
-                act += Arena.round(self.batch * sh.height * sh.width * _rup4(sh.channels))
-        self.arena = ctx_arena(ctx, act + 4096)
-        self.x_ptr = self.arena.take(self.batch * ishape.height * ishape.width * _rup4(ishape.channels))
-        self.bufs: list[dict[int, int]] = []
-        for lw in lowered:
-            b = {-1: self.x_ptr}
-            for v in sorted(lw.values):
-                sh = lw.shapes[v]
-                b[v] = self.arena.take(self.batch * sh.height * sh.width * _rup4(sh.channels))
-            self.bufs.append(b)
-        self._stage_affines()
-        self._prepare()
+        self._link_all()
 
-    # -------------------------------------------------------------- helpers
-    @staticmethod
-    def _in_shape(lw: Lowered, op: Op) -> TensorShape:
-        return lw.shapes[op.src] if op.src >= 0 else lw.graph.input_shape
-
-    def _gemm_geom(self, lw: Lowered, op: Op):
-        n = lw.graph.nodes[op.node]
-        s_in = self._in_shape(lw, op)
-        j = op.j or n.attrs["j"]
-        if n.kind is K.Conv2D:
-            return n.attrs["k1"], n.attrs["k2"], _rup4(s_in.channels), j
-        return s_in.height, s_in.width, _rup4(s_in.channels), j
-
-    def _stage_affines(self) -> None:
-        """Fold every BatchNorm the population's epilogues use into (a, b) with
-        a = scale/sqrt(var+eps), b = shift - mean*a (fp64 -> fp32), caching the
-        device copy by weight-array identity; all misses go up in ONE H2D."""
-        cache = self.ctx.__dict__.setdefault("affine_cache", {})
-        misses: dict[int, np.ndarray] = {}
-        for lw in self.lowered:
-            for op in lw.ops:
-                for st in op.steps:
-                    if st.op == "affine":
-                        w = lw.graph.nodes[st.ref].weights
-                        hit = cache.get(id(w))
-                        if (hit is None or hit[0] is not w) and id(w) not in misses:
-                            misses[id(w)] = w
-        if not misses:
-            return
-        blocks, offs, total = [], [], 0
-        for w in misses.values():
-            w64 = w.astype(np.float64)
-            a = w64[0] / np.sqrt(w64[3] + BN_EPS)
-            b = w64[1] - w64[2] * a
-            cp = _rup4(w.shape[1])
-            blk = np.zeros((2, cp), np.float32)
-            blk[0, :w.shape[1]] = a
-            blk[1, :w.shape[1]] = b
-            offs.append(total)
-            blocks.append(blk.reshape(-1))
-            total += Arena.round(2 * cp)
-        host = np.zeros(total, np.float32)
-        for o, blk in zip(offs, blocks):
-            host[o:o + blk.size] = blk
-        dev = self.ctx.upload_array(host)
-        if len(cache) > 200000:
-            cache.clear()
-        for (key, w), o in zip(misses.items(), offs):
-            cache[key] = (w, dev, dev.data_ptr() + 4 * o)
-
-    def _affine(self, lw: Lowered, nid: int) -> int:
-        return self.ctx.affine_cache[id(lw.graph.nodes[nid].weights)][2]
-
-    def _const(self, lw: Lowered, nid: int) -> int:
-        """Dummy-add constant in NHWC-padded layout, cached per array."""
-        node = lw.graph.nodes[nid]
-        cache = self.ctx.__dict__.setdefault("const_cache", {})
-        hit = cache.get(id(node.weights))
-        if hit is not None and hit[0] is node.weights:
-            return hit[1].data_ptr()
-        sh = lw.shapes[nid]
-        b0 = lw.graph.input_shape.batch
-        cp = _rup4(sh.channels)
-        src_ptr, _ = self.ctx.cached_view(np.ascontiguousarray(node.weights, dtype=np.float32))
-        dev = torch.empty(b0 * sh.height * sh.width * cp, dtype=torch.float32, device=self.ctx.device)
-        self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(src_ptr), C.c_void_p(dev.data_ptr()), b0,
-                                                      sh.channels, sh.height, sh.width, cp, C.c_void_p(self.ctx.sp)),
-                       "const staging")
-        self.ctx.launches += 1
-        cache[id(node.weights)] = (node.weights, dev)
-        return dev.data_ptr()
-
-    def _wimg(self, n, s_in: TensorShape, k1: int, k2: int, cp: int, j: int, bn: int, w=None) -> int:
-        """Packed tf32 hi/lo operand image of a conv/linear weight view, cached
-        by (device view, geometry): one pack per distinct view per cache life."""
+    # -------------------------------------------------------------- tables
+    def _wimg_ptr(self, entry: tuple) -> int:
         ctx, lib = self.ctx, self.ctx.lib
-        wptr, st = ctx.cached_view(n.weights if w is None else w)
-        if n.kind is K.Conv2D:
+        ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn = entry
+        wptr, st = ctx.cached_view(self.refs.resolve(ref))
+        if is_conv:
             su, sv, sc, sn = st
         else:
             r, cstride = st
-            su, sv, sc, sn = s_in.width * r, r, s_in.height * s_in.width * r, cstride
-        key = (wptr, su, sv, sc, sn, k1, k2, s_in.channels, cp, j, bn)
+            su, sv, sc, sn = in_w * r, r, in_h * in_w * r, cstride
+        key = (wptr, su, sv, sc, sn, k1, k2, in_c, cp, j, bn)
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
             return hit.data_ptr()
         nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
-        ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, s_in.channels, cp, j, su, sv, sc, sn, bn,
+        ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn, bn,
                                         C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
         ctx.launches += 1
         cache[key] = img
         return img.data_ptr()
 
-    def _epi_rows(self, lw: Lowered, bufs: dict, steps: list) -> list:
-        out = []
-        for st in steps:
-            if st.op == "affine":
-                out.append((N.EPI_AFFINE, _rup4(lw.shapes[st.ref].channels), self._affine(lw, st.ref)))
-            elif st.op == "relu":
-                out.append((N.EPI_RELU, 0, 0))
-            elif st.op == "add":
-                sh = lw.shapes[st.ref] if st.ref >= 0 else lw.graph.input_shape
-                out.append((N.EPI_ADD_TENSOR, _rup4(sh.channels), bufs[st.ref]))
-            elif st.op == "const":
-                out.append((N.EPI_ADD_CONST, lw.graph.input_shape.batch, self._const(lw, st.ref)))
+    def _affine_ptrs(self, refs_needed: list) -> dict:
+        """Fold every BatchNorm the epilogues use into (a, b) with
+        a = scale/sqrt(var+eps), b = shift - mean*a (fp64 -> fp32), cached by
+        weight-array identity; all misses go up in ONE H2D."""
+        cache = self.ctx.__dict__.setdefault("affine_cache", {})
+        out, misses = {}, {}
+        for ref in refs_needed:
+            w = self.refs.resolve(ref)
+            hit = cache.get(id(w))
+            if hit is not None and hit[0] is w:
+                out[ref] = hit[2]
+            else:
+                misses[ref] = w
+        if misses:
+            blocks, offs, total = [], [], 0
+            for w in misses.values():
+                w64 = w.astype(np.float64)
+                a = w64[0] / np.sqrt(w64[3] + BN_EPS)
+                b = w64[1] - w64[2] * a
+                cp = _rup4(w.shape[1])
+                blk = np.zeros((2, cp), np.float32)
+                blk[0, :w.shape[1]] = a
+                blk[1, :w.shape[1]] = b
+                offs.append(total)
+                blocks.append(blk.reshape(-1))
+                total += Arena.round(2 * cp)
+            host = np.zeros(total, np.float32)
+            for o, blk in zip(offs, blocks):
+                host[o:o + blk.size] = blk
+            dev = self.ctx.upload_array(host)
+            if len(cache) > 200000:
+                cache.clear()
+            for (ref, w), o in zip(misses.items(), offs):
+                cache[id(w)] = (w, dev, dev.data_ptr() + 4 * o)
+                out[ref] = dev.data_ptr() + 4 * o
         return out
 
-    # -------------------------------------------------------------- prepare
-    def _prepare(self) -> None:
-        ctx, lib = self.ctx, self.ctx.lib
-        levels: dict[int, dict[str, list]] = {}
-        for gi, lw in enumerate(self.lowered):
-            bufs = self.bufs[gi]
-            nodes = lw.graph.nodes
-            for op in lw.ops:
-                lvl = levels.get(op.level)
-                if lvl is None:
-                    lvl = levels[op.level] = {"g64": [], "g128": [], "ew": []}
-                s_in = self._in_shape(lw, op)
-                s_out = lw.shapes[op.out]
-                if op.kind == "gemm":
-                    n = nodes[op.node]
-                    k1, k2, cp, j = self._gemm_geom(lw, op)
-                    bn = 128 if j > 64 else 64
-                    if n.kind is K.Conv2D:
-                        stride, pad = n.attrs["stride"], n.attrs["padding"]
+    def _const_ptr(self, entry: tuple) -> int:
+        """Dummy-add constant in NHWC-padded layout, cached per array."""
+        ref, b0, ch, h, w_, cp = entry
+        w = self.refs.resolve(ref)
+        cache = self.ctx.__dict__.setdefault("const_cache", {})
+        hit = cache.get(id(w))
+        if hit is not None and hit[0] is w:
+            return hit[1].data_ptr()
+        src_ptr, _ = self.ctx.cached_view(np.ascontiguousarray(w, dtype=np.float32))
+        dev = torch.empty(b0 * h * w_ * cp, dtype=torch.float32, device=self.ctx.device)
+        self.ctx.check(self.ctx.lib.tobf_nchw_to_nhwc(C.c_void_p(src_ptr), C.c_void_p(dev.data_ptr()), b0, ch, h,
+                                                      w_, cp, C.c_void_p(self.ctx.sp)), "const staging")
+        self.ctx.launches += 1
+        cache[id(w)] = (w, dev)
+        return dev.data_ptr()
+
+    # -------------------------------------------------------------- link
+    def _link_all(self) -> None:
+        ctx, lib, plans = self.ctx, self.ctx.lib, self.plans
+        s = self.input_shape
+        in_floats = Arena.round(self.batch * s.height * s.width * _rup4(s.channels))
+        total = 4 * in_floats + sum(p.arena_bytes for p in plans)
+        self.arena = ctx_arena(ctx, total // 4 + 4096)
+        self.x_ptr = self.arena.take(in_floats)
+        bases = np.zeros(len(plans), np.int64)
+        cur = self.x_ptr + 4 * in_floats
+        for i, p in enumerate(plans):
+            bases[i] = cur
+            cur += p.arena_bytes
+        self.arena.used = (cur - self.arena.base) // 4
+        self.out_ptrs = [int(bases[i]) + p.out_off for i, p in enumerate(plans)]
+        # requirement tables -> device pointers (per plan, concatenated)
+        wimg_memo: dict = {}
+        const_memo: dict = {}
+        aff = self._affine_ptrs(list({r for p in plans for r in p.affine}))
+        tabs = {}
+        for sp, name in ((SP_WIMG, "wimg"), (SP_AFFINE, "affine"), (SP_CONST, "const")):
+            ptrs, offsets = [], np.zeros(len(plans), np.int64)
+            for i, p in enumerate(plans):
+                offsets[i] = len(ptrs)
+                for e in getattr(p, name):
+                    if sp == SP_WIMG:
+                        v = wimg_memo.get(e)
+                        if v is None:
+                            v = wimg_memo[e] = self._wimg_ptr(e)
+                    elif sp == SP_AFFINE:
+                        v = aff[e]
                     else:
-                        stride, pad = 1, 0
-                    epi = self._epi_rows(lw, bufs, op.steps)
-                    row = (bufs[op.src], self._wimg(n, s_in, k1, k2, cp, j, bn, op.w), bufs[op.out],
-                           self.batch, s_in.height, s_in.width, cp, s_out.height, s_out.width, _rup4(j), j,
-                           k1, k2, stride, pad, 0, 0, 0, 0, 0, len(epi), cp, _rup4(j),
-                           epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi)))
-                    lvl["g128" if bn == 128 else "g64"].append((k1 * k2 * cp, row))
-                    continue
-                ldx, ldy = _rup4(s_in.channels), _rup4(s_out.channels)
-                epi = []
-                if op.kind == "pool":
-                    n = nodes[op.node]
-                    head = (N.OP_MAXPOOL, self.batch, s_in.height, s_in.width, s_in.channels, ldx, s_out.height,
-                            s_out.width, ldy, n.attrs["window"], n.attrs["stride"])
-                    cpo = _rup4(s_in.channels)
-                elif op.kind == "epi":
-                    epi = self._epi_rows(lw, bufs, op.steps)
-                    head = (N.OP_EPI, self.batch, s_in.height, s_in.width, s_out.channels, ldx, s_out.height,
-                            s_out.width, ldy, 0, 0)
-                    cpo = _rup4(s_out.channels)
-                elif op.kind == "copy":
-                    total = s_out.channels
-                    head = (N.OP_COPYCH, self.batch, s_in.height, s_in.width, op.cc, ldx, 0, 0, ldy, op.a0, op.a1)
-                    cpo = _rup4(total) if op.a0 + op.cc == total else op.a0 + op.cc
-                else:  # softmax
-                    head = (N.OP_SOFTMAX, self.batch, s_in.height, s_in.width, s_in.channels, ldx, 0, 0, ldy, 0, 0)
-                    cpo = _rup4(s_in.channels)
-                lvl["ew"].append((bufs[op.src], bufs[op.out]) + head +
-                                 (len(epi), 0, cpo, 0, epi + [_NO_EPI] * (N.TOBF_MAX_EPI - len(epi))))
-        # one structured array per op class for the whole population (numpy's
-        # nested-sequence parsing is the dominant host cost per call), then
-        # one contiguous slice per launch
-        conv_rows, conv_keys, ew_rows, ew_keys = [], [], [], []
-        for lv in sorted(levels):
-            grp = levels[lv]
-            for key, bn in (("g128", 128), ("g64", 64)):
-                if grp[key]:
-                    rows = [r for _, r in sorted(grp[key], key=lambda t: -t[0])]  # long K first
-                    conv_keys.append((lv, bn, len(conv_rows), len(rows)))
-                    conv_rows += rows
-            if grp["ew"]:
-                ew_keys.append((lv, len(ew_rows), len(grp["ew"])))
-                ew_rows += grp["ew"]
-        conv_arr = np.array(conv_rows, dtype=CONV_DTYPE) if conv_rows else np.zeros(0, CONV_DTYPE)
-        ew_arr = np.array(ew_rows, dtype=EW_DTYPE) if ew_rows else np.zeros(0, EW_DTYPE)
+                        v = const_memo.get(e)
+                        if v is None:
+                            v = const_memo[e] = self._const_ptr(e)
+                    ptrs.append(v)
+            tabs[sp] = (np.array(ptrs + [0], np.uint64), offsets)
+        # rows of all plans, linked, grouped into launches
+        conv = np.concatenate([p.conv for p in plans]) if plans else np.zeros(0, CONV_DTYPE)
+        ew = np.concatenate([p.ew for p in plans]) if plans else np.zeros(0, EW_DTYPE)
+        conv_plan = np.concatenate([np.full(len(p.conv), i, np.int64) for i, p in enumerate(plans)])
+        ew_plan = np.concatenate([np.full(len(p.ew), i, np.int64) for i, p in enumerate(plans)])
+        for arr, rp in ((conv, conv_plan), (ew, ew_plan)):
+            if not len(arr):
+                continue
+            for f in ("x", "y") + (("wimg",) if arr.dtype == CONV_DTYPE else ()):
+                arr[f] = _link(arr[f], rp, self.x_ptr, bases, tabs)
+            arr["epi"]["ptr"] = _link(arr["epi"]["ptr"], rp, self.x_ptr, bases, tabs)
+        conv_level = np.concatenate([p.conv_level for p in plans])
+        conv_bn = np.concatenate([p.conv_bn for p in plans])
+        conv_k = np.concatenate([p.conv_k for p in plans])
+        ew_level = np.concatenate([p.ew_level for p in plans])
+        # one launch per (level, BN), long K first; one ew launch per level
+        order = np.lexsort((-conv_k, -conv_bn, conv_level))
+        conv = conv[order]
+        ckey = np.stack([conv_level[order], conv_bn[order]], 1) if len(conv) else np.zeros((0, 2), np.int64)
+        eorder = np.argsort(ew_level, kind="stable")
+        ew = ew[eorder]
+        ekey = ew_level[eorder]
         launches = []
-        for lv, bn, lo, n in conv_keys:
+        lo = 0
+        while lo < len(conv):
+            hi = lo + 1
+            while hi < len(conv) and ckey[hi, 0] == ckey[lo, 0] and ckey[hi, 1] == ckey[lo, 1]:
+                hi += 1
             tot = C.c_int64()
-            ctx.check(lib.tobf_conv_prepare(C.c_void_p(conv_arr[lo:].ctypes.data), n, bn, C.byref(tot)),
-                      "conv prepare")
-            launches.append((lv, 0, "conv", lo, n, tot.value, bn))
-        for lv, lo, n in ew_keys:
+            ctx.check(lib.tobf_conv_prepare(C.c_void_p(conv[lo:].ctypes.data), hi - lo, int(ckey[lo, 1]),
+                                            C.byref(tot)), "conv prepare")
+            launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, int(ckey[lo, 1])))
+            lo = hi
+        lo = 0
+        while lo < len(ew):
+            hi = lo + 1
+            while hi < len(ew) and ekey[hi] == ekey[lo]:
+                hi += 1
             tot = C.c_int64()
-            ctx.check(lib.tobf_ew_prepare(C.c_void_p(ew_arr[lo:].ctypes.data), n, C.byref(tot)), "ew prepare")
-            launches.append((lv, 1, "ew", lo, n, tot.value, 0))
+            ctx.check(lib.tobf_ew_prepare(C.c_void_p(ew[lo:].ctypes.data), hi - lo, C.byref(tot)), "ew prepare")
+            launches.append((int(ekey[lo]), 1, "ew", lo, hi - lo, tot.value, 0))
+            lo = hi
         launches.sort(key=lambda t: (t[0], t[1]))
-        conv_bytes = conv_arr.tobytes()
+        conv_bytes = conv.tobytes()
         pad = (-len(conv_bytes)) % 256
-        host = conv_bytes + bytes(pad) + ew_arr.tobytes()
+        host = conv_bytes + bytes(pad) + ew.tobytes()
         self.desc_dev = ctx.upload_bytes(host) if host else None
         base = self.desc_dev.data_ptr() if host else 0
         ew_base = base + len(conv_bytes) + pad
@@ -527,7 +685,7 @@ class PopulationRun:
     # -------------------------------------------------------------- run
     def set_input(self, x_nchw: torch.Tensor) -> None:
         """x: (batch, C, H, W) float32 on the device (batch = graph batch * reps)."""
-        s = self.lowered[0].graph.input_shape
+        s = self.input_shape
         if tuple(x_nchw.shape) != (self.batch, s.channels, s.height, s.width):
             raise ShapeMismatch(-1, f"input shape {tuple(x_nchw.shape)} != stacked {(self.batch, *s.as_tuple()[1:])}")
         x = x_nchw.contiguous()
@@ -555,8 +713,7 @@ class PopulationRun:
         self.ctx.launches += len(self.launches)
 
     def output_ptr(self, gi: int) -> tuple[int, TensorShape]:
-        lw = self.lowered[gi]
-        return self.bufs[gi][lw.out_node], lw.shapes[lw.out_node]
+        return self.out_ptrs[gi], self.plans[gi].out_shape
 
     def output_nchw(self, gi: int) -> torch.Tensor:
         ptr, s = self.output_ptr(gi)
@@ -570,20 +727,7 @@ class PopulationRun:
         """Algorithmic conv/linear FLOPs of one run (all graphs, all reps): the
         emitted (obfuscated) layers, 2*M*N*K each; a fused sibling group counts
         exactly the sum of its parts."""
-        total = 0
-        for lw in self.lowered:
-            for op in lw.ops:
-                if op.kind == "gemm":
-                    n = lw.graph.nodes[op.node]
-                    s = lw.shapes[op.node]
-                    s_in = self._in_shape(lw, op)
-                    j = op.j or n.attrs["j"]
-                    if n.kind is K.Conv2D:
-                        kk = n.attrs["k1"] * n.attrs["k2"] * s_in.channels
-                        total += 2 * self.batch * s.height * s.width * j * kk
-                    else:
-                        total += 2 * self.batch * j * s_in.channels * s_in.height * s_in.width
-        return total
+        return sum(p.flops_per_image for p in self.plans) * self.reps
 
 
 # ---------------------------------------------------------------------------

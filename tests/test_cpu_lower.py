@@ -46,3 +46,30 @@ def test_sibling_fusion_covers_every_node_once():
             assert gemm_j <= ref_j  # in-branch groups compute j once for all parts
             if not fuse:
                 assert gemm_j == ref_j
+
+
+def test_forward_plan_symbolic_rows():
+    """plan_forward (host only): every pointer field is symbolic and refers to
+    an arena offset inside the graph's block or to an entry of its tables."""
+    S = executor
+    for g, og in _plans("sequence", 6, seed=5):
+        refs = S.ArrayRefs()
+        plan = S.plan_forward(S.lower(og), 8, refs)
+        assert len(plan.conv) and len(plan.conv) == len(plan.conv_level) == len(plan.conv_bn)
+        sizes = {S.SP_WIMG: len(plan.wimg), S.SP_AFFINE: len(plan.affine), S.SP_CONST: len(plan.const)}
+        cols = [plan.conv["x"], plan.conv["y"], plan.conv["wimg"], plan.conv["epi"]["ptr"].ravel(),
+                plan.ew["x"], plan.ew["y"], plan.ew["epi"]["ptr"].ravel()]
+        for col in cols:
+            col = col.astype(np.uint64)
+            space = col >> np.uint64(S._SP_SHIFT)
+            val = col & np.uint64(S._SP_LOW)
+            for sp, v in zip(space.tolist(), val.tolist()):
+                if sp == S.SP_ARENA:
+                    assert v < plan.arena_bytes
+                elif sp in sizes:
+                    assert v < sizes[sp]
+                else:
+                    assert sp in (0, S.SP_INPUT)
+        for e in plan.wimg:
+            w = refs.resolve(e[0])
+            assert w.dtype == np.float32 and w.ndim in (2, 4)
