@@ -302,7 +302,8 @@ def main_ours(args):
                "h2d_bytes_per_step": int((ctx.h2d_bytes - h0) / args.steps) + x_bytes,
                "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms,
                "host_ms_per_step": {k: round(v / args.steps, 2) for k, v in host_ms.items()},
-               "micro_batch": args.micro}
+               "micro_batch": args.micro, "host_workers": pe.pool.workers if pe.pool is not None else 0}
+        pe.close()
 
     # ---- cpu baseline (rank 0, N == 1 only)
     cpu = None

@@ -42,6 +42,8 @@ class DeviceContext:
         self.weight_cache: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
         self.weight_cache_bytes = 0
         self.weight_cache_limit = int(os.environ.get("TOBF_WEIGHT_CACHE_BYTES", str(24 << 30)))
+        self.pinned_cache: dict[int, tuple] = {}
+        self.pinned_bytes = 0
         self.launches = 0      # libtobf kernel launches issued (bench evidence)
         self.h2d_bytes = 0     # host->device bytes staged through this context
 
@@ -89,17 +91,27 @@ class DeviceContext:
         key = id(a)
         hit = self.weight_cache.get(key)
         if hit is None or hit[0] is not a:
-            dev = self._pinned_copy(own)
+            dev = self._pinned_copy(own, cache=False)
             self.h2d_bytes += own.nbytes
             self._remember(key, a, dev)
         return self.weight_cache[key][1].data_ptr(), tuple(st // 4 for st in own.strides)
 
-    def _pinned_copy(self, a: np.ndarray) -> torch.Tensor:
-        """Stage ``a`` (possibly read-only) in pinned memory and copy it to the
-        device, stream-ordered."""
-        host = torch.empty(a.size, dtype=torch.float32, pin_memory=True)
-        host.numpy()[:] = a.reshape(-1)
-        return host.to(self.device, non_blocking=True)
+    def _pinned_copy(self, a: np.ndarray, cache: bool = True) -> torch.Tensor:
+        """Copy ``a`` (possibly read-only) to the device, stream-ordered, from
+        a pinned host mirror kept per host array: clear_cache() drops device
+        copies only, so a re-upload is one DMA, not a pageable memcpy."""
+        hit = self.pinned_cache.get(id(a)) if cache else None
+        if hit is None or hit[0] is not a:
+            host = torch.empty(a.size, dtype=torch.float32, pin_memory=True)
+            host.numpy()[:] = a.reshape(-1)
+            if self.pinned_bytes > self.weight_cache_limit:
+                self.pinned_cache.clear()
+                self.pinned_bytes = 0
+            hit = (a, host)
+            if cache:
+                self.pinned_cache[id(a)] = hit
+                self.pinned_bytes += a.nbytes
+        return hit[1].to(self.device, non_blocking=True)
 
     def _remember(self, key, base, dev) -> None:
         if self.weight_cache_bytes > self.weight_cache_limit:

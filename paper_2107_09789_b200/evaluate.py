@@ -19,6 +19,7 @@ non-function-preserving candidate is infeasible by the paper's contract).
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -26,11 +27,12 @@ import numpy as np
 import torch
 
 from .engine import device
-from .executor import PopulationRun, compare_outputs, lower, trial_inputs
+from .executor import PopulationRun, compare_outputs, lower, plan_forward, trial_inputs
 from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
 from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,
+                    prepare_trace_records,
                     run_trace, trace_population)
 
 RECORD_DTYPE = np.dtype([("reward", "<f8"), ("mean_ler", "<f8"), ("latency", "<f8"), ("worst", "<f4"),
@@ -101,6 +103,54 @@ class PopulationEvaluator:
         # T* = latency of the unobfuscated graph under the same profile (Eq. 10)
         pt = trace_population([(vanilla, None, None)], self.ev.profile, self.memo)
         self.t_star = float(pt.totals.cpu()[0])
+        self.pool = None          # hostpipe.HostPool, started on the first pooled batch
+        self.prefs = None         # hostpipe.ParentRefs (weights of worker results)
+        self.vanilla_plan = None
+
+    def close(self) -> None:
+        if self.pool is not None:
+            self.pool.close()
+            self.pool = None
+
+    def _ensure_pool(self, workers: int | None = None) -> None:
+        if self.pool is None:
+            from .hostpipe import HostPool, ParentRefs
+            self.prefs = ParentRefs(self.vanilla)
+            self.vanilla_plan = plan_forward(self.lowered_vanilla, self.trials, self.prefs)
+            self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers)
+
+    def prepare_encoded(self, plans: list[ObfuscationPlan], results: list, memo: dict | None = None,
+                        first_seen: dict | None = None) -> dict:
+        """Host half from worker results (hostpipe.encode_candidate tuples, in
+        candidate order): link forward plans, resolve the schedule memo,
+        stage everything into HBM."""
+        t0 = time.perf_counter()
+        cands, feas, fps, cts = [], [], [], []
+        base = results[0][0] if results else 0
+        for c, err, payload in results:
+            plan = plans[c - base]
+            if err is not None:
+                cands.append(Candidate(plan, None, None, err))
+                continue
+            fp, ct, new = payload
+            if new:
+                self.prefs.adopt(c, new)
+            feas.append(len(cands))
+            cands.append(Candidate(plan, None, None))
+            fps.append(fp)
+            cts.append(ct)
+        t1 = time.perf_counter()
+        run = PopulationRun(self.ctx, None, reps=self.trials, plans=[self.vanilla_plan] + fps, refs=self.prefs)
+        t2 = time.perf_counter()
+        tp = prepare_trace_records(cts, self.ev.profile, self.memo if memo is None else memo,
+                                   exchange=self.exchange, first_seen=first_seen) if cts else None
+        idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
+        t3 = time.perf_counter()
+        return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
+                "feasible": [c.error is None for c in cands],
+                "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
+                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
+                            "trace_prep": 1e3 * (t3 - t2)}}
 
     # ---------------------------------------------------------------- host
     def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None) -> dict:
@@ -121,6 +171,7 @@ class PopulationEvaluator:
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t3 = time.perf_counter()
         return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
+                "feasible": [c.graph is not None for c in cands],
                 "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
                 "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
                             "trace_prep": 1e3 * (t3 - t2)}}
@@ -170,7 +221,7 @@ class PopulationEvaluator:
         R, mean = reward(lers, T, ok, self.t_star, self.budget, self.eps)
         mark("reward")
         return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": ntok0, "trace": tp, "events": ev,
-                "feasible": [c.graph is not None for c in cands], "lers": lers}
+                "feasible": prep["feasible"], "lers": lers}
 
     def collect(self, out: dict) -> np.ndarray:
         rec = np.zeros(len(out["feasible"]), dtype=RECORD_DTYPE)
@@ -184,17 +235,45 @@ class PopulationEvaluator:
         self.ctx.sync()
         return rec
 
-    def evaluate_records(self, plans: list[ObfuscationPlan], micro: int = 8, memo: dict | None = None) -> np.ndarray:
+    def evaluate_records(self, plans: list[ObfuscationPlan], micro: int = 8, memo: dict | None = None,
+                         workers: int | None = None) -> np.ndarray:
         """Records for ``plans`` with host preparation of micro-batch i+1
         overlapping the device pipeline of micro-batch i (launches are async;
-        the only host waits are the final read-backs). First-seen schedule
-        semantics hold across micro-batches: a signature pending in several of
-        them is searched from its first occurrence's descriptor everywhere."""
+        the only host waits are the final read-backs). With ``workers`` != 0
+        (default: hostpipe.default_workers(), TOBF_HOST_WORKERS=0 disables)
+        the per-candidate host work runs in a process pool and the parent only
+        links and launches. First-seen schedule semantics hold across
+        micro-batches: a signature pending in several of them is searched
+        from its first occurrence's descriptor everywhere."""
         first_seen: dict = {}
         jobs = []
-        for lo in range(0, len(plans), micro):
-            prep = self.prepare(plans[lo:lo + micro], memo=memo, first_seen=first_seen)
-            jobs.append((prep, self.run(prep, cold_schedules=False)))
+        if workers is None:
+            from .hostpipe import default_workers
+            workers = default_workers() if os.environ.get("TOBF_HOST_WORKERS", "") != "0" else 0
+        if workers and len(plans) > 1:
+            self._ensure_pool(workers)
+            per_job = 2
+            handles = self.pool.submit(plans, per_job=per_job)
+            got: dict[int, tuple] = {}
+            nxt = 0  # next handle to receive
+            wait = 0.0
+            for lo in range(0, len(plans), micro):
+                hi = min(len(plans), lo + micro)
+                t0 = time.perf_counter()
+                while nxt * per_job < hi:
+                    for r in self.pool.result(handles[nxt]):
+                        got[r[0]] = r
+                    nxt += 1
+                wait += time.perf_counter() - t0
+                prep = self.prepare_encoded(plans[lo:hi], [got.pop(c) for c in range(lo, hi)], memo=memo,
+                                            first_seen=first_seen)
+                prep["host_ms"]["wait_workers"] = 1e3 * wait
+                wait = 0.0
+                jobs.append((prep, self.run(prep, cold_schedules=False)))
+        else:
+            for lo in range(0, len(plans), micro):
+                prep = self.prepare(plans[lo:lo + micro], memo=memo, first_seen=first_seen)
+                jobs.append((prep, self.run(prep, cold_schedules=False)))
         recs = [self.collect(out) for _, out in jobs]
         for prep, _ in jobs:
             if prep["trace"] is not None:

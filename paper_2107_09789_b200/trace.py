@@ -284,51 +284,86 @@ class TracePlan:
         self.feats = self.totals = None
 
 
+_COMPLEX_VALUES = frozenset(k.value for k in COMPLEX_KINDS)
+
+
+@dataclass
+class CandidateTrace:
+    """Host half of compile_graph for one graph (no device, picklable):
+    kernel records in kernel order (schedule unresolved, sig_index -1) and
+    each kernel's schedule signature (costmodel.py:251-256)."""
+
+    recs: np.ndarray
+    sigs: list
+
+
+def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | None, pname: str,
+                  analysis=None) -> tuple[CandidateTrace, list[Kernel], dict]:
+    """fuse + signatures + integer descriptors of one graph."""
+    ana = analysis if analysis is not None else analyze(graph)
+    shapes = ana.shapes
+    kernels = fuse(graph, fusion_limits, order=ana.order, succ=ana.succ)
+    strategies = strategies or {}
+    nodes = graph.nodes
+    sigs, rows = [], []
+    for k in kernels:
+        a = nodes[k.anchor]
+        ins = shapes[a.inputs[0]] if a.inputs else graph.input_shape
+        sigs.append((pname, a.kind.value, canonical_attrs(a.attrs), ins._t, shapes[k.anchor]._t))
+        rows.append(kernel_tuple(graph, shapes, k, None, strategies.get(k.anchor, 0), -1))
+    recs = np.array(rows, dtype=KERN_DTYPE) if rows else np.zeros(0, KERN_DTYPE)
+    return CandidateTrace(recs, sigs), kernels, shapes
+
+
 def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
                   exchange=None, first_seen: dict | None = None) -> TracePlan:
     """Host half of compile_graph for many graphs: fuse, signatures, integer
     descriptors (one H2D for all). ``items``: (graph, fusion_limits,
-    strategies[, ir.Analysis]).
-
-    ``exchange`` (dist.exchange_signatures) merges this rank's unmemoised
-    signatures with every other rank's in global first-seen order; the
-    resulting table is searched identically on every rank, so all memos stay
-    equal and every schedule is the one a single process would pick.
-    ``first_seen`` (sig -> descriptor bytes) carries first occurrences across
-    batches whose searches have not been folded into the memo yet."""
-    ctx = device()
-    memo = _SCHEDULE_CACHE if memo is None else memo
-    compiled, per_kernel = [], []
-    hits: dict[tuple, Schedule] = {}
-    local_pending: dict[tuple, bytes] = {}
-    pname = profile.name
+    strategies[, ir.Analysis])."""
+    cts, compiled = [], []
     for item in items:
         graph, limits, strategies = item[0], item[1], item[2]
-        ana = item[3] if len(item) > 3 and item[3] is not None else analyze(graph)
-        shapes = ana.shapes
-        kernels = fuse(graph, limits, order=ana.order, succ=ana.succ)
-        strategies = strategies or {}
-        cg = CompiledGraph(kernels=kernels, source=graph, shapes=shapes)
-        nodes = graph.nodes
-        for k in kernels:
-            a = nodes[k.anchor]
-            ins = shapes[a.inputs[0]] if a.inputs else graph.input_shape
-            sig = (pname, a.kind.value, canonical_attrs(a.attrs), ins._t, shapes[k.anchor]._t)
-            if sig not in hits and sig not in local_pending:
-                hit = memo.get(sig)
-                if hit is None and a.kind not in COMPLEX_KINDS:
-                    hit = memo[sig] = TRIVIAL_SCHEDULE
-                if hit is not None:
-                    hits[sig] = hit
-                else:
-                    blob = first_seen.get(sig) if first_seen is not None else None
-                    if blob is None:
-                        blob = np.array([kernel_tuple(graph, shapes, k)], dtype=KERN_DTYPE).tobytes()
-                        if first_seen is not None:
-                            first_seen[sig] = blob
-                    local_pending[sig] = blob
-            per_kernel.append((cg, k, sig, strategies.get(k.anchor, 0)))
-        compiled.append(cg)
+        ana = item[3] if len(item) > 3 and item[3] is not None else None
+        ct, kernels, shapes = trace_records(graph, limits, strategies, profile.name, ana)
+        cts.append(ct)
+        compiled.append(CompiledGraph(kernels=kernels, source=graph, shapes=shapes))
+    return prepare_trace_records(cts, profile, memo, exchange, first_seen, compiled)
+
+
+def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, memo: dict | None = None,
+                          exchange=None, first_seen: dict | None = None,
+                          compiled: list[CompiledGraph] | None = None) -> TracePlan:
+    """Memo resolution and upload of a batch's kernel records.
+
+    Signatures already in the memo resolve to their schedule; the others are
+    searched on the device from their FIRST occurrence's descriptor
+    (costmodel.py:248 first-seen memo). ``exchange`` (dist.exchange_signatures)
+    merges this rank's unmemoised signatures with every other rank's in global
+    first-seen order, so all ranks search the same table and memos stay
+    equal. ``first_seen`` (sig -> descriptor bytes) carries first occurrences
+    across batches whose searches have not been folded into the memo yet."""
+    ctx = device()
+    memo = _SCHEDULE_CACHE if memo is None else memo
+    hits: dict[tuple, Schedule] = {}
+    local_pending: dict[tuple, bytes] = {}
+    for ct in cts:
+        for r, sig in enumerate(ct.sigs):
+            if sig in hits or sig in local_pending:
+                continue
+            hit = memo.get(sig)
+            if hit is None and sig[1] not in _COMPLEX_VALUES:
+                hit = memo[sig] = TRIVIAL_SCHEDULE
+            if hit is not None:
+                hits[sig] = hit
+                continue
+            blob = first_seen.get(sig) if first_seen is not None else None
+            if blob is None:
+                rec = ct.recs[r:r + 1].copy()
+                rec["strategy"] = 0
+                blob = rec.tobytes()
+                if first_seen is not None:
+                    first_seen[sig] = blob
+            local_pending[sig] = blob
     pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
     rows: dict[tuple, int] = {}
     sig_recs = []
@@ -341,17 +376,22 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
         rows[sig] = len(sig_recs)
         pending.append((rows[sig], sig))
         sig_recs.append(blob)
-    nsig, nk = len(sig_recs), len(per_kernel)
-    kern = np.array([kernel_tuple(cg.nodes_source, cg._shapes, k, None, st, rows[sig])
-                     for cg, k, sig, st in per_kernel], dtype=KERN_DTYPE) if nk else np.zeros(1, KERN_DTYPE)
-    offsets = np.zeros(len(compiled) + 1, np.int32)
-    offsets[1:] = np.cumsum([len(cg.kernels) for cg in compiled])
+    nsig = len(sig_recs)
+    counts = [len(ct.sigs) for ct in cts]
+    nk = sum(counts)
+    if nk:
+        kern = np.concatenate([ct.recs for ct in cts])
+        kern["sig_index"] = [rows[sig] for ct in cts for sig in ct.sigs]
+    else:
+        kern = np.zeros(1, KERN_DTYPE)
+    offsets = np.zeros(len(cts) + 1, np.int32)
+    offsets[1:] = np.cumsum(counts)
     sig_blob = b"".join(sig_recs) if sig_recs else np.zeros(1, KERN_DTYPE).tobytes()
     blob = sig_blob + kern.tobytes()
     dev = ctx.upload_bytes(blob)
     offs = ctx.upload_array(offsets)
-    tp = TracePlan(compiled, dev[len(sig_blob):], dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile,
-                   memo)
+    tp = TracePlan(compiled if compiled is not None else [None] * len(cts), dev[len(sig_blob):],
+                   dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile, memo)
     tp._blob = dev
     tp._sig_template = sig_blob
     return tp
@@ -400,12 +440,11 @@ def finish_trace(tp: TracePlan) -> None:
     for i, sig in tp.pending:
         if sig not in tp.memo:
             tp.memo[sig] = Schedule(tuple(sigs[i].ty), tuple(sigs[i].tx), sigs[i].unroll)
-    r = 0
-    for cg in tp.compiled:
-        cg.schedules = []
-        for _ in cg.kernels:
-            cg.schedules.append(Schedule(tuple(kern[r].ty), tuple(kern[r].tx), kern[r].unroll))
-            r += 1
+    for cg, r in zip(tp.compiled, tp.offsets_host[:-1]):
+        if cg is None:
+            continue  # records built out of process: no CompiledGraph to annotate
+        cg.schedules = [Schedule(tuple(kern[q].ty), tuple(kern[q].tx), kern[q].unroll)
+                        for q in range(r, r + len(cg.kernels))]
 
 
 @dataclass

@@ -1,0 +1,59 @@
+"""Worker-process host preparation (hostpipe.py) produces exactly the
+in-process forward plans and trace records: same descriptor rows, same
+signatures, weight references that resolve to equal arrays in the parent."""
+
+import numpy as np
+import pytest
+
+from paper_2107_09789_b200 import executor, fixtures, ga, hostpipe, knobs
+from paper_2107_09789_b200.ir import analyze
+from paper_2107_09789_b200.trace import trace_records
+
+
+@pytest.fixture(scope="module")
+def population():
+    g = fixtures.resnet18(size=64)
+    space = ga.search_space(g, "sequence")
+    sizes = ga.domain_sizes("sequence", space)
+    plans = [ga.decode_genome(g, "sequence", space, x) for x in ga.random_genomes(np.random.default_rng(7), sizes, 6)]
+    return g, plans
+
+
+def _resolved_tables(plan, refs):
+    w = [(refs.resolve(e[0]),) + tuple(e[1:]) for e in plan.wimg]
+    a = [refs.resolve(r) for r in plan.affine]
+    c = [(refs.resolve(e[0]),) + tuple(e[1:]) for e in plan.const]
+    return w, a, c
+
+
+def test_pool_matches_in_process(population):
+    g, plans = population
+    va = analyze(g)
+    pool = hostpipe.HostPool(g, reps=2, pname="default", workers=2)
+    try:
+        handles = pool.submit(plans, per_job=2)
+        results = [r for h in reversed(handles) for r in pool.result(h)][::-1]
+        results.sort(key=lambda r: r[0])
+    finally:
+        pool.close()
+    prefs = hostpipe.ParentRefs(g)
+    assert [r[0] for r in results] == list(range(len(plans)))
+    for (c, err, payload), plan in zip(results, plans):
+        og, d, ana = knobs.apply_plan_analyzed(g, plan, va)
+        assert err is None
+        fp, ct, new = payload
+        prefs.adopt(c, new)
+        refs = executor.ArrayRefs()
+        ref_fp = executor.plan_forward(executor.lower(og, ana), 2, refs)
+        for f in ("conv", "conv_level", "conv_bn", "conv_k", "ew", "ew_level"):
+            assert np.array_equal(getattr(fp, f), getattr(ref_fp, f)), f
+        assert (fp.arena_bytes, fp.out_off, fp.out_shape, fp.flops_per_image) == \
+               (ref_fp.arena_bytes, ref_fp.out_off, ref_fp.out_shape, ref_fp.flops_per_image)
+        (w1, a1, c1), (w2, a2, c2) = _resolved_tables(fp, prefs), _resolved_tables(ref_fp, refs)
+        assert len(w1) == len(w2) and len(a1) == len(a2) and len(c1) == len(c2)
+        for x, y in zip(w1 + c1, w2 + c2):
+            assert np.array_equal(x[0], y[0]) and x[1:] == y[1:]
+        for x, y in zip(a1, a2):
+            assert np.array_equal(x, y)
+        ref_ct, _, _ = trace_records(og, d.fusion_limits, d.schedule_strategies, "default", ana)
+        assert np.array_equal(ct.recs, ref_ct.recs) and ct.sigs == ref_ct.sigs

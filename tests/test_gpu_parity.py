@@ -231,9 +231,17 @@ def test_micro_batched_records_match_single_batch(ctx):
     g = fixtures.resnet18(size=64)
     plans = _plans(g, "sequence", 7, seed=12)
     ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
-    one = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=len(plans), memo={})
-    many = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=3, memo={})
+    one = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=len(plans), memo={},
+                                                                         workers=0)
+    many = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=3, memo={}, workers=0)
     assert one.tobytes() == many.tobytes()
+    # host preparation in worker processes (hostpipe) changes nothing
+    pe = PopulationEvaluator(g, ev, trials=2, memo={})
+    try:
+        pooled = pe.evaluate_records(plans, micro=3, memo={}, workers=2)
+    finally:
+        pe.close()
+    assert pooled.tobytes() == one.tobytes()
     # and the trace totals follow the reference's process-global first-seen memo order
     memo = CM.ScheduleMemo()
     for i, p in enumerate(plans):
