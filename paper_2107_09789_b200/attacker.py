@@ -83,8 +83,10 @@ def bagged_predictors(features: int = 9, hiddens=(128, 256, 512), seed: int = 0)
 # device stages
 # ---------------------------------------------------------------------------
 
-def decode(feats: torch.Tensor, offsets: torch.Tensor, ntraces: int, t_max: int, pred: Predictor):
-    """LSTM + greedy CTC over device-resident trace rows -> (tokens[B,T_max] int8, ntok[B] int32)."""
+def decode(feats: torch.Tensor, offsets: torch.Tensor, ntraces: int, t_max: int, pred: Predictor,
+           stream: int | None = None):
+    """LSTM + greedy CTC over device-resident trace rows -> (tokens[B,T_max] int8, ntok[B] int32).
+    ``stream``: raw cudaStream_t to launch on (default: the engine stream)."""
     ctx = device()
     w = pred.device_weights(ctx)
     tokens = torch.zeros((ntraces, t_max), dtype=torch.int8, device=ctx.device)
@@ -94,12 +96,13 @@ def decode(feats: torch.Tensor, offsets: torch.Tensor, ntraces: int, t_max: int,
                                     C.c_void_p(w["w_ihT"].data_ptr()), C.c_void_p(w["w_hhT"].data_ptr()),
                                     C.c_void_p(w["b"].data_ptr()), C.c_void_p(w["w_out"].data_ptr()),
                                     C.c_void_p(w["b_out"].data_ptr()), C.c_void_p(tokens.data_ptr()), t_max,
-                                    C.c_void_p(ntok.data_ptr()), C.c_void_p(ctx.sp)), "lstm+ctc")
+                                    C.c_void_p(ntok.data_ptr()), C.c_void_p(ctx.sp if stream is None else stream)),
+              "lstm+ctc")
     ctx.launches += 1
     return tokens, ntok
 
 
-def edit_distances(tokens: torch.Tensor, ntok: torch.Tensor, truth: np.ndarray):
+def edit_distances(tokens: torch.Tensor, ntok: torch.Tensor, truth: np.ndarray, stream: int | None = None):
     """Warp-per-pair Levenshtein against one truth -> (ed int32, ler float64) on the device."""
     ctx = device()
     B, t_max = tokens.shape
@@ -109,7 +112,8 @@ def edit_distances(tokens: torch.Tensor, ntok: torch.Tensor, truth: np.ndarray):
     lr = torch.empty(B, dtype=torch.float64, device=ctx.device)
     ctx.check(ctx.lib.tobf_levenshtein(C.c_void_p(tokens.data_ptr()), C.c_void_p(ntok.data_ptr()), B, t_max,
                                        C.c_void_p(tr.data_ptr()), tr.numel(), C.c_void_p(ed.data_ptr()),
-                                       C.c_void_p(lr.data_ptr()), C.c_void_p(ctx.sp)), "levenshtein")
+                                       C.c_void_p(lr.data_ptr()), C.c_void_p(ctx.sp if stream is None else stream)),
+              "levenshtein")
     ctx.launches += 1
     return ed, lr, tr
 

@@ -47,6 +47,13 @@ class DeviceContext:
         self.launches = 0      # libtobf kernel launches issued (bench evidence)
         self.h2d_bytes = 0     # host->device bytes staged through this context
 
+    def side_streams(self, n: int) -> list:
+        """``n`` extra engine streams (created once, reused)."""
+        ss = self.__dict__.setdefault("_side", [])
+        while len(ss) < n:
+            ss.append(torch.cuda.Stream(self.device))
+        return ss[:n]
+
     @property
     def sp(self) -> int:
         """Raw cudaStream_t of the engine stream."""

@@ -208,12 +208,27 @@ class PopulationEvaluator:
             idx = prep["idx"]
             if not hasattr(self, "_truth_dev"):
                 self._truth_dev = ctx.upload_array(self.truth)
+            # the bagged predictors are independent: predictor p > 0 runs on
+            # side stream p-1 (a GPU-latency-bound recurrence each; together
+            # they fill the SMs one alone leaves idle), joined before Eq. 10
+            main = ctx.stream
+            side = ctx.side_streams(len(self.ev.predictors) - 1)
+            fork = torch.cuda.Event()
+            fork.record(main)
             for p, pred in enumerate(self.ev.predictors):
-                toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred)
-                _, lr, _ = edit_distances(toks, ntok, self._truth_dev)
-                lers[p].index_copy_(0, idx, lr)
-                if p == 0:
-                    ntok0.index_copy_(0, idx, ntok)
+                s = main if p == 0 else side[p - 1]
+                with torch.cuda.stream(s):
+                    if p:
+                        s.wait_event(fork)
+                    toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred, s.cuda_stream)
+                    _, lr, _ = edit_distances(toks, ntok, self._truth_dev, s.cuda_stream)
+                    lers[p].index_copy_(0, idx, lr)
+                    if p == 0:
+                        ntok0.index_copy_(0, idx, ntok)
+                if p:
+                    join = torch.cuda.Event()
+                    join.record(s)
+                    main.wait_event(join)
             T.index_copy_(0, idx, tp.totals)
             ok.index_copy_(0, idx, ok_f)
             worst.index_copy_(0, idx, worst_f)
