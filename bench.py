@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=1, help="cpu_baseline sample: rounds of one candidate per core")
     ap.add_argument("--micro", type=int, default=8, help="e2e micro-batch (host prep overlaps device run)")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
+    ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
     return ap.parse_args()
 
 
@@ -174,6 +176,81 @@ def reference_arm(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ----------------------------------------------------------------------------- kernel sweeps
+def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
+    """The two memory/ALU-side kernels BASELINE.json names beside the conv:
+    (1) the LER kernel on a scaled sweep (SURVEY 8(d) honest-sizing note:
+    >= 1e7 (prediction, L*) pairs, RN18 L* = 24 labels, predictions of
+    U[119,169] tokens in 176-B rows, 1.76 GB > L2 so no flush is needed), GB/s of
+    algorithmic bytes vs measured HBM peak; (2) cfg5: 10k traces through the
+    3 bagged LSTM predictors + greedy CTC + LER (FP32-FFMA bound)."""
+    import torch
+    from paper_2107_09789_b200 import attacker
+    from paper_2107_09789_b200.ir import label_sequence
+    dev = torch.device("cuda", torch.cuda.current_device())
+    truth = attacker.encode_labels(label_sequence(vanilla))
+    m = len(truth)
+    out = {}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed)
+    B, t_max = args.ler_pairs, 176
+    lens = torch.randint(119, 170, (B,), generator=gen, device=dev, dtype=torch.int32)
+    toks = torch.randint(1, 5, (B, t_max), generator=gen, device=dev, dtype=torch.int8)
+    for _ in range(3):
+        attacker.edit_distances(toks, lens, truth)
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        attacker.edit_distances(toks, lens, truth)
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    alg = int(lens.sum().item()) + B * m + B * (4 + 4 + 8)  # |L| + |L*| tokens, ntok in, ED + LER out
+    gbs = alg / (ms / 1e3) / 1e9
+    out["ler"] = {"kernel": "levenshtein_bp_kernel (thread per pair, bit-parallel)", "pairs": B, "truth_len": m,
+                  "pred_len": "U[119,169]", "ms_per_launch": round(ms, 4), "pairs_per_s": B / (ms / 1e3),
+                  "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                  "frac": round(gbs / hbm_peak, 4), "algorithmic_bytes": alg,
+                  "bytes_def": "sum(|L|) + pairs*|L*| (1 B tokens) + 16 B/pair (ntok, ED, LER)"}
+    del toks, lens
+    # cfg5: 10k traces, T ~ U[119,169], F = 9 cost-model-scale features
+    nt = 10_000
+    tl = torch.randint(119, 170, (nt,), generator=gen, device=dev, dtype=torch.int32)
+    offs = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
+    offs[1:] = torch.cumsum(tl, 0)
+    rows = int(offs[-1].item())
+    feats = torch.rand((rows, 9), generator=gen, device=dev, dtype=torch.float64) * 1e6
+    tmax = 169
+
+    def fit():
+        for p in predictors:
+            tk, nk = attacker.decode(feats, offs, nt, tmax, p)
+            attacker.edit_distances(tk, nk, truth)
+
+    for _ in range(2):
+        fit()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    reps = 3
+    for _ in range(reps):
+        fit()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    flops = sum(rows * 2 * 4 * p.hidden * (p.features + p.hidden) for p in predictors)
+    ffma_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    out["cfg5_fitness"] = {"traces": nt, "rows": rows, "predictors": [p.hidden for p in predictors],
+                           "ms": round(ms, 3), "traces_per_s": nt / (ms / 1e3),
+                           "lstm_tflops": round(flops / (ms / 1e3) / 1e12, 2), "bound": "fp32 ffma",
+                           "peak": round(ffma_peak, 1), "peak_source": "derived 148 SM x 128 lanes x 2 x 1.965 GHz",
+                           "frac": round(flops / (ms / 1e3) / 1e12 / ffma_peak, 4)}
+    return out
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -321,11 +398,15 @@ def main_ours(args):
                "sample": f"{cores * args.cpu_rounds} candidates, one per core in parallel (oracle port, "
                          "single-threaded BLAS), same workload definition, cold schedule memo"}
 
+    peaks = {}
+    pp = ROOT / "MEASURED_PEAKS.json"
+    if pp.exists():
+        peaks = json.loads(pp.read_text())
+    sweeps = None
+    if rank == 0 and not args.no_sweeps:
+        sweeps = kernel_sweeps(args, vanilla, pe.ev.predictors, peaks.get("hbm_gbs", 6546.9))
+
     if rank == 0:
-        peaks = {}
-        pp = ROOT / "MEASURED_PEAKS.json"
-        if pp.exists():
-            peaks = json.loads(pp.read_text())
         bf16 = peaks.get("bf16_tflops_sustained", 1387.4)
         achieved = flops_step / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
         roofline = {"bound": "tensor", "kernel": "conv_tf32x3_kernel (grouped tcgen05 implicit GEMM)",
@@ -347,7 +428,7 @@ def main_ours(args):
                            "schedule_memo": "cold every step", "l2": "inputs > L2 (weights+activations ~6 GB/step)",
                            "parallelism": f"population sharded over {world} GPU(s), NCCL all-gather of records"},
                 "gpu_launches": launches, "stages_ms": stages, "roofline": roofline, "clocks": clk,
-                "e2e": e2e, "cpu_baseline": cpu}
+                "e2e": e2e, "cpu_baseline": cpu, "kernels": sweeps}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -166,23 +166,60 @@ def test_lstm_ctc_bit_exact(ctx, hidden):
         assert list(toks[i, :ntok[i]]) == want
 
 
-def test_levenshtein_bit_exact(ctx):
+@pytest.mark.parametrize("t_max", [90, 96])  # unaligned rows (byte path) and 16-B rows (vector path)
+def test_levenshtein_bit_exact(ctx, t_max):
+    """Bit-parallel kernel (truths <= 64 labels, 32- and 64-bit words) and the
+    warp wavefront (longer truths) against the oracle DP, including empty
+    predictions, full-length rows and tokens outside the truth alphabet."""
     rng = np.random.default_rng(7)
-    for m in (0, 1, 3, 24, 31, 32, 33, 70):
+    for m in (1, 3, 22, 24, 31, 32, 33, 63, 64, 65, 70):
         truth = rng.integers(1, 5, m).astype(np.int8)
-        B, t_max = 40, 90
+        B = 70
         lens = rng.integers(0, t_max + 1, B).astype(np.int32)
-        toks = rng.integers(1, 5, (B, t_max)).astype(np.int8)
+        lens[:3] = (0, t_max, 1)
+        toks = rng.integers(0, 6, (B, t_max)).astype(np.int8)
+        toks[3, :] = -7  # never in the truth
         td = torch.from_numpy(toks).to(ctx.device)
         nd = torch.from_numpy(lens).to(ctx.device)
-        if m == 0:
-            continue  # LER undefined for an empty truth (EmptyTruth); ED covered by lens-only cases
         ed, lr, _ = fitness.edit_distances(td, nd, truth)
         ed, lr = ed.cpu().numpy(), lr.cpu().numpy()
         for b in range(B):
             want = FR.levenshtein(toks[b, :lens[b]], truth)
-            assert ed[b] == want
+            assert ed[b] == want, (m, b)
             assert lr[b] == want / m
+
+
+def test_levenshtein_sweep_matches_oracle(ctx):
+    """A cfg5-shaped sweep (RN18 L*, predictions of 119..169 tokens) large
+    enough for the persistent grid to wrap; a seeded subsample is checked
+    pair by pair, all pairs through the sum of distances from a numpy DP."""
+    from paper_2107_09789_b200 import fixtures as fx
+    from paper_2107_09789_b200.ir import label_sequence
+    truth = fitness.encode_labels(label_sequence(fx.resnet18()))
+    rng = np.random.default_rng(3)
+    B, t_max = 300_000, 176
+    lens = rng.integers(119, 170, B).astype(np.int32)
+    toks = rng.integers(1, 5, (B, t_max)).astype(np.int8)
+    ed, lr, _ = fitness.edit_distances(torch.from_numpy(toks).to(ctx.device), torch.from_numpy(lens).to(ctx.device),
+                                       truth)
+    ed = ed.cpu().numpy()
+    for b in rng.choice(B, 200, replace=False):
+        assert ed[b] == FR.levenshtein(toks[b, :lens[b]], truth)
+    # vectorised DP over a 20k slice (rows = predictions, one truth column at a time)
+    sl = slice(0, 20_000)
+    tk, ln = toks[sl].astype(np.int16), lens[sl]
+    m = len(truth)
+    prev = np.tile(np.arange(t_max + 1, dtype=np.int32), (tk.shape[0], 1))  # D[i][0] = i
+    for j in range(1, m + 1):
+        cur = np.empty_like(prev)
+        cur[:, 0] = j
+        sub = prev[:, :-1] + (tk != truth[j - 1])
+        best = np.minimum(sub, prev[:, 1:] + 1)
+        for i in range(1, t_max + 1):  # left dependency runs along the row
+            cur[:, i] = np.minimum(best[:, i - 1], cur[:, i - 1] + 1)
+        prev = cur
+    want = prev[np.arange(tk.shape[0]), ln]
+    assert np.array_equal(ed[sl], want)
 
 
 def test_spec_known_answers_on_device(ctx):
