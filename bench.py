@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=1, help="cpu_baseline sample: rounds of one candidate per core")
-    ap.add_argument("--micro", type=int, default=8, help="e2e micro-batch (host prep overlaps device run)")
+    ap.add_argument("--micro", type=lambda v: [int(x) for x in v.split(",")], default=[16],
+                    help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run)")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
     return ap.parse_args()
@@ -329,6 +330,7 @@ def main_ours(args):
     conv_ms = sum(a.elapsed_time(b) for a, b in conv_events) / args.steps
     conv_launches = len(conv_events) // args.steps
     flops_step = run.gemm_flops()
+    gemm_bytes_step = run.gemm_bytes()
     value = world * P / (ms / 1e3)
 
     # stage split of one extra (untimed-for-value) step
@@ -409,9 +411,19 @@ def main_ours(args):
     if rank == 0:
         bf16 = peaks.get("bf16_tflops_sustained", 1387.4)
         achieved = flops_step / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+        # traffic: dram__bytes_read.sum + dram__bytes_write.sum over one step's conv
+        # launches, from the committed ncu capture of this same command (ncu cannot
+        # run inside the timed region); null when no capture matches this workload
+        traffic, traffic_src = None, None
+        tp = ROOT / "profiles" / "conv_traffic.json"
+        if tp.exists():
+            tj = json.loads(tp.read_text())
+            if tj.get("flops_per_step") == flops_step and tj.get("conv_launches_per_step") == conv_launches:
+                traffic, traffic_src = tj["dram_bytes_per_step"], tj["source"]
         roofline = {"bound": "tensor", "kernel": "conv_tf32x3_kernel (grouped tcgen05 implicit GEMM)",
                     "achieved": round(achieved, 2), "peak": bf16, "unit": "TFLOP/s",
-                    "frac": round(achieved / bf16, 4), "traffic": None,
+                    "frac": round(achieved / bf16, 4), "traffic": traffic, "traffic_unit": "bytes per step",
+                    "traffic_source": traffic_src, "algorithmic_bytes_per_step": gemm_bytes_step,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)",
                     "flops_per_step": flops_step, "conv_ms_per_step": round(conv_ms, 3),
                     "conv_launches_per_step": conv_launches,

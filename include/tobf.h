@@ -63,11 +63,31 @@ typedef struct tobf_conv_desc {
   int32_t K, kblocks, mtiles, ntiles; /* filled by tobf_conv_prepare */
   int32_t tile_start, nepi, ldx, ldy; /* ldx/ldy = channel stride of the x/y buffers */
   tobf_epi_step epi[TOBF_MAX_EPI];
+  /* split-K (filled by tobf_conv_prepare / tobf_conv_prepare_split): a tile's
+   * K blocks are cut into `ksplit` work units of `kper` blocks; units write
+   * fp32 partial tiles to `ws` and the last unit of a tile (per-tile arrival
+   * counter in `cnt`, zero between launches) sums them in unit order and runs
+   * the epilogue. ksplit = 1: no workspace. */
+  float* ws;
+  int32_t* cnt;
+  int32_t ksplit, kper;
 } tobf_conv_desc;
 
 /* Fill K/kblocks/mtiles/ntiles/tile_start for a group of descriptors (host
- * memory) for the given N tile width (64 or 128); returns total tile count. */
+ * memory) for the given N tile width (64 or 128); returns total tile count
+ * (no split-K: ksplit = 1). */
 int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles);
+
+/* As tobf_conv_prepare, and split the K loop of long tiles when the group
+ * has too few tiles to balance `sms` SMs (work units of >= 16 K blocks,
+ * <= max_split units per tile). `tile_start` then counts work units. `ws` /
+ * `cnt` of split problems are set to ws_base / cnt_base plus their offsets
+ * (NULL bases: the byte offsets themselves, for the caller to rebase);
+ * *ws_floats and *cnt_count return the workspace (floats) and counter
+ * (int32, zero-initialised by the caller) extents this group needs. A group
+ * may share the workspace with any other group launched on the same stream. */
+int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split, float* ws_base,
+                            int32_t* cnt_base, int64_t* total_units, int64_t* ws_floats, int64_t* cnt_count);
 
 /* Bytes of the packed weight image for a conv with the given geometry. */
 int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n);

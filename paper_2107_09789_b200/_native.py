@@ -41,6 +41,7 @@ class ConvDesc(C.Structure):
         ("K", C.c_int32), ("kblocks", C.c_int32), ("mtiles", C.c_int32), ("ntiles", C.c_int32),
         ("tile_start", C.c_int32), ("nepi", C.c_int32), ("ldx", C.c_int32), ("ldy", C.c_int32),
         ("epi", EpiStep * TOBF_MAX_EPI),
+        ("ws", C.c_void_p), ("cnt", C.c_void_p), ("ksplit", C.c_int32), ("kper", C.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ class DeviceProfileC(C.Structure):
     ]
 
 
-assert C.sizeof(ConvDesc) == 200, C.sizeof(ConvDesc)
+assert C.sizeof(ConvDesc) == 224, C.sizeof(ConvDesc)
 assert C.sizeof(EwDesc) == 176, C.sizeof(EwDesc)
 assert C.sizeof(KernDesc) == 136, C.sizeof(KernDesc)
 
@@ -87,6 +88,8 @@ _vp, _i32, _i64, _f32, _f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_d
 # name -> (restype, argtypes); mirrors include/tobf.h one to one.
 SIGNATURES = {
     "tobf_conv_prepare": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_i64)]),
+    "tobf_conv_prepare_split": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, C.POINTER(_i64),
+                                          C.POINTER(_i64), C.POINTER(_i64)]),
     "tobf_wimg_bytes": (_i64, [_i32, _i32, _i32, _i32, _i32]),
     "tobf_pack_weights": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "tobf_conv_grouped": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _vp]),

@@ -94,7 +94,20 @@ __device__ unsigned long long g_conv_prof[32];
 #define PROF_FLUSH(base)
 #endif
 
-constexpr int kInfoSlots = 4;
+// Tile-info ring depth: how many tiles the scheduler warp may claim ahead of
+// the drain. Tiles are claimed dynamically (atomic counter): an idle SM takes
+// the next tile instead of a pre-assigned one waiting behind a long tile
+// elsewhere. Must be >= 4: the A producer issues cp.async up to
+// kStagingKB-1 = 3 K blocks ahead of its split, which for 1-K-block tiles is
+// 3 tiles ahead, while a slot frees only when its tile is fully drained.
+#ifndef TOBF_CONV_INFO_SLOTS
+#define TOBF_CONV_INFO_SLOTS 4
+#endif
+constexpr int kInfoSlots = TOBF_CONV_INFO_SLOTS;
+// Dynamic tile counters: [0] next tile (beyond the first gridDim.x), [1] CTAs
+// exited; the last CTA to exit resets both, so consecutive launches (stream
+// ordered: every conv of the executor runs on its engine stream) start at 0.
+__device__ int g_conv_sched[2][2];
 constexpr int kInfoConsumers = 4 /*A warps*/ + 1 /*B*/ + 1 /*MMA*/ + 4 /*drain warps*/;
 
 __device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ descs, int lo, int nprob, int tile) {
@@ -269,6 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
   uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + kInfoSlots);
+  volatile int* info_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kInfoSlots], -1 = no more tiles
+  volatile int* split_last = info_tile + kInfoSlots;  // drain: this unit completes its split-K tile
+  int* sched = g_conv_sched[BN >= 128 ? 1 : 0];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -314,7 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     PROF_DECL;
     PROF_T0();
     // ---- issue cursor state (current tile of the issue side)
-    int itile = blockIdx.x, iit = 0, ikb = 0, ikblocks = 0;
+    int iit = 0, ikb = 0, ikblocks = 0;
+    bool adone = false;
     const float* x = nullptr;
     const float* rowp[8];
     int yb[8], xb[8];
@@ -324,15 +341,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 8; ++i) { rowp[i] = nullptr; yb[i] = xb[i] = -(1 << 28); }
     auto ensure = [&]() -> bool {  // a K block is ready to issue (fetches the next tile's descriptor)
       while (ikb == ikblocks) {
-        if (itile >= total_tiles) return false;
+        if (adone) return false;
         const int islot = iit % kInfoSlots;
         PROF_WAIT(0, mbar_wait(&info_full[islot], (iit / kInfoSlots) & 1, 0x110));
+        const int itile = info_tile[islot];
+        if (itile < 0) {
+          adone = true;
+          return false;
+        }
         const tobf_conv_desc& d = info[islot];
         const int lt = itile - d.tile_start;
-        const int m0 = (lt / d.ntiles) * kBM + 32 * warp + rsub;
+        const int t2 = lt / d.ksplit;             // tile within the problem
+        const int kb0 = (lt - t2 * d.ksplit) * d.kper;  // first K block of this work unit
+        const int m0 = (t2 / d.ntiles) * kBM + 32 * warp + rsub;
         const int HWo = d.Ho * d.Wo;
         const int M = d.batch * HWo;
-        ikblocks = d.kblocks;
+        ikblocks = min(d.kper, d.kblocks - kb0);
         Cp = d.Cp; k1 = d.k1; k2 = d.k2; H = d.H; W = d.W; ldx = d.ldx;
         x = d.x;
 #pragma unroll
@@ -351,16 +375,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             rowp[i] = x;
           }
         }
-        u = 0; v = 0; c0 = chunk * 4;
-        while (c0 >= Cp) {
-          c0 -= Cp;
-          if (++v == k2) { v = 0; ++u; }
+        {  // cursor at K element kb0*kBK + chunk*4 = ((u*k2 + v)*Cp + c0)
+          const int k0 = kb0 * kBK + chunk * 4;
+          const int tap = k0 / Cp;
+          c0 = k0 - tap * Cp;
+          u = tap / k2;
+          v = tap - u * k2;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
         ikb = 0;
         ++iit;
-        itile += gridDim.x;
       }
       return true;
     };
@@ -449,15 +474,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       PROF_DECL;
       PROF_T0();
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      for (;; ++it) {
         const int islot = it % kInfoSlots;
         PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x111));
+        const int tile = info_tile[islot];
+        if (tile < 0) break;
         const tobf_conv_desc& d = info[islot];
         const int lt = tile - d.tile_start;
-        const int n_tile = lt - (lt / d.ntiles) * d.ntiles;
-        const int kblocks = d.kblocks;
+        const int t2 = lt / d.ksplit;
+        const int kb0 = (lt - t2 * d.ksplit) * d.kper;
+        const int n_tile = t2 - (t2 / d.ntiles) * d.ntiles;
+        const int kblocks = min(d.kper, d.kblocks - kb0);
         const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
-                              (int64_t)n_tile * kblocks * (2 * Cfg::kBBytes);
+                              ((int64_t)n_tile * d.kblocks + kb0) * (2 * Cfg::kBBytes);
         mbar_arrive(&info_empty[islot]);
         for (int kb = 0; kb < kblocks; ++kb) {
           PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x104));
@@ -485,10 +514,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;  // local tile counter (correction accumulator slot)
     PROF_DECL;
     PROF_T0();
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    for (;; ++it) {
       const int islot = it % kInfoSlots;
       PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x112));
-      const int kblocks = __shfl_sync(0xffffffffu, info[islot].kblocks, 0);
+      const int mtile = info_tile[islot];
+      if (mtile < 0) break;
+      int kblocks;
+      {
+        const tobf_conv_desc& d = info[islot];
+        const int lt = mtile - d.tile_start;
+        const int kb0 = (lt % d.ksplit) * d.kper;
+        kblocks = min(d.kper, d.kblocks - kb0);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_empty[islot]);
       const int slot = it % Cfg::kCorrSlots;
@@ -536,20 +573,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     int gc = 0, it = 0;
     PROF_DECL;
     PROF_T0();
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    for (;; ++it) {
       const int islot = it % kInfoSlots;
       // one drain warp polls, the other three sleep in the named barrier
       // (polling warps take issue slots from the producers on their SMSPs)
       if (ew == 0) PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x113));
       asm volatile("bar.sync 2, 128;" ::: "memory");
+      const int tile = info_tile[islot];
+      if (tile < 0) break;
       const tobf_conv_desc& d = info[islot];
       const int lt = tile - d.tile_start;
-      const int m_tile = lt / d.ntiles;
-      const int n_tile = lt - m_tile * d.ntiles;
+      const int t2 = lt / d.ksplit;
+      const int ks = lt - t2 * d.ksplit;
+      const int m_tile = t2 / d.ntiles;
+      const int n_tile = t2 - m_tile * d.ntiles;
       const int m0 = m_tile * kBM;
       const int HWo = d.Ho * d.Wo;
       const int M = d.batch * HWo;
-      const int kblocks = d.kblocks;
+      const int kblocks = min(d.kper, d.kblocks - ks * d.kper);
       const int slot = it % Cfg::kCorrSlots;
       float sum[BN];
 #pragma unroll
@@ -604,7 +645,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long _e1 = clock64();
       _pacc[3] += _e1 - _e0;
 #endif
+      bool run_epi = true;
+      if (d.ksplit > 1) {
+        // ---- split-K: publish this unit's partial tile (coalesced rows), count
+        // arrivals; the last unit of the tile sums all partials in unit order
+        // (deterministic whichever unit arrives last) back into the staging
+        // buffer and runs the epilogue. Partials stay L2-resident.
+        constexpr int kLPR = BN / 4, kRPI = 32 / kLPR;
+        const int sub = lane / kLPR, g = lane % kLPR;
+        const int S = d.ksplit;
+        float* part0 = d.ws + (int64_t)t2 * S * (kBM * BN);
+        float* mine = part0 + (int64_t)ks * (kBM * BN);
+#pragma unroll 4
+        for (int row = ew * kRPI + sub; row < kBM; row += 4 * kRPI)
+          __stcg(reinterpret_cast<float4*>(mine + row * BN + g * 4), lds_tile(epi_s, row, g, BN));
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ew == 0 && lane == 0) *split_last = atomicAdd(d.cnt + t2, 1) == S - 1 ? 1 : 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        run_epi = *split_last != 0;
+        if (run_epi) {
+          __threadfence();
+#pragma unroll 2
+          for (int row = ew * kRPI + sub; row < kBM; row += 4 * kRPI) {
+            const float* src = part0 + row * BN + g * 4;
+            float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+            for (int q = 1; q < S; ++q) {
+              const float4 p = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)q * (kBM * BN)));
+              acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+            }
+            sts128(epi_s + row * BN * 4 + ((g ^ (row & (BN / 4 - 1))) << 4), acc);
+          }
+          if (ew == 0 && lane == 0) atomicExch(d.cnt + t2, 0);  // ready for the next launch
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+      }
 
+      if (run_epi) {
       // ---- fused epilogue over the staged tile -----------------------------
       const int nepi = d.nepi;
       int eop[TOBF_MAX_EPI], eaux[TOBF_MAX_EPI];
@@ -660,6 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         epi_rows_generic<BN>(ea, d, ew, lane, HWo);
       }
+      }  // run_epi
 #ifdef TOBF_CONV_PROF
       const long long _e3 = clock64();
       _pacc[5] += _e3 - _e2;
@@ -678,17 +756,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   } else if (warp == 6) {
     // ---------------------------------------------------------- tile scheduler
-    int prob = 0, it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    // Claims tiles: the CTA's first tile is blockIdx.x, every further one
+    // comes from the launch-wide counter (tiles are in longest-K-first order,
+    // so greedy claiming is an LPT schedule).
+    int prob = 0;
+    for (int it = 0;; ++it) {
       const int islot = it % kInfoSlots;
       mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
-      prob = find_problem(descs, prob, nprob, tile);  // tiles only increase: search forward
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
-      uint64_t* dst = reinterpret_cast<uint64_t*>(info + islot);
-      constexpr int kWords = sizeof(tobf_conv_desc) / 8;
-      if (lane < kWords) dst[lane] = __ldg(src + lane);
+      int tile = 0;
+      if (lane == 0) tile = it == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&sched[0], 1);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile >= total_tiles) tile = -1;
+      if (tile >= 0) {
+        prob = find_problem(descs, prob, nprob, tile);  // a CTA's tiles only increase: search forward
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(info + islot);
+        constexpr int kWords = sizeof(tobf_conv_desc) / 8;
+        if (lane < kWords) dst[lane] = __ldg(src + lane);
+      }
+      if (lane == 0) info_tile[islot] = tile;
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_full[islot]);
+      if (tile < 0) break;
     }
   }
 
@@ -697,6 +786,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+  if (threadIdx.x == 0) {
+    // every claim of this CTA happened before the barrier above; the last CTA
+    // out resets the counters for the next launch
+    __threadfence();
+    if (atomicAdd(&sched[1], 1) == (int)gridDim.x - 1) {
+      atomicExch(&sched[0], 0);
+      atomicExch(&sched[1], 0);
+    }
   }
 }
 
@@ -761,10 +859,61 @@ extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int6
     d.mtiles = (int)((M + kBM - 1) / kBM);
     d.ntiles = (d.j + block_n - 1) / block_n;
     d.tile_start = (int)acc;
+    d.ksplit = 1;
+    d.kper = d.kblocks;
+    d.ws = nullptr;
+    d.cnt = nullptr;
     acc += (int64_t)d.mtiles * d.ntiles;
   }
   if (acc >= (int64_t)1 << 31) return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare: too many tiles");
   *total_tiles = acc;
+  return TOBF_OK;
+}
+
+// Split policy: a group with fewer than 2 tiles per SM leaves SMs idle behind
+// its longest tiles; cut K into work units of U >= 16 K blocks, U chosen so
+// the group has ~4 units per SM (the partial write + read of a 128 x BN fp32
+// tile costs about as much as 3-4 K blocks of MMAs, hence the floor).
+extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split,
+                                       float* ws_base, int32_t* cnt_base, int64_t* total_units,
+                                       int64_t* ws_floats, int64_t* cnt_count) {
+  int64_t tiles = 0;
+  int rc = tobf_conv_prepare(descs, n, block_n, &tiles);
+  if (rc != TOBF_OK) return rc;
+  if (sms < 1 || max_split < 1 || !total_units || !ws_floats || !cnt_count)
+    return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare_split: bad arguments");
+  *ws_floats = 0;
+  *cnt_count = 0;
+  int64_t work = 0;
+  for (int i = 0; i < n; ++i) work += (int64_t)descs[i].mtiles * descs[i].ntiles * descs[i].kblocks;
+  if (tiles >= 2 * (int64_t)sms || max_split == 1) {
+    *total_units = tiles;
+    return TOBF_OK;
+  }
+  const int64_t per_unit = std::max<int64_t>(16, (work + 4 * (int64_t)sms - 1) / (4 * (int64_t)sms));
+  int64_t acc = 0, wsf = 0, cnts = 0;
+  for (int i = 0; i < n; ++i) {
+    tobf_conv_desc& d = descs[i];
+    int s = (int)std::min<int64_t>(max_split, (d.kblocks + per_unit - 1) / per_unit);
+    s = std::max(s, 1);
+    const int kper = (d.kblocks + s - 1) / s;
+    s = (d.kblocks + kper - 1) / kper;  // no empty unit
+    const int64_t t = (int64_t)d.mtiles * d.ntiles;
+    d.tile_start = (int)acc;
+    d.ksplit = s;
+    d.kper = kper;
+    if (s > 1) {  // NULL bases: byte offsets, for the caller to rebase
+      d.ws = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(ws_base) + wsf * sizeof(float));
+      d.cnt = reinterpret_cast<int32_t*>(reinterpret_cast<uintptr_t>(cnt_base) + cnts * sizeof(int32_t));
+      wsf += t * s * kBM * block_n;
+      cnts += t;
+    }
+    acc += t * s;
+  }
+  if (acc >= (int64_t)1 << 31) return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare_split: too many units");
+  *total_units = acc;
+  *ws_floats = wsf;
+  *cnt_count = cnts;
   return TOBF_OK;
 }
 

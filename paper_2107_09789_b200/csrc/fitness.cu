@@ -369,44 +369,51 @@ __global__ void levenshtein_kernel(const int8_t* __restrict__ pred, const int32_
 
 // Bit-parallel edit distance (Myers 1999 / Hyyrö 2003 global variant), one
 // THREAD per (prediction, truth) pair, for truths of up to 64 labels (every
-// fixture: RN18 24, VGG16 22, C1C2 3). Bit i of the vertical delta vectors
-// Pv/Mv is D[i+1][j] - D[i][j] = +1/-1 for truth row i; one prediction token
-// advances the whole column in ~17 integer ops, so a 144-token prediction is
-// 144 steps instead of the warp wavefront's (n + 32) x ceil(m/32) shuffle
-// steps. Bits above m-1 hold garbage but never reach the low m bits (carries
-// and shifts only move upwards). Exact integer arithmetic: identical ED.
+// fixture: RN18 24, VGG16 22, C1C2 3). Bit i of Pv / Mv is the vertical delta
+// D[i+1][j] - D[i][j] = +1 / -1 of truth row i in DP column j; one prediction
+// token advances the whole column in 10 integer ops plus one shared-memory
+// Peq lookup, so a 144-token prediction is 144 such steps instead of the warp
+// wavefront's (n + 32) x ceil(m/32) shuffle steps. No per-step score: the
+// final column gives D[m][n] = D[0][n] + sum of its deltas
+//   = n + popc(Pv & mask) - popc(Mv & mask).
+// Bits above m-1 hold garbage that never reaches the low m bits (carries and
+// shifts only move upwards). Exact integer arithmetic: identical ED.
 //
 // Data movement: the Peq table (bit j set where truth[j] == c, 256 entries) is
-// built once per CTA in shared memory; the persistent grid walks 32-pair warp
-// tiles; each thread streams its own token row with 16-B loads (or bytes when
-// rows are not 16-B aligned), prefetching the next chunk while the current one
-// is consumed. Every token byte is read once: HBM traffic = sum of prediction
-// lengths (rounded up to 16 B) + ntok + ED + LER.
+// built once per CTA in shared memory; the persistent grid walks pairs
+// thread-strided; each thread streams its own token row with 16-B loads (or
+// bytes when rows are not 16-B aligned), prefetching the next chunk while the
+// current one is consumed; full chunks run 16 unpredicated steps. Every token
+// byte is read once: HBM traffic = sum of prediction lengths (rounded up to
+// 16 B) + ntok + ED + LER.
 template <typename W>
-__device__ __forceinline__ void myers_step(W eq, W& pv, W& mv, int& score, W hb) {
+__device__ __forceinline__ void myers_step(W eq, W& pv, W& mv) {
   const W xv = eq | mv;
   const W xh = (((eq & pv) + pv) ^ pv) | eq;
-  W ph = mv | ~(xh | pv);
-  W mh = pv & xh;
-  score += (ph & hb) ? 1 : 0;
-  score -= (mh & hb) ? 1 : 0;
-  ph = (ph << 1) | (W)1;  // row 0 of the DP is D[0][j] = j: horizontal delta +1
-  mh = mh << 1;
-  pv = mh | ~(xv | ph);
-  mv = ph & xv;
+  const W ph = mv | ~(xh | pv);
+  const W mh = pv & xh;
+  const W phs = (ph << 1) | (W)1;  // row 0 of the DP is D[0][j] = j: horizontal delta +1
+  const W mhs = mh << 1;
+  pv = mhs | ~(xv | phs);
+  mv = phs & xv;
 }
 
 template <typename W>
-__device__ __forceinline__ void myers_chunk(uint4 v, int cnt, const W* peq, W& pv, W& mv, int& score, W hb) {
+__device__ __forceinline__ const W& peq_at(const W* peq, uint32_t word, int k) {
+  return peq[(word >> (8 * k)) & 0xFFu];
+}
+
+template <typename W>
+__device__ __forceinline__ void myers_chunk16(uint4 v, const W* peq, W& pv, W& mv) {
   const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (q * 4 + k < cnt) myers_step<W>(peq[(w4[q] >> (8 * k)) & 0xFFu], pv, mv, score, hb);
-    }
-  }
+    for (int k = 0; k < 4; ++k) myers_step<W>(peq_at(peq, w4[q], k), pv, mv);
 }
+
+__device__ __forceinline__ int popc_w(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc_w(unsigned long long x) { return __popcll(x); }
 
 template <typename W>
 __global__ void __launch_bounds__(256) levenshtein_bp_kernel(const int8_t* __restrict__ pred,
@@ -420,26 +427,29 @@ __global__ void __launch_bounds__(256) levenshtein_bp_kernel(const int8_t* __res
     peq[c] = bits;
   }
   __syncthreads();
-  const W hb = (W)1 << (m - 1);
+  const W mask = m == (int)(8 * sizeof(W)) ? ~(W)0 : (((W)1 << m) - 1);
   const bool vec = ((T_max & 15) == 0) && ((reinterpret_cast<uintptr_t>(pred) & 15) == 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += stride) {
     const int n = min(max(ntok[b], 0), T_max);
     const int8_t* p = pred + b * (int64_t)T_max;
     W pv = ~(W)0, mv = 0;
-    int score = m;
+    int i = 0;
     if (vec) {
       const uint4* p4 = reinterpret_cast<const uint4*>(p);
-      const int nch = (n + 15) >> 4;
-      uint4 cur = nch > 0 ? __ldg(p4) : make_uint4(0, 0, 0, 0);
-      for (int ch = 0; ch < nch; ++ch) {
-        const uint4 nxt = ch + 1 < nch ? __ldg(p4 + ch + 1) : cur;
-        myers_chunk<W>(cur, min(16, n - 16 * ch), peq, pv, mv, score, hb);
+      const int full = n >> 4;
+      uint4 cur = full > 0 ? __ldg(p4) : make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+      for (int ch = 0; ch < full; ++ch) {
+        const uint4 nxt = ch + 1 < full ? __ldg(p4 + ch + 1) : cur;
+        myers_chunk16<W>(cur, peq, pv, mv);
         cur = nxt;
       }
-    } else {
-      for (int i = 0; i < n; ++i) myers_step<W>(peq[(uint8_t)__ldg(p + i)], pv, mv, score, hb);
+      i = full << 4;
     }
+#pragma unroll 1
+    for (; i < n; ++i) myers_step<W>(peq[(uint8_t)__ldg(p + i)], pv, mv);
+    const int score = n + popc_w(pv & mask) - popc_w(mv & mask);
     ed[b] = score;
     ler[b] = (double)score / (double)m;
   }

@@ -37,6 +37,7 @@ class DeviceContext:
         self.device = torch.device("cuda", index)
         torch.cuda.set_device(self.device)
         self.stream = torch.cuda.current_stream(self.device)
+        self.sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         # cache of device copies of host weight arrays, keyed by id(base array);
         # the base array is held so ids are never recycled while cached
         self.weight_cache: dict[int, tuple[np.ndarray, torch.Tensor]] = {}
@@ -138,7 +139,10 @@ class DeviceContext:
 
     def sync(self) -> None:
         self.stream.synchronize()
-        self.check(self.lib.tobf_check_fault(C.c_void_p(self.sp)), "device pipeline")
+        rc = self.lib.tobf_check_fault(C.c_void_p(self.sp))
+        if rc != 0 and self.__dict__.get("splitk_cnt") is not None:
+            self.splitk_cnt.zero_()  # a drained (faulted) launch may leave split-K counters mid-count
+        self.check(rc, "device pipeline")
 
 
 def _root(a: np.ndarray) -> np.ndarray:

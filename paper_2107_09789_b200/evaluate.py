@@ -250,7 +250,7 @@ class PopulationEvaluator:
         self.ctx.sync()
         return rec
 
-    def evaluate_records(self, plans: list[ObfuscationPlan], micro: int = 8, memo: dict | None = None,
+    def evaluate_records(self, plans: list[ObfuscationPlan], micro=16, memo: dict | None = None,
                          workers: int | None = None) -> np.ndarray:
         """Records for ``plans`` with host preparation of micro-batch i+1
         overlapping the device pipeline of micro-batch i (launches are async;
@@ -262,6 +262,7 @@ class PopulationEvaluator:
         from its first occurrence's descriptor everywhere."""
         first_seen: dict = {}
         jobs = []
+        bounds = _micro_bounds(len(plans), micro)
         if workers is None:
             from .hostpipe import default_workers
             workers = default_workers() if os.environ.get("TOBF_HOST_WORKERS", "") != "0" else 0
@@ -272,8 +273,7 @@ class PopulationEvaluator:
             got: dict[int, tuple] = {}
             nxt = 0  # next handle to receive
             wait = 0.0
-            for lo in range(0, len(plans), micro):
-                hi = min(len(plans), lo + micro)
+            for lo, hi in bounds:
                 t0 = time.perf_counter()
                 while nxt * per_job < hi:
                     for r in self.pool.result(handles[nxt]):
@@ -284,16 +284,22 @@ class PopulationEvaluator:
                                             first_seen=first_seen)
                 prep["host_ms"]["wait_workers"] = 1e3 * wait
                 wait = 0.0
+                t1 = time.perf_counter()
                 jobs.append((prep, self.run(prep, cold_schedules=False)))
+                prep["host_ms"]["launch"] = 1e3 * (time.perf_counter() - t1)
         else:
-            for lo in range(0, len(plans), micro):
-                prep = self.prepare(plans[lo:lo + micro], memo=memo, first_seen=first_seen)
+            for lo, hi in bounds:
+                prep = self.prepare(plans[lo:hi], memo=memo, first_seen=first_seen)
+                t1 = time.perf_counter()
                 jobs.append((prep, self.run(prep, cold_schedules=False)))
+                prep["host_ms"]["launch"] = 1e3 * (time.perf_counter() - t1)
+        t1 = time.perf_counter()
         recs = [self.collect(out) for _, out in jobs]
+        jobs[0][0]["host_ms"]["collect"] = 1e3 * (time.perf_counter() - t1)
         for prep, _ in jobs:
             if prep["trace"] is not None:
                 finish_trace(prep["trace"])
-        self.last_host_ms = {k: sum(p["host_ms"][k] for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
+        self.last_host_ms = {k: sum(p["host_ms"].get(k, 0.0) for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
         return np.concatenate(recs)
 
     def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
@@ -314,6 +320,21 @@ class PopulationEvaluator:
                                          equivalent=bool(r["ok"]) if c.graph is not None else None,
                                          worst_rel=float(r["worst"]) if c.graph is not None else None))
         return PopulationResult(rec, self.t_star, stage, prep["run"].gemm_flops(), reports)
+
+
+def _micro_bounds(n: int, micro) -> list[tuple[int, int]]:
+    """Micro-batch [lo, hi) ranges: ``micro`` is a size (every batch that big,
+    the last one ragged) or a sequence of sizes (the last one repeats), e.g.
+    (8, 24): a small first batch gets the device busy early."""
+    sizes = [int(micro)] if isinstance(micro, (int, np.integer)) else [int(m) for m in micro]
+    if not sizes or min(sizes) < 1:
+        raise ValueError(f"bad micro-batch sizes {micro!r}")
+    out, lo, i = [], 0, 0
+    while lo < n:
+        hi = min(n, lo + sizes[min(i, len(sizes) - 1)])
+        out.append((lo, hi))
+        lo, i = hi, i + 1
+    return out
 
 
 def fitness(plan: ObfuscationPlan, graph: Graph, evaluator: Evaluator, budget: float, t_star: float | None = None,

@@ -352,6 +352,8 @@ class ForwardPlan:
     out_shape: TensorShape
     input_shape: TensorShape
     flops_per_image: int
+    gemm_act_bytes_per_image: int = 0   # conv/linear input + output activations, fp32, once each
+    gemm_weight_bytes: int = 0          # conv/linear weights, fp32, once
 
 
 def _gemm_geom(lw: Lowered, op: Op, s_in: TensorShape):
@@ -408,6 +410,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
     conv_rows, conv_lv, conv_bn, conv_k = [], [], [], []
     ew_rows, ew_lv = [], []
     flops = 0
+    act_bytes = w_bytes = 0
     for op in lw.ops:
         s_in = shapes[op.src] if op.src >= 0 else ishape
         s_out = shapes[op.out]
@@ -421,13 +424,16 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
             else:
                 stride, pad = 1, 0
                 flops += 2 * ishape.batch * j * s_in.channels * s_in.height * s_in.width
+            act_bytes += 4 * ishape.batch * (s_in.height * s_in.width * s_in.channels +
+                                             s_out.height * s_out.width * j)
+            w_bytes += 4 * k1 * k2 * s_in.channels * j
             w = n.weights if op.w is None else op.w
             wi = index("wimg", (refs.ref(w), n.kind is K.Conv2D, s_in.height, s_in.width, s_in.channels,
                                 k1, k2, cp, j, bn))
             epi = epi_rows(op.steps)
             conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
                               s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
-                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi))
+                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0))
             conv_lv.append(op.level)
             conv_bn.append(bn)
             conv_k.append(k1 * k2 * cp)
@@ -463,7 +469,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
         ew_level=np.array(ew_lv, np.int32),
         wimg=tables["wimg"][1], affine=tables["affine"][1], const=tables["const"][1],
         arena_bytes=used, out_off=offs[lw.out_node], out_shape=shapes[lw.out_node], input_shape=ishape,
-        flops_per_image=flops)
+        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes)
 
 
 def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, tables: dict) -> np.ndarray:
@@ -484,6 +490,24 @@ def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, 
         if m.any():
             out[m] = ptrs[offsets[rp[m]] + val[m]]
     return out
+
+
+SPLITK_MAX = 16  # work units per tile at most
+
+
+def splitk_workspace(ctx: DeviceContext, floats: int, counters: int):
+    """The context's split-K workspace (partial tiles) and per-tile arrival
+    counters, grown on demand. Shared by every conv launch: they are ordered
+    on the engine stream, and the last unit of each tile re-zeroes its counter."""
+    ws, cnt = ctx.__dict__.get("splitk_ws"), ctx.__dict__.get("splitk_cnt")
+    if ws is None or ws.numel() < floats:
+        ws = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=ctx.device)
+        ctx.splitk_ws = ws
+    if cnt is None or cnt.numel() < counters:
+        # a fresh zeroed buffer: counters of the old one may be mid-launch
+        cnt = torch.zeros(int(counters * 1.25) + 256, dtype=torch.int32, device=ctx.device)
+        ctx.splitk_cnt = cnt
+    return ws, cnt
 
 
 class PopulationRun:
@@ -654,15 +678,25 @@ class PopulationRun:
         ekey = ew_level[eorder]
         launches = []
         lo = 0
+        ws_need = cnt_need = 0
         while lo < len(conv):
             hi = lo + 1
             while hi < len(conv) and ckey[hi, 0] == ckey[lo, 0] and ckey[hi, 1] == ckey[lo, 1]:
                 hi += 1
-            tot = C.c_int64()
-            ctx.check(lib.tobf_conv_prepare(C.c_void_p(conv[lo:].ctypes.data), hi - lo, int(ckey[lo, 1]),
-                                            C.byref(tot)), "conv prepare")
+            tot, wsf, cnts = C.c_int64(), C.c_int64(), C.c_int64()
+            # split-K for groups too small to fill the SMs; workspace offsets
+            # now, one workspace shared by every (stream-ordered) conv launch
+            ctx.check(lib.tobf_conv_prepare_split(C.c_void_p(conv[lo:].ctypes.data), hi - lo, int(ckey[lo, 1]),
+                                                  ctx.sms, SPLITK_MAX, None, None, C.byref(tot), C.byref(wsf),
+                                                  C.byref(cnts)), "conv prepare")
+            ws_need, cnt_need = max(ws_need, wsf.value), max(cnt_need, cnts.value)
             launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, int(ckey[lo, 1])))
             lo = hi
+        if ws_need:
+            ws, cnt = splitk_workspace(ctx, ws_need, cnt_need)
+            split = conv["ksplit"] > 1
+            conv["ws"][split] += np.uint64(ws.data_ptr())
+            conv["cnt"][split] += np.uint64(cnt.data_ptr())
         lo = 0
         while lo < len(ew):
             hi = lo + 1
@@ -728,6 +762,12 @@ class PopulationRun:
         emitted (obfuscated) layers, 2*M*N*K each; a fused sibling group counts
         exactly the sum of its parts."""
         return sum(p.flops_per_image for p in self.plans) * self.reps
+
+    def gemm_bytes(self) -> int:
+        """Algorithmic conv/linear HBM bytes of one run: every input and output
+        activation once per stacked trial, every weight once (fp32)."""
+        return sum(p.gemm_act_bytes_per_image for p in self.plans) * self.reps + \
+            sum(p.gemm_weight_bytes for p in self.plans)
 
 
 # ---------------------------------------------------------------------------

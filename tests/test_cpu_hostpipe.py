@@ -57,3 +57,14 @@ def test_pool_matches_in_process(population):
             assert np.array_equal(x, y)
         ref_ct, _, _ = trace_records(og, d.fusion_limits, d.schedule_strategies, "default", ana)
         assert np.array_equal(ct.recs, ref_ct.recs) and ct.sigs == ref_ct.sigs
+
+
+def test_micro_batch_bounds():
+    from paper_2107_09789_b200.evaluate import _micro_bounds
+    assert _micro_bounds(32, 16) == [(0, 16), (16, 32)]
+    assert _micro_bounds(7, 3) == [(0, 3), (3, 6), (6, 7)]
+    assert _micro_bounds(32, (8, 24)) == [(0, 8), (8, 32)]
+    assert _micro_bounds(30, [4, 12]) == [(0, 4), (4, 16), (16, 28), (28, 30)]
+    assert _micro_bounds(0, 8) == []
+    with pytest.raises(ValueError):
+        _micro_bounds(4, 0)

@@ -41,12 +41,13 @@ def test_struct_layouts_match_header(tmp_path):
     src.write_text(f'#include "{HEADER}"\n#include <stdio.h>\n#include <stddef.h>\n'
                    "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(tobf_conv_desc),"
                    " sizeof(tobf_ew_desc), sizeof(tobf_kern_desc), offsetof(tobf_conv_desc, epi),"
-                   " offsetof(tobf_ew_desc, work_start), offsetof(tobf_kern_desc, ty)); return 0;}\n")
+                   " offsetof(tobf_ew_desc, work_start), offsetof(tobf_kern_desc, ty));"
+                   " printf(\"%zu %zu\\n\", offsetof(tobf_conv_desc, ws), offsetof(tobf_conv_desc, kper)); return 0;}\n")
     exe = tmp_path / "sz"
     subprocess.run(["gcc", str(src), "-o", str(exe)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert got == [C.sizeof(N.ConvDesc), C.sizeof(N.EwDesc), C.sizeof(N.KernDesc), N.ConvDesc.epi.offset,
-                   N.EwDesc.work_start.offset, N.KernDesc.ty.offset]
+                   N.EwDesc.work_start.offset, N.KernDesc.ty.offset, N.ConvDesc.ws.offset, N.ConvDesc.kper.offset]
 
 
 def test_conv_prepare_tiles_and_validation(lib):
@@ -94,3 +95,49 @@ def test_invalid_arguments_never_throw(lib):
     assert lib.tobf_lstm_ctc(None, None, 4, 9, 128, 5, None, None, None, None, None, None, 8, None, None) != 0
     assert lib.tobf_levenshtein(None, None, 4, 8, None, 3, None, None, None) != 0
     assert lib.tobf_version() >= 1
+
+
+def _descs(shapes):
+    arr = (N.ConvDesc * len(shapes))()
+    for d, (b, h, c, j, k) in zip(arr, shapes):
+        d.batch, d.H, d.W, d.Cp = b, h, h, c
+        d.Ho, d.Wo, d.Cpo, d.j = h, h, j, j
+        d.k1 = d.k2 = k
+        d.stride, d.pad, d.ldx, d.ldy = 1, k // 2, c, j
+    return arr
+
+
+def test_conv_prepare_split_policy(lib):
+    """Split-K only for groups with < 2 tiles per SM; units of >= 16 K blocks,
+    no empty unit, tile_start counts units, workspace offsets per split tile."""
+    tot, wsf, cnt = C.c_int64(), C.c_int64(), C.c_int64()
+    # many tiles: no split, identical to tobf_conv_prepare
+    big = _descs([(8, 56, 64, 64, 3)] * 2)
+    assert lib.tobf_conv_prepare_split(big, 2, 64, 148, 16, None, None, C.byref(tot), C.byref(wsf), C.byref(cnt)) == 0
+    assert tot.value == 2 * 196 and wsf.value == 0 and cnt.value == 0
+    assert all(d.ksplit == 1 and d.kper == d.kblocks and not d.ws for d in big)
+    # stage-4 shaped tail: 3 problems of 4 x 4 tiles, K = 4608 (144 blocks) / 512 (16 blocks)
+    small = _descs([(8, 7, 512, 512, 3), (8, 7, 512, 512, 3), (8, 7, 512, 512, 1)])
+    base = 1 << 20
+    assert lib.tobf_conv_prepare_split(small, 3, 128, 148, 16, C.c_void_p(base), C.c_void_p(base * 4),
+                                       C.byref(tot), C.byref(wsf), C.byref(cnt)) == 0
+    units = 0
+    for d in small:
+        assert d.kper >= 16 or d.ksplit == 1
+        assert (d.ksplit - 1) * d.kper < d.kblocks <= d.ksplit * d.kper
+        assert d.tile_start == units
+        units += d.mtiles * d.ntiles * d.ksplit
+    assert tot.value == units
+    assert small[0].ksplit > 1 and small[2].ksplit == 1 and not small[2].ws
+    assert small[0].ws == base and small[0].cnt == base * 4
+    assert small[1].ws == base + 4 * 16 * small[0].ksplit * 128 * 128
+    assert wsf.value == 16 * 128 * 128 * (small[0].ksplit + small[1].ksplit)
+    assert cnt.value == 32
+    # NULL bases: byte offsets for the caller to rebase (executor.py does)
+    assert lib.tobf_conv_prepare_split(small, 3, 128, 148, 16, None, None, C.byref(tot), C.byref(wsf),
+                                       C.byref(cnt)) == 0
+    assert not small[0].ws and small[1].ws == 4 * 16 * small[0].ksplit * 128 * 128 and small[1].cnt == 4 * 16
+    # max_split caps the units per tile
+    assert lib.tobf_conv_prepare_split(small, 3, 128, 148, 2, None, None, C.byref(tot), C.byref(wsf),
+                                       C.byref(cnt)) == 0
+    assert max(d.ksplit for d in small) == 2

@@ -62,6 +62,46 @@ def test_conv_kernel_matches_oracle(ctx, case):
     assert _rel(got, ref) <= FP32_TOL
 
 
+def test_conv_split_k_deterministic(ctx):
+    """A few-tile, long-K group (stage-4 shape, K = 4608) runs split-K: the
+    partial tiles are summed in unit order by whichever unit finishes last, so
+    repeated runs are bit-identical, and the result is fp32-faithful."""
+    import ctypes as C
+    from paper_2107_09789_b200 import _native as N
+    from paper_2107_09789_b200.ir import Graph, Node, OperatorKind, TensorShape
+    b, c, h, j, k = 8, 512, 7, 512, 3
+    rng = np.random.default_rng(99)
+    x = rng.standard_normal((b, c, h, h)).astype(np.float32)
+    wt = (rng.standard_normal((k, k, c, j)) * np.sqrt(2.0 / (k * k * c))).astype(np.float32)
+    g = Graph({0: Node(0, OperatorKind.Conv2D, {"k1": k, "k2": k, "c": c, "j": j, "stride": 1, "padding": 1}, wt, [])},
+              0, TensorShape(b, c, h, h))
+    run = executor.PopulationRun(ctx, [executor.lower(g)], reps=1)
+    kind, dptr, n, tot, bn = run.launches[0]
+    host = run.desc_dev.cpu().numpy().tobytes()
+    d = N.ConvDesc.from_buffer_copy(host[dptr - run.desc_dev.data_ptr():][:C.sizeof(N.ConvDesc)])
+    assert kind == "conv" and d.ksplit > 1 and tot == d.mtiles * d.ntiles * d.ksplit
+    outs = [executor.execute(g, x) for _ in range(3)]
+    assert all(np.array_equal(o, outs[0]) for o in outs[1:])
+    ref = IR.conv2d(x, wt, 1, 1).astype(np.float64)
+    assert _rel(outs[0], ref) <= FP32_TOL
+    # two split problems in one launch (separate workspace regions / counters)
+    w5 = (rng.standard_normal((5, 5, c, j)) * np.sqrt(2.0 / (25 * c))).astype(np.float32)
+    nodes = {0: Node(0, OperatorKind.Conv2D, {"k1": 3, "k2": 3, "c": c, "j": j, "stride": 1, "padding": 1}, wt, []),
+             1: Node(1, OperatorKind.Conv2D, {"k1": 5, "k2": 5, "c": c, "j": j, "stride": 1, "padding": 2}, w5, []),
+             2: Node(2, OperatorKind.Concat, {}, None, [0, 1])}
+    g2 = Graph(nodes, 2, TensorShape(b, c, h, h))
+    run2 = executor.PopulationRun(ctx, [executor.lower(g2)], reps=1)
+    host = run2.desc_dev.cpu().numpy().tobytes()
+    base = run2.desc_dev.data_ptr()
+    convs = [L for L in run2.launches if L[0] == "conv"]
+    assert len(convs) == 1 and convs[0][2] == 2
+    ds = (N.ConvDesc * 2).from_buffer_copy(host[convs[0][1] - base:][:2 * C.sizeof(N.ConvDesc)])
+    assert ds[0].ksplit > 1 and ds[1].ksplit > 1 and ds[0].ws != ds[1].ws and ds[0].cnt != ds[1].cnt
+    got = executor.execute(g2, x)
+    ref2 = np.concatenate([ref, IR.conv2d(x, w5, 1, 2).astype(np.float64)], axis=1)
+    assert _rel(got, ref2) <= FP32_TOL
+
+
 # ----------------------------------------------------------------- executor
 @pytest.mark.parametrize("name,mode,size", [("c1c2", "dimension", 24), ("resnet18", "sequence", 64),
                                             ("resnet18", "dimension", 64), ("vgg16", "dimension", 32)])
@@ -276,9 +316,11 @@ def test_micro_batched_records_match_single_batch(ctx):
     pe = PopulationEvaluator(g, ev, trials=2, memo={})
     try:
         pooled = pe.evaluate_records(plans, micro=3, memo={}, workers=2)
+        ragged = pe.evaluate_records(plans, micro=(1, 4), memo={}, workers=2)
     finally:
         pe.close()
     assert pooled.tobytes() == one.tobytes()
+    assert ragged.tobytes() == one.tobytes()
     # and the trace totals follow the reference's process-global first-seen memo order
     memo = CM.ScheduleMemo()
     for i, p in enumerate(plans):
