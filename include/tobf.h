@@ -101,6 +101,15 @@ int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, in
                       int64_t su, int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg,
                       void* stream);
 
+/* As tobf_pack_weights for a knob-derived weight (widen / kernel-widen /
+ * branch, transforms.py:115-335) that is never materialised: element
+ * (u,v,c,n) = w[mu[u]*su + mv[v]*sv + mc[c]*sc + mn[n]*sn] * s_c[c] * s_n[n],
+ * 0 where any map entry is -1. `maps` (device) = [mu(k1) | mv(k2) | mc(c_real)
+ * | mn(j)] int32, `scales` (device) = [s_c(c_real) | s_n(j)] float32. */
+int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
+                             int64_t su, int64_t sv, int64_t sc, int64_t sn, const int32_t* maps,
+                             const float* scales, int32_t block_n, void* wimg, void* stream);
+
 /* Grouped 3xTF32 tcgen05 implicit-GEMM convolution over `n` problems whose
  * descriptors live in DEVICE memory (prepared with tobf_conv_prepare). */
 int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, void* stream);

@@ -92,6 +92,8 @@ SIGNATURES = {
                                           C.POINTER(_i64), C.POINTER(_i64)]),
     "tobf_wimg_bytes": (_i64, [_i32, _i32, _i32, _i32, _i32]),
     "tobf_pack_weights": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "tobf_pack_weights_gather": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32,
+                                           _vp, _vp]),
     "tobf_conv_grouped": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _vp]),
     "tobf_ew_prepare": (C.c_int, [_vp, C.c_int, C.POINTER(_i64)]),
     "tobf_ew_grouped": (C.c_int, [_vp, C.c_int, _i64, _vp]),

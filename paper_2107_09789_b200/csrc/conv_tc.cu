@@ -140,7 +140,7 @@ __device__ __forceinline__ float4 lds_tile(uint32_t epi_s, int row, int g, int b
 // Lanes own 4 consecutive channels; a warp covers 32/(BN/4) rows per step,
 // kEpiUnroll steps are issued before any is consumed (loads in flight),
 // row addresses are linear in the row index (no divisions).
-constexpr int kEpiUnroll = 4;
+constexpr int kEpiUnroll = 8;
 
 template <int BN>
 __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt, int ew, int lane) {
@@ -429,6 +429,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int g = 0;; ++g) {
       __syncwarp();  // every lane is done reading the slot about to be refilled
+#ifdef TOBF_CONV_DIAG_NOA
+      // diagnostic build: no A gather/split (wrong results; isolates the MMA/B/drain side)
+      if (ensure()) { ++ikb; ++issued; }
+      cp_async_commit();
+      if (g >= issued) break;
+      PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
+      mbar_arrive(&full_bar[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      continue;
+#endif
       PROF_WAIT(4, if (ensure()) issue());
       cp_async_commit();  // one group per block (empty past the end): group g holds block g
       if (g >= issued) break;
@@ -491,8 +501,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x104));
           uint8_t* dst = smem + stage * Cfg::kStageBytes;
+#ifdef TOBF_CONV_DIAG_NOB
+          (void)dst;  // diagnostic build: no B stream (wrong results)
+          mbar_arrive(&full_bar[stage]);
+#else
           mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
           bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
+#endif
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -601,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync 2, 128;" ::: "memory");
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + Cfg::kTmemMainCol + buf * BN;
+#ifndef TOBF_CONV_DIAG_NOD  // diagnostic build: no drain / epilogue (wrong results)
 #pragma unroll
         for (int cc = 0; cc < BN / 16; ++cc) {
           float part[16];
@@ -608,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
         }
+#endif
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
       }
@@ -645,8 +662,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long _e1 = clock64();
       _pacc[3] += _e1 - _e0;
 #endif
+#ifdef TOBF_CONV_DIAG_NOD
+      bool run_epi = false;
+      if (false) {
+#else
       bool run_epi = true;
       if (d.ksplit > 1) {
+#endif
         // ---- split-K: publish this unit's partial tile (coalesced rows), count
         // arrivals; the last unit of the tile sums all partials in unit order
         // (deterministic whichever unit arrives last) back into the staging
@@ -801,9 +823,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------ weight packing
 // Image layout: [ntiles][kblocks][hi|lo][BN rows][128 B swizzled], element
 // (k, n) of the GEMM B operand (k = (u*k2 + v)*Cp + c) in row n%BN, column k%32.
+// maps (optional, knob-derived weights, derived.py): [mu(k1) | mv(k2) | mc(c_real) | mn(j)]
+// source indices into the vanilla array (-1 = zero) and scales [sc(c_real) | sn(j)]:
+// element (u, v, c, n) = w[mu[u]*su + mv[v]*sv + mc[c]*sc + mn[n]*sn] * sc[c] * sn[n].
 __global__ void pack_weights_kernel(const float* __restrict__ w, int k1, int k2, int c_real, int Cp, int j,
                                     int64_t su, int64_t sv, int64_t sc, int64_t sn, int BN, int kblocks,
-                                    int ntiles, float* __restrict__ img) {
+                                    int ntiles, float* __restrict__ img, const int32_t* __restrict__ maps,
+                                    const float* __restrict__ scales) {
   const int64_t total = (int64_t)ntiles * kblocks * BN * 8;  // 16-B chunks of the hi plane
   const int K = k1 * k2 * Cp;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
@@ -825,7 +851,16 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int k1, int k2,
         const int c = k - uv * Cp;
         const int uu = uv / k2;
         const int vv = uv - uu * k2;
-        if (c < c_real) val = w[uu * su + vv * sv + c * sc + n * sn];
+        if (c < c_real) {
+          if (maps == nullptr) {
+            val = w[uu * su + vv * sv + c * sc + n * sn];
+          } else {
+            const int mu = __ldg(maps + uu), mv = __ldg(maps + k1 + vv);
+            const int mc = __ldg(maps + k1 + k2 + c), mn = __ldg(maps + k1 + k2 + c_real + n);
+            if ((mu | mv | mc | mn) >= 0)
+              val = w[mu * su + mv * sv + mc * sc + mn * sn] * __ldg(scales + c) * __ldg(scales + c_real + n);
+          }
+        }
       }
       hv[e] = __uint_as_float(to_tf32_rna(val));
       lv[e] = val - hv[e];
@@ -924,9 +959,27 @@ extern "C" int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j
   return ntiles * kblocks * 2 * block_n * kRowBytes;
 }
 
+static int pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j, int64_t su,
+                        int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg, const int32_t* maps,
+                        const float* scales, void* stream);
+
 extern "C" int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
                                  int64_t su, int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg,
                                  void* stream) {
+  return pack_weights(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, wimg, nullptr, nullptr, stream);
+}
+
+extern "C" int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp,
+                                        int32_t j, int64_t su, int64_t sv, int64_t sc, int64_t sn,
+                                        const int32_t* maps, const float* scales, int32_t block_n, void* wimg,
+                                        void* stream) {
+  if (!maps || !scales) return tobf_fail(TOBF_E_INVALID, "tobf_pack_weights_gather: null maps");
+  return pack_weights(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, wimg, maps, scales, stream);
+}
+
+static int pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j, int64_t su,
+                        int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg, const int32_t* maps,
+                        const float* scales, void* stream) {
   if (!w || !wimg || Cp % 4 || c_real > Cp || (block_n != 64 && block_n != 128)) {
     return tobf_fail(TOBF_E_INVALID, "tobf_pack_weights: bad arguments");
   }
@@ -937,7 +990,7 @@ extern "C" int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((chunks + threads - 1) / threads, 148 * 16);
   pack_weights_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-      w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, kblocks, ntiles, static_cast<float*>(wimg));
+      w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, kblocks, ntiles, static_cast<float*>(wimg), maps, scales);
   return tobf_cuda_check("tobf_pack_weights");
 }
 

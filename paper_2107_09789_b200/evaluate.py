@@ -63,7 +63,7 @@ def build_candidates(vanilla: Graph, plans: list[ObfuscationPlan], vanilla_analy
     out = []
     for p in plans:
         try:
-            g, d, ana = apply_plan_analyzed(vanilla, p, va)
+            g, d, ana = apply_plan_analyzed(vanilla, p, va, lazy=os.environ.get("TOBF_EAGER_KNOBS", "") != "1")
             out.append(Candidate(p, g, d, analysis=ana))
         except TransformError as exc:
             out.append(Candidate(p, None, None, str(exc)))

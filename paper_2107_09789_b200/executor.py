@@ -29,6 +29,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from .derived import DerivedWeight, consecutive_derived
 from .engine import Arena, DeviceContext, _root, device
 from .ir import BN_EPS, Graph, OperatorKind as K, ShapeMismatch, TensorShape, analyze, shape_map, topo_order
 
@@ -87,6 +88,8 @@ _CHAIN_KINDS = (K.BatchNorm, K.ReLU, K.Add)
 def _consecutive_views(ws: list, axis: int):
     """If the arrays are consecutive slices of one buffer along ``axis`` (same
     dtype / strides / other extents), return the merged view, else None."""
+    if any(isinstance(w, DerivedWeight) for w in ws):
+        return consecutive_derived(ws, axis)
     w0 = ws[0]
     if not all(isinstance(w, np.ndarray) and w.dtype == np.float32 and w.ndim == w0.ndim and
                w.strides == w0.strides for w in ws):
@@ -319,12 +322,16 @@ class ArrayRefs:
     def root(self, key) -> np.ndarray:
         return self._roots[key]
 
-    def ref(self, a: np.ndarray) -> tuple:
+    def ref(self, a) -> tuple:
+        if isinstance(a, DerivedWeight):  # knob-derived weight: its vanilla base + the gather
+            return ("D", self.ref(a.base)) + a.key()
         r = _root(a)
         off = a.__array_interface__["data"][0] - r.__array_interface__["data"][0]
         return (self.root_key(r), off, a.shape, a.strides)
 
-    def resolve(self, ref: tuple) -> np.ndarray:
+    def resolve(self, ref: tuple):
+        if ref[0] == "D":
+            return DerivedWeight(self.resolve(ref[1]), *ref[2:])
         key, off, shape, strides = ref
         r = self.root(key)
         if off == 0 and shape == r.shape and strides == r.strides:
@@ -545,7 +552,10 @@ class PopulationRun:
     def _wimg_ptr(self, entry: tuple) -> int:
         ctx, lib = self.ctx, self.ctx.lib
         ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn = entry
-        wptr, st = ctx.cached_view(self.refs.resolve(ref))
+        w = self.refs.resolve(ref)
+        if isinstance(w, DerivedWeight):
+            return self._derived_wimg_ptr(w, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn)
+        wptr, st = ctx.cached_view(w)
         if is_conv:
             su, sv, sc, sn = st
         else:
@@ -562,6 +572,38 @@ class PopulationRun:
                                         C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
         ctx.launches += 1
         cache[key] = img
+        return img.data_ptr()
+
+    def _derived_wimg_ptr(self, w: DerivedWeight, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn) -> int:
+        """Weight image of a knob-derived weight, packed on the device straight
+        from the resident vanilla array through the gather maps (derived.py);
+        only the maps (a few KB) cross PCIe."""
+        ctx, lib = self.ctx, self.ctx.lib
+        wptr, st = ctx.cached_view(w.base)
+        if is_conv:
+            su, sv, sc, sn = st
+        else:
+            r, cstride = st
+            H, W = w.hw
+            su, sv, sc, sn = W * r, r, H * W * r, cstride
+        key = ("D", wptr, su, sv, sc, sn, w.key(), k1, k2, in_c, cp, j, bn)
+        cache = ctx.__dict__.setdefault("wimg_cache", {})
+        hit = cache.get(key)
+        if hit is not None:
+            return hit[0].data_ptr()
+        mu, mv, mc, mn, s_c, s_n = w.maps()
+        if (len(mu), len(mv), len(mc), len(mn)) != (k1, k2, in_c, j):
+            raise ShapeMismatch(-1, f"derived weight maps {(len(mu), len(mv), len(mc), len(mn))} "
+                                    f"!= conv geometry {(k1, k2, in_c, j)}")
+        maps = ctx.upload_array(np.concatenate([mu, mv, mc, mn]).astype(np.int32))
+        scales = ctx.upload_array(np.concatenate([s_c, s_n]).astype(np.float32))
+        nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
+        img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
+        ctx.check(lib.tobf_pack_weights_gather(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn,
+                                               C.c_void_p(maps.data_ptr()), C.c_void_p(scales.data_ptr()), bn,
+                                               C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack derived weights")
+        ctx.launches += 1
+        cache[key] = (img, maps, scales)  # maps stay alive until the (async) pack has run
         return img.data_ptr()
 
     def _affine_ptrs(self, refs_needed: list) -> dict:

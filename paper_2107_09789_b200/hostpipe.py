@@ -117,11 +117,16 @@ def _worker_init(vanilla: Graph, reps: int, pname: str) -> None:
                    if isinstance(n.weights, np.ndarray)}
 
 
+# knob weights as device-packed gathers (derived.py); TOBF_EAGER_KNOBS=1 ships
+# materialised arrays instead (A/B measurements only)
+LAZY_KNOBS = os.environ.get("TOBF_EAGER_KNOBS", "") != "1"
+
+
 def encode_candidate(cand: int, plan: ObfuscationPlan, vanilla: Graph, vanilla_analysis, reps: int, pname: str,
                      roots: dict):
     """(cand, error, payload): payload = (ForwardPlan, CandidateTrace, new arrays)."""
     try:
-        g, d, ana = apply_plan_analyzed(vanilla, plan, vanilla_analysis)
+        g, d, ana = apply_plan_analyzed(vanilla, plan, vanilla_analysis, lazy=LAZY_KNOBS)
     except TransformError as exc:
         return cand, str(exc), None
     refs = WorkerRefs(roots, cand)

@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .derived import DerivedWeight
 from .ir import (COMPLEX_KINDS, Graph, Node, OperatorKind, TensorShape, analyze, shape_map, topo_order)
 
 BRANCH_MODES = ("none", "in2", "in4", "out2", "out4")            # transforms.py:19
@@ -60,8 +61,12 @@ def _round_half_up(x: float) -> int:
 class _Work:
     """Mutable view used by the knobs. ``nodes`` are private copies."""
 
-    def __init__(self, graph: Graph, own: bool = False, analysis=None):
+    def __init__(self, graph: Graph, own: bool = False, analysis=None, lazy: bool = False):
         self.g = graph if own else graph.copy()
+        # lazy: Conv2D / Linear weights the knobs change become DerivedWeights
+        # (derived.py: per-axis gathers of the vanilla array, packed on the
+        # device) instead of materialised numpy arrays
+        self.lazy = lazy
         if analysis is not None:  # reuse the input graph's structure (copied: we mutate)
             self.succ = {k: list(v) for k, v in analysis.succ.items()}
             self._shapes: dict[int, TensorShape] | None = dict(analysis.shapes)
@@ -135,6 +140,17 @@ class _Work:
         self._shapes = None
 
 
+def _derived(w: _Work, node: Node) -> DerivedWeight:
+    """The node's weight as a DerivedWeight (lazy mode): a Linear's rows are
+    factored (c, H, W) by the activation that feeds it."""
+    if isinstance(node.weights, DerivedWeight):
+        return node.weights
+    if node.kind is OperatorKind.Conv2D:
+        return DerivedWeight.of(node.weights, "conv")
+    fed = w.shapes()[node.inputs[0]] if node.inputs else w.g.input_shape
+    return DerivedWeight.of(node.weights, "linear", (fed.height, fed.width))
+
+
 # ---------------------------------------------------------------------------
 # Layer widening (transforms.py:82-165)
 # ---------------------------------------------------------------------------
@@ -187,7 +203,10 @@ def _widen(w: _Work, layer_id: int, factor: float) -> None:
 
     # producer: duplicates of the first `extra` output channels go at the end
     wt = layer.weights
-    layer.weights = np.concatenate([wt, wt[..., :extra]], axis=-1)
+    if w.lazy:
+        layer.weights = _derived(w, layer).dup_tail(3, extra)
+    else:
+        layer.weights = np.concatenate([wt, wt[..., :extra]], axis=-1)
     layer.attrs["j"] = j_new
     for nid in path[:-1]:
         node = w.g.nodes[nid]
@@ -196,7 +215,11 @@ def _widen(w: _Work, layer_id: int, factor: float) -> None:
 
     consumer = w.g.nodes[path[-1]]
     cw = consumer.weights
-    if consumer.kind is OperatorKind.Conv2D:
+    if w.lazy:
+        consumer.weights = _derived(w, consumer).dup_tail(2, extra, 0.5)
+        consumer.attrs["c"] = j_new if consumer.kind is OperatorKind.Conv2D else \
+            j_new * consumer.weights.hw[0] * consumer.weights.hw[1]
+    elif consumer.kind is OperatorKind.Conv2D:
         half = cw.copy()
         half[:, :, :extra, :] *= 0.5
         consumer.weights = np.concatenate([half, half[:, :, :extra, :]], axis=2)
@@ -246,8 +269,9 @@ def _branch(w: _Work, layer_id: int, mode: str, parts: int) -> list[int]:
         step = j // parts
         part_ids = []
         for i in range(parts):
-            new_nodes.append(Node(nid, layer.kind, dict(layer.attrs, j=step),
-                                  layer.weights[..., i * step:(i + 1) * step], list(layer.inputs)))
+            wt = layer.weights.slice(3, i * step, (i + 1) * step) if isinstance(layer.weights, DerivedWeight) \
+                else layer.weights[..., i * step:(i + 1) * step]
+            new_nodes.append(Node(nid, layer.kind, dict(layer.attrs, j=step), wt, list(layer.inputs)))
             part_ids.append(nid)
             nid += 1
         combiner = Node(nid, OperatorKind.Concat, {"axis": 1}, None, part_ids)
@@ -266,7 +290,10 @@ def _branch(w: _Work, layer_id: int, mode: str, parts: int) -> list[int]:
                       None, list(layer.inputs))
             new_nodes.append(sl)
             nid += 1
-            if is_conv:
+            if isinstance(layer.weights, DerivedWeight):  # channel slice of the derived gather
+                wt = layer.weights.slice(2, i * step, (i + 1) * step)
+                attrs = dict(layer.attrs, c=step * hw)
+            elif is_conv:
                 wt = layer.weights[:, :, i * step:(i + 1) * step, :]
                 attrs = dict(layer.attrs, c=step)
             else:
@@ -435,7 +462,10 @@ def _kernel_widen(w: _Work, layer_id: int, steps: int) -> None:
         raise TransformError(f"cannot kernel-widen {node.kind.value}")
     if steps <= 0:
         return
-    node.weights = np.pad(node.weights, ((steps, steps), (steps, steps), (0, 0), (0, 0)))
+    if w.lazy:
+        node.weights = _derived(w, node).pad_kernel(steps)
+    else:
+        node.weights = np.pad(node.weights, ((steps, steps), (steps, steps), (0, 0), (0, 0)))
     node.attrs = dict(node.attrs, k1=node.attrs["k1"] + 2 * steps, k2=node.attrs["k2"] + 2 * steps,
                       padding=node.attrs["padding"] + steps)
 
@@ -516,10 +546,12 @@ def apply_plan(graph: Graph, plan: ObfuscationPlan) -> tuple[Graph, BackendDirec
     return out, directives
 
 
-def apply_plan_analyzed(graph: Graph, plan: ObfuscationPlan, vanilla_analysis=None):
+def apply_plan_analyzed(graph: Graph, plan: ObfuscationPlan, vanilla_analysis=None, lazy: bool = False):
     """``apply_plan`` that also returns the obfuscated graph's structural
     analysis (order / successors / shapes), reusing the knobs' incremental
-    successor index and shape table instead of recomputing them."""
+    successor index and shape table instead of recomputing them. ``lazy``:
+    changed Conv2D / Linear weights are DerivedWeights (never materialised on
+    the host; ``np.asarray`` gives the eager arrays bit for bit)."""
     if vanilla_analysis is not None:
         vanilla = [nid for nid in vanilla_analysis.order if graph.nodes[nid].kind in COMPLEX_KINDS]
     else:
@@ -532,7 +564,7 @@ def apply_plan_analyzed(graph: Graph, plan: ObfuscationPlan, vanilla_analysis=No
     # Fast exit: an all-identity plan returns the input graph object.
     touched = any(e.widen_factor != 1.0 or e.kernel_widen or e.branching != "none" or e.deepen or e.skip
                   or e.dummy_count for e in entries)
-    w = _Work(graph, analysis=vanilla_analysis) if touched else None
+    w = _Work(graph, analysis=vanilla_analysis, lazy=lazy) if touched else None
     failures: list[tuple[int, str, str]] = []
     anchor = {lid: lid for lid in vanilla}
     carriers = {lid: [lid] for lid in vanilla}

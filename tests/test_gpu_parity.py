@@ -129,6 +129,28 @@ def test_execute_obfuscated_matches_oracle(ctx, name, mode, size):
             assert err_gpu <= max(FP32_TOL, 2.0 * err_ref), (err_gpu, err_ref)
 
 
+@pytest.mark.parametrize("name,kw", [("vgg16", {"size": 32, "hidden": 256}), ("resnet18", {"size": 64}),
+                                     ("c1c2", {"size": 24})])
+def test_derived_weights_pack_like_eager(ctx, name, kw):
+    """Dimension-mode candidates built lazily (knob weights as gathers of the
+    resident vanilla arrays, packed on the device by tobf_pack_weights_gather)
+    run bit-identically to the eagerly materialised graphs."""
+    from paper_2107_09789_b200.derived import DerivedWeight
+    from paper_2107_09789_b200.ir import analyze
+    g = fixtures.FIXTURES[name](**kw)
+    va = analyze(g)
+    x = np.random.default_rng(8).standard_normal(g.input_shape.as_tuple()).astype(np.float32)
+    n_derived = 0
+    for plan in _plans(g, "dimension", 3, seed=17):
+        eager, _ = knobs.apply_plan(g, plan)
+        lazy, _, _ = knobs.apply_plan_analyzed(g, plan, va, lazy=True)
+        n_derived += sum(isinstance(n.weights, DerivedWeight) for n in lazy.nodes.values())
+        a = executor.execute(eager, x)
+        b = executor.execute(lazy, x)
+        assert a.tobytes() == b.tobytes()
+    assert n_derived > 0
+
+
 def test_equivalence_verdicts_match_oracle(ctx):
     g = fixtures.c1c2(size=24)
     plans = _plans(g, "dimension", 3, seed=3)
