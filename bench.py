@@ -59,6 +59,7 @@ def parse():
                     help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run)")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
+    ap.add_argument("--cfg4-pop", type=int, default=16, help="cfg4 (VGG-16 dimension) candidates per step; 0 = skip")
     return ap.parse_args()
 
 
@@ -254,6 +255,62 @@ def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
     return out
 
 
+# ----------------------------------------------------------------------------- cfg4
+def workload_cfg4(args) -> dict:
+    """SURVEY cfg4: VGG-16 224x224 b1, dimension-mode candidates (widen, kernel
+    widen, dummy; widened weights synthesised on the device from the resident
+    vanilla arrays), 8 trials, full path (forward + verdict + trace + fitness).
+    Device-resident candidates/s and end-to-end candidates/s (public API,
+    cold caches, host apply_plan in worker processes), like the headline."""
+    import torch
+    from paper_2107_09789_b200 import fixtures, ga
+    from paper_2107_09789_b200.engine import device
+    from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
+    ctx = device()
+    P, steps, warm = args.cfg4_pop, 3, 2
+    g = fixtures.vgg16()
+    space = ga.search_space(g, "dimension")
+    sizes = ga.domain_sizes("dimension", space)
+    rng = np.random.default_rng(args.seed)
+    plans = [ga.decode_genome(g, "dimension", space, x) for x in ga.random_genomes(rng, sizes, P * (steps + warm + 1))]
+    pe = PopulationEvaluator(g, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed, memo={})
+    prep = pe.prepare(plans[:P], memo={})
+    x = pe.x_host.to(ctx.device)
+    for _ in range(warm):
+        pe.run(prep, x_dev=x, cold_schedules=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pe.run(prep, x_dev=x, cold_schedules=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    flops = prep["run"].gemm_flops()
+    del prep
+    for s in range(warm):
+        ctx.clear_cache()
+        pe.evaluate_records(plans[P * (1 + s):P * (2 + s)], memo={})
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for s in range(steps):
+        ctx.clear_cache()
+        pe.evaluate_records(plans[P * (1 + warm + s):P * (2 + warm + s)], memo={})
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / steps
+    pe.close()
+    ctx.clear_cache()
+    return {"workload": "vgg16_dimension_generation (SURVEY cfg4)", "candidates_per_step": P, "trials": args.trials,
+            "value": P / (ms / 1e3), "unit": UNIT, "ms_per_step": round(ms, 2),
+            "conv_alg_tflops": round(flops / (ms / 1e3) / 1e12, 1), "flops_per_step": flops,
+            "e2e": {"value": P / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": round(e2e_ms, 1),
+                    "host_ms_per_step": {k: round(v, 1) for k, v in pe.last_host_ms.items()}},
+            "note": "knob weights synthesised on the device (tobf_pack_weights_gather); no CPU baseline "
+                    "(the numpy port needs ~30 s per VGG-16 candidate per core)"}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main_ours(args):
     import torch
@@ -407,6 +464,9 @@ def main_ours(args):
     sweeps = None
     if rank == 0 and not args.no_sweeps:
         sweeps = kernel_sweeps(args, vanilla, pe.ev.predictors, peaks.get("hbm_gbs", 6546.9))
+    cfg4 = None
+    if rank == 0 and world == 1 and args.cfg4_pop > 0:
+        cfg4 = workload_cfg4(args)
 
     if rank == 0:
         bf16 = peaks.get("bf16_tflops_sustained", 1387.4)
@@ -440,7 +500,7 @@ def main_ours(args):
                            "schedule_memo": "cold every step", "l2": "inputs > L2 (weights+activations ~6 GB/step)",
                            "parallelism": f"population sharded over {world} GPU(s), NCCL all-gather of records"},
                 "gpu_launches": launches, "stages_ms": stages, "roofline": roofline, "clocks": clk,
-                "e2e": e2e, "cpu_baseline": cpu, "kernels": sweeps}
+                "e2e": e2e, "cpu_baseline": cpu, "kernels": sweeps, "workloads": {"cfg4": cfg4}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
