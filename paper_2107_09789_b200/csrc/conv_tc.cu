@@ -59,7 +59,10 @@ struct ConvCfg {
 // short chains on the main term, the 2^-11-smaller correction terms in their
 // own accumulator, and round-to-nearest fp32 adds keep the conv
 // fp32-faithful (error at OpenBLAS-sgemm level).
-constexpr int kChunkKB = 4;
+#ifndef TOBF_CONV_CHUNK_KB
+#define TOBF_CONV_CHUNK_KB 4
+#endif
+constexpr int kChunkKB = TOBF_CONV_CHUNK_KB;
 
 // Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ... of the
 // group (problems sorted by K descending, so long tiles go first). Every role
