@@ -45,7 +45,7 @@ UNIT = "candidates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--pop", type=int, default=32, help="candidates per GPU per step")
@@ -73,49 +73,53 @@ def population_plans(vanilla, total: int, seed: int):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while active."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 5 ms from a thread (nvidia-smi -lms cannot
+    resolve a ~100 ms region), nvidia-smi as the fallback."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []
-        self.proc = None
+        self.samples = []   # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop_flag = threading.Event()
+        self.nvml = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nvml = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._poll, daemon=True)
         self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, self.max_mhz, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_flag.set()
+        self.thread.join(timeout=1)
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({n for s in self.samples for n, bit in self.REASONS if s[2] & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
+                "source": "NVML, 5 ms polling inside the timed region"}
 
 
 # ----------------------------------------------------------------------------- cpu (oracle port)
@@ -364,8 +368,6 @@ def main_ours(args):
     torch.cuda.synchronize()
     barrier()
     clocks = ClockSampler(ctx.index)
-    clocks.start()
-    time.sleep(0.3)
     launches0 = ctx.launches
     run = prep["run"]
     run.conv_events = []
@@ -373,13 +375,14 @@ def main_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
+    clocks.start()
     e0.record()
     for _ in range(args.steps):
         gather(pe.run(prep, x_dev=x_dev, cold_schedules=True))
     e1.record()
     torch.cuda.synchronize()
-    barrier()
     clk = clocks.stop()
+    barrier()
     launches = (ctx.launches - launches0) // args.steps
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     conv_events = run.conv_events

@@ -78,9 +78,9 @@ typedef struct tobf_conv_desc {
  * (no split-K: ksplit = 1). */
 int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles);
 
-/* As tobf_conv_prepare, and split the K loop of long tiles when the group
- * has too few tiles to balance `sms` SMs (work units of >= 16 K blocks,
- * <= max_split units per tile). `tile_start` then counts work units. `ws` /
+/* As tobf_conv_prepare, and, in groups with fewer than 2 tiles per SM, split
+ * the K loop of tiles longer than ~1/4 of one SM's share of the group's work
+ * (work units of >= 16 K blocks, <= max_split units per tile). `tile_start` then counts work units. `ws` /
  * `cnt` of split problems are set to ws_base / cnt_base plus their offsets
  * (NULL bases: the byte offsets themselves, for the caller to rebase);
  * *ws_floats and *cnt_count return the workspace (floats) and counter

@@ -284,11 +284,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* small_empty = acc_empty + 2;     // [2] drain -> MMA (tile-slot correction accumulator)
   uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
   uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + kInfoSlots);
+  uint64_t* a_took = info_empty + kInfoSlots;     // A producer took tile k's descriptor (phase k)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_took + 1);
   volatile int* info_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kInfoSlots], -1 = no more tiles
   volatile int* split_last = info_tile + kInfoSlots;  // drain: this unit completes its split-K tile
   int* sched = g_conv_sched[BN >= 128 ? 1 : 0];
 
+#ifdef TOBF_CONV_PROF
+  const unsigned long long _cta_t0 = globaltimer_ns();
+  if (threadIdx.x == 0) {
+    atomicMax(&g_conv_prof[28], _cta_t0);
+    atomicMax(&g_conv_prof[29], ~_cta_t0);
+  }
+#endif
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -306,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&info_full[s], 1);
       mbar_init(&info_empty[s], kInfoConsumers);
     }
+    mbar_init(a_took, 4);
     fence_mbar_init();
   }
   if (warp == 4) tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -386,7 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           v = tap - u * k2;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
+        if (lane == 0) {
+          mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
+          mbar_arrive(a_took);              // the scheduler may claim the next tile
+        }
         ikb = 0;
         ++iit;
       }
@@ -450,22 +462,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 row[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      // split hi/lo BEFORE waiting for the free TMEM stage: after the MMAs
+      // release it only the four tcgen05.st are left on the critical path
+      float hh[2][16], ll[2][16];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a = row[half * 4 + q];
+          hh[half][4 * q + 0] = tf32_rna_finite(a.x); ll[half][4 * q + 0] = a.x - hh[half][4 * q + 0];
+          hh[half][4 * q + 1] = tf32_rna_finite(a.y); ll[half][4 * q + 1] = a.y - hh[half][4 * q + 1];
+          hh[half][4 * q + 2] = tf32_rna_finite(a.z); ll[half][4 * q + 2] = a.z - hh[half][4 * q + 2];
+          hh[half][4 * q + 3] = tf32_rna_finite(a.w); ll[half][4 * q + 3] = a.w - hh[half][4 * q + 3];
+        }
+      }
       PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
       tc_fence_after();
       const uint32_t ta = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + Cfg::kTmemACol + stage * 64;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        float hh[16], ll[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 a = row[half * 4 + q];
-          hh[4 * q + 0] = tf32_rna_finite(a.x); ll[4 * q + 0] = a.x - hh[4 * q + 0];
-          hh[4 * q + 1] = tf32_rna_finite(a.y); ll[4 * q + 1] = a.y - hh[4 * q + 1];
-          hh[4 * q + 2] = tf32_rna_finite(a.z); ll[4 * q + 2] = a.z - hh[4 * q + 2];
-          hh[4 * q + 3] = tf32_rna_finite(a.w); ll[4 * q + 3] = a.w - hh[4 * q + 3];
-        }
-        tmem_st16(ta + half * 16, hh);
-        tmem_st16(ta + 32 + half * 16, ll);
+        tmem_st16(ta + half * 16, hh[half]);
+        tmem_st16(ta + 32 + half * 16, ll[half]);
       }
       PROF_WAIT(3, tmem_wait_st());
       tc_fence_before();
@@ -663,6 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
 #ifdef TOBF_CONV_PROF
       const long long _e1 = clock64();
+      long long _e2 = _e1;
       _pacc[3] += _e1 - _e0;
 #endif
 #ifdef TOBF_CONV_DIAG_NOD
@@ -751,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #ifdef TOBF_CONV_PROF
-      const long long _e2 = clock64();
+      _e2 = clock64();
       _pacc[4] += _e2 - _e1;
 #endif
       // Simple chains (<= 1 folded BN, <= 2 tensor operands, no dummy
@@ -788,6 +806,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0;; ++it) {
       const int islot = it % kInfoSlots;
       mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
+      // claim lazily: only once the A producer has taken tile it-1, so a CTA
+      // holds at most one claimed-but-unstarted tile and the launch's tail
+      // stays balanced (the info ring would otherwise let it claim 3 ahead)
+      if (it > 0) mbar_wait_backoff(a_took, (it - 1) & 1, 0x118);
       int tile = 0;
       if (lane == 0) tile = it == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&sched[0], 1);
       tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -812,6 +834,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
+#ifdef TOBF_CONV_PROF
+  if (threadIdx.x == 0) {
+    const unsigned long long _cta_t1 = globaltimer_ns();
+    atomicMax(&g_conv_prof[30], _cta_t1);
+    atomicAdd(&g_conv_prof[26], _cta_t1 - _cta_t0);
+  }
+#endif
   if (threadIdx.x == 0) {
     // every claim of this CTA happened before the barrier above; the last CTA
     // out resets the counters for the next launch
@@ -908,10 +937,15 @@ extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int6
   return TOBF_OK;
 }
 
+#ifndef TOBF_SPLIT_TILES_PER_SM
+#define TOBF_SPLIT_TILES_PER_SM 2
+#endif
 // Split policy: a group with fewer than 2 tiles per SM leaves SMs idle behind
-// its longest tiles; cut K into work units of U >= 16 K blocks, U chosen so
-// the group has ~4 units per SM (the partial write + read of a 128 x BN fp32
-// tile costs about as much as 3-4 K blocks of MMAs, hence the floor).
+// its longest tiles; cut the K loop of tiles clearly longer than ~1/4 of an
+// SM's share of the group's work into units of U >= 16 K blocks (the partial
+// write + read of a 128 x BN fp32 tile costs about as much as 3-4 K blocks of
+// MMAs, hence the floor). Measured: splitting also in groups of 2-8 tiles per
+// SM cost more in partial traffic than it won in balance (10.8 vs 10.6 ms).
 extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split,
                                        float* ws_base, int32_t* cnt_base, int64_t* total_units,
                                        int64_t* ws_floats, int64_t* cnt_count) {
@@ -924,15 +958,21 @@ extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n
   *cnt_count = 0;
   int64_t work = 0;
   for (int i = 0; i < n; ++i) work += (int64_t)descs[i].mtiles * descs[i].ntiles * descs[i].kblocks;
-  if (tiles >= 2 * (int64_t)sms || max_split == 1) {
+  // unit size: ~1/4 of one SM's share of the group's work (>= 16 K blocks), so
+  // no single unit is long enough to leave the other SMs idle at the tail of
+  // the greedy (longest-first) claim order; shorter tiles stay whole
+  const int64_t per_unit = std::max<int64_t>(16, (work + 4 * (int64_t)sms - 1) / (4 * (int64_t)sms));
+  const int64_t threshold = per_unit * 3 / 2;  // only clearly-too-long tiles are cut
+  int64_t longest = 0;
+  for (int i = 0; i < n; ++i) longest = std::max<int64_t>(longest, descs[i].kblocks);
+  if (tiles >= TOBF_SPLIT_TILES_PER_SM * (int64_t)sms || longest <= threshold || max_split == 1) {
     *total_units = tiles;
     return TOBF_OK;
   }
-  const int64_t per_unit = std::max<int64_t>(16, (work + 4 * (int64_t)sms - 1) / (4 * (int64_t)sms));
   int64_t acc = 0, wsf = 0, cnts = 0;
   for (int i = 0; i < n; ++i) {
     tobf_conv_desc& d = descs[i];
-    int s = (int)std::min<int64_t>(max_split, (d.kblocks + per_unit - 1) / per_unit);
+    int s = d.kblocks > threshold ? (int)std::min<int64_t>(max_split, (d.kblocks + per_unit - 1) / per_unit) : 1;
     s = std::max(s, 1);
     const int kper = (d.kblocks + s - 1) / s;
     s = (d.kblocks + kper - 1) / kper;  // no empty unit

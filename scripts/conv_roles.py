@@ -49,7 +49,12 @@ def main():
         ctas = min(tot, 148)
         per = {NAMES[k]: buf[k] / ctas / 1e3 for k in NAMES}  # kcycles per CTA
         tot_m = per["M.total"]
-        print(f"launch {idx}: {ms:.3f} ms probs {n} tiles {tot} BN {bn}  (kcycles/CTA)  " +
+        t_first = (~int(buf[29])) & ((1 << 64) - 1)
+        span = (int(buf[30]) - t_first) / 1e3
+        start_skew = (int(buf[28]) - t_first) / 1e3
+        life = int(buf[26]) / ctas / 1e3
+        print(f"launch {idx}: {ms:.3f} ms probs {n} tiles {tot} BN {bn}  CTA span {span:.1f} us, start skew "
+              f"{start_skew:.1f} us, mean CTA life {life:.1f} us  (kcycles/CTA)  " +
               "  ".join(f"{k}={v:.1f}" for k, v in per.items()))
 
 
