@@ -146,6 +146,12 @@ __global__ void lstm_ctc_kernel(const double* __restrict__ feats, const int32_t*
 // accumulation order (bias, x[0..F), h[0..H)) and every rounding are the
 // same as the single-CTA formulation and the CPU oracle.
 constexpr int kLstmUnits = 32;
+#ifndef TOBF_LSTM_TPC_SMALL
+#define TOBF_LSTM_TPC_SMALL 16
+#endif
+#ifndef TOBF_LSTM_SMALL_B
+#define TOBF_LSTM_SMALL_B 64
+#endif
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -503,10 +509,10 @@ static int launch_lstm(const double* feats, const int32_t* offsets, int32_t B, i
   return tobf_cuda_check("tobf_lstm_ctc");
 }
 
+template <int TPC>
 static int launch_lstm_cluster(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H,
                                int32_t NC, const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
                                const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, cudaStream_t st) {
-  constexpr int TPC = 8;
   const int L = F + H, Lq = L / 4, Lp = (L + 3) & ~3, CS = H / kLstmUnits;
   const size_t smem = (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2 +
                       sizeof(float) * (2 * TPC * Lp + 4 * kLstmUnits + NC * H);
@@ -540,8 +546,16 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
       NC < 2 || NC > kMaxNC || H < 32 || H > 1024 || H % 32 || T_max < 1)
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16)
-    return launch_lstm_cluster(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16) {
+    // Small batches (one GA generation: the recurrence is latency-bound and
+    // runs concurrently with the forward) pack 16 traces per cluster (the h double buffer of 16 traces plus the
+    // bf16 gate rows fill the 227 KB of shared memory at H=512) so
+    // the attacker occupies few SMs; large sweeps keep 8 per cluster.
+    if (B <= TOBF_LSTM_SMALL_B)
+      return launch_lstm_cluster<TOBF_LSTM_TPC_SMALL>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out,
+                                                      tokens, T_max, ntok, st);
+    return launch_lstm_cluster<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+  }
   if (B >= 148 * 8) return launch_lstm<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   return launch_lstm<2>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
 }

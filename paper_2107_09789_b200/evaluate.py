@@ -188,12 +188,11 @@ class PopulationEvaluator:
         mark = (lambda k: ev.setdefault(k, torch.cuda.Event(enable_timing=True)).record()) if timing else \
             (lambda k: None)
         mark("start")
-        if x_dev is None:
-            x_dev = self.x_host.to(ctx.device, non_blocking=True)
-        run.set_input(x_dev)
-        run.run()
-        ok_f, worst_f = compare_outputs(ctx, run, 0, list(range(1, len(feas) + 1)), self.tol)
-        mark("forward")
+        # The trace features and the attacker's fitness stage do not depend on
+        # the forward: trace first, then the three bagged predictors (LSTM +
+        # CTC + LER, GPU-latency-bound recurrences) on side streams running
+        # concurrently with the forward + verdict on the main stream; joined
+        # before Eq. 10, which needs both.
         if tp is not None:
             run_trace(tp, restore=cold_schedules)
         mark("trace")
@@ -204,31 +203,36 @@ class PopulationEvaluator:
         ok = torch.zeros(n, dtype=torch.int32, device=ctx.device)
         worst = torch.zeros(n, dtype=torch.float32, device=ctx.device)
         ntok0 = torch.zeros(n, dtype=torch.int32, device=ctx.device)
+        main = ctx.stream
+        joins = []
         if ncf:
             idx = prep["idx"]
             if not hasattr(self, "_truth_dev"):
                 self._truth_dev = ctx.upload_array(self.truth)
-            # the bagged predictors are independent: predictor p > 0 runs on
-            # side stream p-1 (a GPU-latency-bound recurrence each; together
-            # they fill the SMs one alone leaves idle), joined before Eq. 10
-            main = ctx.stream
-            side = ctx.side_streams(len(self.ev.predictors) - 1)
+            side = ctx.side_streams(len(self.ev.predictors))
             fork = torch.cuda.Event()
             fork.record(main)
             for p, pred in enumerate(self.ev.predictors):
-                s = main if p == 0 else side[p - 1]
+                s = side[p]
                 with torch.cuda.stream(s):
-                    if p:
-                        s.wait_event(fork)
+                    s.wait_event(fork)
                     toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred, s.cuda_stream)
                     _, lr, _ = edit_distances(toks, ntok, self._truth_dev, s.cuda_stream)
                     lers[p].index_copy_(0, idx, lr)
                     if p == 0:
                         ntok0.index_copy_(0, idx, ntok)
-                if p:
-                    join = torch.cuda.Event()
-                    join.record(s)
-                    main.wait_event(join)
+                join = torch.cuda.Event()
+                join.record(s)
+                joins.append(join)
+        if x_dev is None:
+            x_dev = self.x_host.to(ctx.device, non_blocking=True)
+        run.set_input(x_dev)
+        run.run()
+        ok_f, worst_f = compare_outputs(ctx, run, 0, list(range(1, len(feas) + 1)), self.tol)
+        mark("forward")
+        for join in joins:
+            main.wait_event(join)
+        if ncf:
             T.index_copy_(0, idx, tp.totals)
             ok.index_copy_(0, idx, ok_f)
             worst.index_copy_(0, idx, worst_f)

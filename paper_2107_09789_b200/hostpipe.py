@@ -235,7 +235,11 @@ def default_workers() -> int:
     env = os.environ.get("TOBF_HOST_WORKERS")
     if env:
         return max(1, int(env))
-    return max(1, min(16, (os.cpu_count() or 2) - 2))
+    # one GPU process per rank shares the host: split the cores the parents
+    # leave free between the node's ranks (torchrun's LOCAL_WORLD_SIZE)
+    ranks = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 2)
+    return max(1, min(16, (cores - ranks - 1) // ranks))
 
 
 __all__ = ["ForwardPlan", "CandidateTrace", "WorkerRefs", "ParentRefs", "HostPool", "encode_candidate",
