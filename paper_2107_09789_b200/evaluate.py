@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import device
+from .engine import cat_records, device
 from .executor import PopulationRun, compare_outputs, lower, plan_forward, trial_inputs
 from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, analyze, label_sequence
@@ -304,7 +304,7 @@ class PopulationEvaluator:
             if prep["trace"] is not None:
                 finish_trace(prep["trace"])
         self.last_host_ms = {k: sum(p["host_ms"].get(k, 0.0) for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
-        return np.concatenate(recs)
+        return cat_records(recs, RECORD_DTYPE)
 
     def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
         prep = self.prepare(plans)

@@ -30,7 +30,7 @@ import torch
 
 from . import _native as N
 from .derived import DerivedWeight, consecutive_derived
-from .engine import Arena, DeviceContext, _root, device
+from .engine import Arena, DeviceContext, _root, cat_records, device
 from .ir import BN_EPS, Graph, OperatorKind as K, ShapeMismatch, TensorShape, analyze, shape_map, topo_order
 
 
@@ -697,8 +697,8 @@ class PopulationRun:
                     ptrs.append(v)
             tabs[sp] = (np.array(ptrs + [0], np.uint64), offsets)
         # rows of all plans, linked, grouped into launches
-        conv = np.concatenate([p.conv for p in plans]) if plans else np.zeros(0, CONV_DTYPE)
-        ew = np.concatenate([p.ew for p in plans]) if plans else np.zeros(0, EW_DTYPE)
+        conv = cat_records([p.conv for p in plans], CONV_DTYPE)
+        ew = cat_records([p.ew for p in plans], EW_DTYPE)
         conv_plan = np.concatenate([np.full(len(p.conv), i, np.int64) for i, p in enumerate(plans)])
         ew_plan = np.concatenate([np.full(len(p.ew), i, np.int64) for i, p in enumerate(plans)])
         for arr, rp in ((conv, conv_plan), (ew, ew_plan)):

@@ -18,6 +18,7 @@ for every not-yet-memoised signature of a whole population (first-seen order
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 from dataclasses import dataclass
 from enum import Enum
 
@@ -25,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .engine import device
+from .engine import cat_records, device
 from .ir import COMPLEX_KINDS, Graph, OperatorKind as K, TensorShape, analyze, infer_shapes, shape_map, topo_order
 from .kernels import DEFAULT_UNROLL, TRIVIAL_SCHEDULE, Kernel, Schedule, fuse, modify_schedule
 
@@ -295,6 +296,14 @@ class CandidateTrace:
 
     recs: np.ndarray
     sigs: list
+    sig_keys: np.ndarray | None = None  # 64-bit content digest per signature (process-independent)
+
+
+def sig_digest(sig: tuple) -> int:
+    """Deterministic 64-bit digest of a schedule signature (unlike hash(),
+    equal across the host worker processes), so a batch's signatures are
+    deduplicated with numpy instead of one dict lookup per kernel."""
+    return int.from_bytes(hashlib.blake2b(repr(sig).encode(), digest_size=8).digest(), "little")
 
 
 def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | None, pname: str,
@@ -312,7 +321,10 @@ def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | N
         sigs.append((pname, a.kind.value, canonical_attrs(a.attrs), ins._t, shapes[k.anchor]._t))
         rows.append(kernel_tuple(graph, shapes, k, None, strategies.get(k.anchor, 0), -1))
     recs = np.array(rows, dtype=KERN_DTYPE) if rows else np.zeros(0, KERN_DTYPE)
-    return CandidateTrace(recs, sigs), kernels, shapes
+    memo_keys: dict = {}
+    keys = np.array([memo_keys[sg] if sg in memo_keys else memo_keys.setdefault(sg, sig_digest(sg)) for sg in sigs],
+                    dtype=np.uint64)
+    return CandidateTrace(recs, sigs, keys), kernels, shapes
 
 
 def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
@@ -346,24 +358,37 @@ def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, mem
     memo = _SCHEDULE_CACHE if memo is None else memo
     hits: dict[tuple, Schedule] = {}
     local_pending: dict[tuple, bytes] = {}
-    for ct in cts:
-        for r, sig in enumerate(ct.sigs):
-            if sig in hits or sig in local_pending:
-                continue
-            hit = memo.get(sig)
-            if hit is None and sig[1] not in _COMPLEX_VALUES:
-                hit = memo[sig] = TRIVIAL_SCHEDULE
-            if hit is not None:
-                hits[sig] = hit
-                continue
-            blob = first_seen.get(sig) if first_seen is not None else None
-            if blob is None:
-                rec = ct.recs[r:r + 1].copy()
-                rec["strategy"] = 0
-                blob = rec.tobytes()
-                if first_seen is not None:
-                    first_seen[sig] = blob
-            local_pending[sig] = blob
+    # Dedupe the batch's signatures by digest (numpy); only the distinct ones,
+    # in first-occurrence order, go through the memo (first-seen semantics
+    # unchanged). Records without digests take the per-kernel path.
+    flat_sigs = [sg for ct in cts for sg in ct.sigs]
+    nk_all = len(flat_sigs)
+    use_keys = nk_all > 0 and all(ct.sig_keys is not None and len(ct.sig_keys) == len(ct.sigs) for ct in cts)
+    if use_keys:
+        allk = np.concatenate([ct.sig_keys for ct in cts])
+        _, first, inverse = np.unique(allk, return_index=True, return_inverse=True)
+        order = np.sort(first)
+        recs_all = cat_records([ct.recs for ct in cts], KERN_DTYPE)
+        visit = [(flat_sigs[i], recs_all, int(i)) for i in order]
+    else:
+        visit = [(sig, ct.recs, r) for ct in cts for r, sig in enumerate(ct.sigs)]
+    for sig, recs_src, r in visit:
+        if sig in hits or sig in local_pending:
+            continue
+        hit = memo.get(sig)
+        if hit is None and sig[1] not in _COMPLEX_VALUES:
+            hit = memo[sig] = TRIVIAL_SCHEDULE
+        if hit is not None:
+            hits[sig] = hit
+            continue
+        blob = first_seen.get(sig) if first_seen is not None else None
+        if blob is None:
+            rec = recs_src[r:r + 1].copy()
+            rec["strategy"] = 0
+            blob = rec.tobytes()
+            if first_seen is not None:
+                first_seen[sig] = blob
+        local_pending[sig] = blob
     pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
     rows: dict[tuple, int] = {}
     sig_recs = []
@@ -380,8 +405,13 @@ def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, mem
     counts = [len(ct.sigs) for ct in cts]
     nk = sum(counts)
     if nk:
-        kern = np.concatenate([ct.recs for ct in cts])
-        kern["sig_index"] = [rows[sig] for ct in cts for sig in ct.sigs]
+        kern = recs_all if use_keys else cat_records([ct.recs for ct in cts], KERN_DTYPE)
+        if use_keys:
+            # row of each distinct signature, broadcast through the unique inverse
+            uniq_rows = np.array([rows[flat_sigs[i]] for i in first], np.int32)
+            kern["sig_index"] = uniq_rows[inverse.reshape(-1)]
+        else:
+            kern["sig_index"] = [rows[sig] for sig in flat_sigs]
     else:
         kern = np.zeros(1, KERN_DTYPE)
     offsets = np.zeros(len(cts) + 1, np.int32)
