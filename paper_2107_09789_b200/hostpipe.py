@@ -171,6 +171,8 @@ class HostPool:
         root = str(Path(__file__).resolve().parents[1])
         env["PYTHONPATH"] = root + (os.pathsep + env["PYTHONPATH"] if env.get("PYTHONPATH") else "")
         env["CUDA_VISIBLE_DEVICES"] = ""  # workers never need a GPU
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            env[var] = "1"  # one core per worker: no BLAS / OpenMP thread pools oversubscribing the host
         for _ in range(n):
             to_r, to_w = os.pipe()      # parent -> worker
             from_r, from_w = os.pipe()  # worker -> parent
