@@ -119,8 +119,6 @@ int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles,
 #define TOBF_OP_EPI 2      /* y = epilogue-chain(x) (standalone BN / ReLU / Add) */
 #define TOBF_OP_COPYCH 3   /* y[..., a0:a0+C] = x[..., a1:a1+C] channel copy (Concat / Slice) */
 #define TOBF_OP_SOFTMAX 4  /* y = softmax over channels (spatial 1x1 or per pixel) */
-#define TOBF_OP_IM2COL 5   /* y[pix][k] = im2col of x for k = (u*k2+v)*C + c, C = padded input channels;
-                            * a0 = k1 | k2 << 8, a1 = stride | pad << 8, Cpo = k1*k2*C, zero padding taps */
 
 typedef struct tobf_ew_desc {
   const float* x;

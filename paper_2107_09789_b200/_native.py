@@ -17,7 +17,7 @@ TOBF_OK = 0
 TOBF_E_INVALID, TOBF_E_CUDA, TOBF_E_FAULT = -1, -2, -3
 TOBF_MAX_EPI = 6
 EPI_NONE, EPI_AFFINE, EPI_RELU, EPI_ADD_TENSOR, EPI_ADD_CONST = 0, 1, 2, 3, 4
-OP_MAXPOOL, OP_EPI, OP_COPYCH, OP_SOFTMAX, OP_IM2COL = 1, 2, 3, 4, 5
+OP_MAXPOOL, OP_EPI, OP_COPYCH, OP_SOFTMAX = 1, 2, 3, 4
 
 
 class NativeUnavailable(RuntimeError):

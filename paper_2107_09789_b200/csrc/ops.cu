@@ -117,26 +117,6 @@ __global__ void ew_grouped_kernel(const tobf_ew_desc* __restrict__ descs, int n,
         for (int c = lane; c < d.Cpo; c += 32) yr[c] = c < d.C ? expf(xr[c] - mx) / sum : 0.0f;
         break;
       }
-      case TOBF_OP_IM2COL: {
-        // one float4 group of one output pixel's im2col row; C % 4 == 0, so a
-        // group never straddles two filter taps
-        const int groups = d.Cpo >> 2;
-        const int64_t pix = local / groups;
-        const int k = (int)(local - pix * groups) * 4;
-        const int k2 = (d.a0 >> 8) & 0xFF, st = d.a1 & 0xFF, pad = (d.a1 >> 8) & 0xFF;
-        const int tap = k / d.C, c = k - tap * d.C;
-        const int u = tap / k2, v = tap - u * k2;
-        const int64_t hw = (int64_t)d.Ho * d.Wo;
-        const int n_img = (int)(pix / hw);
-        const int rem = (int)(pix - (int64_t)n_img * hw);
-        const int yo = rem / d.Wo, xo = rem - (rem / d.Wo) * d.Wo;
-        const int iy = yo * st - pad + u, ix = xo * st - pad + v;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if ((unsigned)iy < (unsigned)d.H && (unsigned)ix < (unsigned)d.W)
-          q = __ldg(reinterpret_cast<const float4*>(d.x + (((int64_t)n_img * d.H + iy) * d.W + ix) * d.ldx + c));
-        *reinterpret_cast<float4*>(d.y + pix * d.ldy + k) = q;
-        break;
-      }
       default:
         break;
     }
@@ -240,14 +220,6 @@ extern "C" int tobf_ew_prepare(tobf_ew_desc* descs, int n, int64_t* total_work) 
       case TOBF_OP_SOFTMAX:
         work = pix_in * 32;
         break;
-      case TOBF_OP_IM2COL: {
-        const int k1 = d.a0 & 0xFF, k2 = (d.a0 >> 8) & 0xFF;
-        if (d.C % 4 || d.ldx % 4 || d.ldy % 4 || k1 < 1 || k2 < 1 || d.Cpo != k1 * k2 * d.C || d.ldy < d.Cpo ||
-            (d.a1 & 0xFF) < 1)
-          return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad im2col geometry", i);
-        work = (int64_t)d.batch * d.Ho * d.Wo * (d.Cpo / 4);
-        break;
-      }
       default:
         return tobf_fail(TOBF_E_INVALID, "ew desc %d: unknown op %d", i, d.op);
     }

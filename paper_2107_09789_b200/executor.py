@@ -297,14 +297,7 @@ _NO_EPI = (0, 0, 0)
 # A symbolic pointer is (space << 56) | value: value = byte offset into the
 # graph's activation block (SP_ARENA) or an index into one of the plan's
 # requirement tables (packed weight images, folded BatchNorms, constants).
-SP_INPUT, SP_ARENA, SP_WIMG, SP_AFFINE, SP_CONST, SP_IM2COL = 1, 2, 3, 4, 5, 6
-
-# Convs reading the stacked graph input with at most this many (padded)
-# channels — the stem — run as a 1x1 GEMM over an explicit im2col of the
-# input, built ONCE per run for every such conv of the population with the
-# same geometry (tobf OP_IM2COL): a 4-channel 7x7 tap is a 16-B chunk, so
-# gathering it inside the GEMM costs more cp.async issue than MMA time.
-IM2COL_MAX_CP = 8
+SP_INPUT, SP_ARENA, SP_WIMG, SP_AFFINE, SP_CONST = 1, 2, 3, 4, 5
 _SP_SHIFT = 56
 _SP_LOW = (1 << _SP_SHIFT) - 1
 
@@ -367,7 +360,6 @@ class ForwardPlan:
     input_shape: TensorShape
     flops_per_image: int
     gemm_act_bytes_per_image: int = 0   # conv/linear input + output activations, fp32, once each
-    im2col: list = field(default_factory=list)  # (k1, k2, stride, pad, Ho, Wo, cp) of the graph input
     gemm_weight_bytes: int = 0          # conv/linear weights, fp32, once
 
 
@@ -394,8 +386,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
     def buf(v: int) -> int:
         return _sym(SP_INPUT, 0) if v < 0 else _sym(SP_ARENA, offs[v])
 
-    tables: dict[str, tuple[dict, list]] = {"wimg": ({}, []), "affine": ({}, []), "const": ({}, []),
-                                            "im2col": ({}, [])}
+    tables: dict[str, tuple[dict, list]] = {"wimg": ({}, []), "affine": ({}, []), "const": ({}, [])}
 
     def index(table: str, entry) -> int:
         idx, lst = tables[table]
@@ -447,19 +438,9 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
             wi = index("wimg", (refs.ref(w), n.kind is K.Conv2D, s_in.height, s_in.width, s_in.channels,
                                 k1, k2, cp, j, bn))
             epi = epi_rows(op.steps)
-            ho, wo = s_out.height, s_out.width
-            if n.kind is K.Conv2D and op.src < 0 and cp <= IM2COL_MAX_CP and k1 * k2 > 1:
-                # the same GEMM as a 1x1 conv over the shared im2col buffer; its
-                # K order (u, v, c) is the packed weight image's, so the image is reused
-                ii = index("im2col", (k1, k2, stride, pad, ho, wo, cp))
-                kk = k1 * k2 * cp
-                conv_rows.append((_sym(SP_IM2COL, ii), _sym(SP_WIMG, wi), buf(op.out), batch, ho, wo, kk,
-                                  ho, wo, _rup4(j), j, 1, 1, 1, 0, 0, 0, 0, 0, 0,
-                                  sum(1 for e in epi if e[0]), kk, _rup4(j), epi, 0, 0, 1, 0))
-            else:
-                conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
-                                  ho, wo, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
-                                  sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0))
+            conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
+                              s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
+                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0))
             conv_lv.append(op.level)
             conv_bn.append(bn)
             conv_k.append(k1 * k2 * cp)
@@ -495,8 +476,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
         ew_level=np.array(ew_lv, np.int32),
         wimg=tables["wimg"][1], affine=tables["affine"][1], const=tables["const"][1],
         arena_bytes=used, out_off=offs[lw.out_node], out_shape=shapes[lw.out_node], input_shape=ishape,
-        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes,
-        im2col=tables["im2col"][1])
+        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes)
 
 
 def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, tables: dict) -> np.ndarray:
@@ -684,15 +664,11 @@ class PopulationRun:
         ctx, lib, plans = self.ctx, self.ctx.lib, self.plans
         s = self.input_shape
         in_floats = Arena.round(self.batch * s.height * s.width * _rup4(s.channels))
-        # one shared im2col buffer per distinct stem geometry of the population
-        col_geo = list(dict.fromkeys(e for p in plans for e in getattr(p, "im2col", [])))
-        col_floats = [Arena.round(self.batch * e[4] * e[5] * e[0] * e[1] * e[6]) for e in col_geo]
-        total = 4 * in_floats + 4 * sum(col_floats) + sum(p.arena_bytes for p in plans)
+        total = 4 * in_floats + sum(p.arena_bytes for p in plans)
         self.arena = ctx_arena(ctx, total // 4 + 4096)
         self.x_ptr = self.arena.take(in_floats)
-        col_ptr = {e: self.arena.take(f) for e, f in zip(col_geo, col_floats)}
         bases = np.zeros(len(plans), np.int64)
-        cur = self.arena.base + 4 * self.arena.used
+        cur = self.x_ptr + 4 * in_floats
         for i, p in enumerate(plans):
             bases[i] = cur
             cur += p.arena_bytes
@@ -703,7 +679,7 @@ class PopulationRun:
         const_memo: dict = {}
         aff = self._affine_ptrs(list({r for p in plans for r in p.affine}))
         tabs = {}
-        for sp, name in ((SP_WIMG, "wimg"), (SP_AFFINE, "affine"), (SP_CONST, "const"), (SP_IM2COL, "im2col")):
+        for sp, name in ((SP_WIMG, "wimg"), (SP_AFFINE, "affine"), (SP_CONST, "const")):
             ptrs, offsets = [], np.zeros(len(plans), np.int64)
             for i, p in enumerate(plans):
                 offsets[i] = len(ptrs)
@@ -714,8 +690,6 @@ class PopulationRun:
                             v = wimg_memo[e] = self._wimg_ptr(e)
                     elif sp == SP_AFFINE:
                         v = aff[e]
-                    elif sp == SP_IM2COL:
-                        v = col_ptr[e]
                     else:
                         v = const_memo.get(e)
                         if v is None:
@@ -737,13 +711,6 @@ class PopulationRun:
         conv_bn = np.concatenate([p.conv_bn for p in plans])
         conv_k = np.concatenate([p.conv_k for p in plans])
         ew_level = np.concatenate([p.ew_level for p in plans])
-        if col_geo:  # the shared im2col builds run first (level -1), already linked
-            cp_in = _rup4(s.channels)
-            col_rows = [(self.x_ptr, col_ptr[e], N.OP_IM2COL, self.batch, s.height, s.width, cp_in, cp_in, e[4],
-                         e[5], e[0] * e[1] * cp_in, e[0] | (e[1] << 8), e[2] | (e[3] << 8), 0, 0,
-                         e[0] * e[1] * cp_in, 0, [_NO_EPI] * N.TOBF_MAX_EPI) for e in col_geo]
-            ew = cat_records([np.array(col_rows, dtype=EW_DTYPE), ew], EW_DTYPE)
-            ew_level = np.concatenate([np.full(len(col_rows), -1, ew_level.dtype), ew_level])
         # one launch per (level, BN), long K first; one ew launch per level
         order = np.lexsort((-conv_k, -conv_bn, conv_level))
         conv = conv[order]
