@@ -204,25 +204,30 @@ def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
     B, t_max = args.ler_pairs, 176
     lens = torch.randint(119, 170, (B,), generator=gen, device=dev, dtype=torch.int32)
     toks = torch.randint(1, 5, (B, t_max), generator=gen, device=dev, dtype=torch.int8)
+    truth_dev = torch.from_numpy(truth).to(dev)
     for _ in range(3):
-        attacker.edit_distances(toks, lens, truth)
+        attacker.edit_distances(toks, lens, truth_dev)
     torch.cuda.synchronize()
     evs = []
+    clocks = ClockSampler(dev.index)
+    clocks.start()
     for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        attacker.edit_distances(toks, lens, truth)
+        attacker.edit_distances(toks, lens, truth_dev)
         b.record()
         evs.append((a, b))
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    ler_clk = clocks.stop()
+    ms = statistics.median(a.elapsed_time(b) for a, b in evs)
     alg = int(lens.sum().item()) + B * m + B * (4 + 4 + 8)  # |L| + |L*| tokens, ntok in, ED + LER out
     gbs = alg / (ms / 1e3) / 1e9
     out["ler"] = {"kernel": "levenshtein_bp_kernel (thread per pair, bit-parallel)", "pairs": B, "truth_len": m,
                   "pred_len": "U[119,169]", "ms_per_launch": round(ms, 4), "pairs_per_s": B / (ms / 1e3),
                   "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                   "frac": round(gbs / hbm_peak, 4), "algorithmic_bytes": alg,
-                  "bytes_def": "sum(|L|) + pairs*|L*| (1 B tokens) + 16 B/pair (ntok, ED, LER)"}
+                  "bytes_def": "sum(|L|) + pairs*|L*| (1 B tokens) + 16 B/pair (ntok, ED, LER)",
+                  "timing": "median of 10 launches", "clocks": ler_clk}
     del toks, lens
     # cfg5: 10k traces, T ~ U[119,169], F = 9 cost-model-scale features
     nt = 10_000
@@ -236,7 +241,7 @@ def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
     def fit():
         for p in predictors:
             tk, nk = attacker.decode(feats, offs, nt, tmax, p)
-            attacker.edit_distances(tk, nk, truth)
+            attacker.edit_distances(tk, nk, truth_dev)
 
     for _ in range(2):
         fit()
