@@ -146,12 +146,7 @@ __global__ void lstm_ctc_kernel(const double* __restrict__ feats, const int32_t*
 // accumulation order (bias, x[0..F), h[0..H)) and every rounding are the
 // same as the single-CTA formulation and the CPU oracle.
 constexpr int kLstmUnits = 32;
-#ifndef TOBF_LSTM_TPC_SMALL
-#define TOBF_LSTM_TPC_SMALL 16
-#endif
-#ifndef TOBF_LSTM_SMALL_B
-#define TOBF_LSTM_SMALL_B 64
-#endif
+
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -547,14 +542,13 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   if (H % kLstmUnits == 0 && H / kLstmUnits <= 16) {
-    // Small batches (one GA generation: the recurrence is latency-bound and
-    // runs concurrently with the forward) pack 16 traces per cluster (the h double buffer of 16 traces plus the
-    // bf16 gate rows fill the 227 KB of shared memory at H=512) so
-    // the attacker occupies few SMs; large sweeps keep 8 per cluster.
-    if (B <= TOBF_LSTM_SMALL_B)
-      return launch_lstm_cluster<TOBF_LSTM_TPC_SMALL>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out,
-                                                      tokens, T_max, ntok, st);
-    return launch_lstm_cluster<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+    // 16 traces per cluster (the h double buffer of 16 traces plus the bf16
+    // gate rows fill the 227 KB of shared memory at H=512): the per-step
+    // cluster barrier and h broadcast are paid once for twice the traces of
+    // TPC=8 (cfg5 sweep 375 -> 334 ms), and a generation-sized batch running
+    // concurrently with the forward occupies half the SMs.
+    return launch_lstm_cluster<16>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok,
+                                   st);
   }
   if (B >= 148 * 8) return launch_lstm<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   return launch_lstm<2>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
