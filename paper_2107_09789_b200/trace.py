@@ -436,7 +436,13 @@ def run_trace(tp: TracePlan, profile: bool = True, restore: bool = False) -> Non
     pc = tp.profile.as_c()
     sp = C.c_void_p(ctx.sp)
     if restore:
-        tp.sigs.copy_(torch.frombuffer(bytearray(tp._sig_template), dtype=torch.uint8), non_blocking=True)
+        # pristine table kept on the device: a stream-ordered D2D copy (a
+        # pageable H2D here would block the host until the previous step
+        # drained and leave the GPU idle while this step is enqueued)
+        tmpl = getattr(tp, "_sig_template_dev", None)
+        if tmpl is None:
+            tmpl = tp._sig_template_dev = ctx.upload_bytes(tp._sig_template)
+        tp.sigs.copy_(tmpl, non_blocking=True)
     if tp.pending:
         ctx.check(ctx.lib.tobf_schedule_search(C.c_void_p(tp.sigs.data_ptr()), tp.nsig, C.byref(pc), sp),
                   "schedule search")
