@@ -264,6 +264,9 @@ class PopulationEvaluator:
         links and launches. First-seen schedule semantics hold across
         micro-batches: a signature pending in several of them is searched
         from its first occurrence's descriptor everywhere."""
+        if not plans:
+            self.last_host_ms = {}
+            return np.zeros(0, dtype=RECORD_DTYPE)
         first_seen: dict = {}
         jobs = []
         bounds = _micro_bounds(len(plans), micro)

@@ -859,6 +859,9 @@ def compare_outputs(ctx: DeviceContext, run: PopulationRun, ref_index: int, cand
                     tol: float) -> tuple[torch.Tensor, torch.Tensor]:
     """Device verdicts of candidates vs the reference graph output (a = ref,
     b = cand). Pointer tables are staged once per run and reused."""
+    if not cand_indices:  # e.g. every plan of the batch was infeasible
+        return (torch.zeros(0, dtype=torch.int32, device=ctx.device),
+                torch.zeros(0, dtype=torch.float32, device=ctx.device))
     key = (ref_index, tuple(cand_indices))
     cache = run.__dict__.setdefault("_cmp", {})
     if key not in cache:

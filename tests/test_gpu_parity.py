@@ -324,6 +324,54 @@ def test_population_evaluation_matches_oracles(ctx):
         assert rec["reward"][i] == R
 
 
+@pytest.mark.parametrize("name,kw,mode,n", [("vgg16", {"size": 32, "hidden": 256}, "dimension", 4),
+                                             ("c1c2", {"size": 24}, "dimension", 5)])
+def test_dimension_population_matches_oracles(ctx, name, kw, mode, n):
+    """cfg4 / cfg1 shape, end to end through the worker pool: widened,
+    kernel-widened candidates whose weights are synthesised on the device
+    (derived.py), plus an identity plan; T / verdict / LER / R against the
+    oracles on the eagerly materialised graphs."""
+    g = fixtures.FIXTURES[name](**kw)
+    plans = _plans(g, mode, n, seed=6) + [knobs.identity_plan(g, mode)]
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128, 256)))
+    pe = PopulationEvaluator(g, ev, budget=0.02, trials=2, seed=0, memo={})
+    try:
+        rec = pe.evaluate_records(plans, micro=3, memo={}, workers=2)
+    finally:
+        pe.close()
+    truth = fitness.encode_labels(label_sequence(g))
+    memo = CM.ScheduleMemo()
+    t_star = CM.profile_pipeline(g, "default", None, None, CM.ScheduleMemo())[3]
+    for i, p in enumerate(plans):
+        og, d = knobs.apply_plan(g, p)
+        _, _, rows, T = CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)
+        ok, _ = IR.equivalence_check(g, og, trials=2, seed=0)
+        assert rec["latency"][i] == T and bool(rec["ok"][i]) == ok, i
+        feats = np.array([[r[f] for f in CM.FEATURES] for r in rows])
+        lers = [FR.ler(FR.lstm_ctc(feats, 9, pr.weights()), truth) for pr in ev.predictors]
+        R, mean = FR.eq10(lers, T, ok, t_star, 0.02)
+        assert rec["mean_ler"][i] == mean and rec["reward"][i] == R, i
+    assert rec["ok"][-1] == 1 and rec["latency"][-1] == t_star  # the identity plan is the vanilla graph
+
+
+def test_population_edge_cases(ctx):
+    """An empty batch, an all-infeasible batch (plans that cannot be applied
+    score R = 0 without touching the device pipeline's candidates) and a
+    single candidate."""
+    g = fixtures.c1c2(size=16)
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
+    pe = PopulationEvaluator(g, ev, budget=0.02, trials=2, seed=0, memo={})
+    assert len(pe.evaluate_records([], workers=0)) == 0
+    space = ga.search_space(g, "dimension")
+    bad = knobs.ObfuscationPlan("dimension", tuple(knobs.PlanEntry(e.layer_id, widen_factor=0.5) for e in
+                                                   knobs.identity_plan(g, "dimension").entries))  # NotWidenable
+    rec = pe.evaluate_records([bad, bad], workers=0)
+    assert rec["feasible"].tolist() == [0, 0] and rec["reward"].tolist() == [0.0, 0.0]
+    one = pe.evaluate_records(_plans(g, "dimension", 1, seed=2), workers=0)
+    assert len(one) == 1 and one["feasible"][0] == 1
+    assert space  # the search space the GA draws from is non-empty
+
+
 def test_micro_batched_records_match_single_batch(ctx):
     """evaluate_records overlaps host prep of micro-batch i+1 with the device
     run of micro-batch i; records (incl. first-seen schedules) are identical."""
