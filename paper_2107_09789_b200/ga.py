@@ -137,9 +137,26 @@ class GaResult:
     log: list = field(default_factory=list)   # (generation, index, reward, mean_ler, T/T*)
 
 
-def run_ga(graph: Graph, mode: str, budget: float, params: GaParams, evaluate_fn) -> GaResult:
-    """SPEC.md:572-580. ``evaluate_fn(plans) -> records`` (RECORD_DTYPE) — the
-    GPU population evaluator, possibly sharded across ranks."""
+@dataclass
+class GaState:
+    """Everything the search needs to continue after generation ``gen``: the
+    surviving population and its rewards, the best-so-far, the log and the
+    RNG state (a checkpoint is this object; resuming is bit-identical to an
+    uninterrupted run, SPEC.md:600 generation log)."""
+
+    mode: str
+    params: GaParams
+    gen: int
+    pop: np.ndarray
+    rewards: np.ndarray
+    best_reward: float
+    best_genome: np.ndarray
+    rng_state: dict
+    log: list = field(default_factory=list)   # (generation, index, reward, mean_ler, T)
+
+
+def ga_init(graph: Graph, mode: str, params: GaParams, evaluate_fn) -> GaState:
+    """Generation 0: random genomes from the master seed, evaluated."""
     rng = np.random.default_rng(params.seed)
     space = search_space(graph, mode)
     sizes = domain_sizes(mode, space)
@@ -148,18 +165,48 @@ def run_ga(graph: Graph, mode: str, budget: float, params: GaParams, evaluate_fn
     rewards = rec["reward"].astype(np.float64)
     log = [(0, i, float(r["reward"]), float(r["mean_ler"]), float(r["latency"])) for i, r in enumerate(rec)]
     bi = int(_order(rewards)[0])
-    best = (float(rewards[bi]), pop[bi].copy())
-    for gen in range(1, params.generations + 1):
-        sigma = params.sigma0 / (2 ** ((gen - 1) // params.sigma_halving_period))
-        kids = next_generation(rng, pop, rewards, sizes, sigma, params)
-        krec = evaluate_fn([decode_genome(graph, mode, space, g) for g in kids])
-        krew = krec["reward"].astype(np.float64)
-        log += [(gen, i, float(r["reward"]), float(r["mean_ler"]), float(r["latency"])) for i, r in enumerate(krec)]
-        ki = int(_order(krew)[0])
-        if krew[ki] > best[0]:
-            best = (float(krew[ki]), kids[ki].copy())
-        merged = np.concatenate([pop, kids])
-        mrew = np.concatenate([rewards, krew])
-        keep = _order(mrew)[:params.population]
-        pop, rewards = merged[keep], mrew[keep]
-    return GaResult(best[1], decode_genome(graph, mode, space, best[1]), best[0], log)
+    return GaState(mode, params, 0, pop, rewards, float(rewards[bi]), pop[bi].copy(), rng.bit_generator.state, log)
+
+
+def ga_step(graph: Graph, state: GaState, evaluate_fn) -> GaState:
+    """One generation: offspring, evaluation, elitist truncation."""
+    params, mode = state.params, state.mode
+    rng = np.random.default_rng()
+    rng.bit_generator.state = state.rng_state
+    space = search_space(graph, mode)
+    sizes = domain_sizes(mode, space)
+    gen = state.gen + 1
+    sigma = params.sigma0 / (2 ** ((gen - 1) // params.sigma_halving_period))
+    kids = next_generation(rng, state.pop, state.rewards, sizes, sigma, params)
+    krec = evaluate_fn([decode_genome(graph, mode, space, g) for g in kids])
+    krew = krec["reward"].astype(np.float64)
+    log = state.log + [(gen, i, float(r["reward"]), float(r["mean_ler"]), float(r["latency"]))
+                       for i, r in enumerate(krec)]
+    best_r, best_g = state.best_reward, state.best_genome
+    ki = int(_order(krew)[0])
+    if krew[ki] > best_r:
+        best_r, best_g = float(krew[ki]), kids[ki].copy()
+    merged = np.concatenate([state.pop, kids])
+    mrew = np.concatenate([state.rewards, krew])
+    keep = _order(mrew)[:params.population]
+    return GaState(mode, params, gen, merged[keep], mrew[keep], best_r, best_g, rng.bit_generator.state, log)
+
+
+def ga_result(graph: Graph, state: GaState) -> GaResult:
+    space = search_space(graph, state.mode)
+    return GaResult(state.best_genome, decode_genome(graph, state.mode, space, state.best_genome),
+                    state.best_reward, state.log)
+
+
+def run_ga(graph: Graph, mode: str, budget: float, params: GaParams, evaluate_fn, on_generation=None) -> GaResult:
+    """SPEC.md:572-580. ``evaluate_fn(plans) -> records`` (RECORD_DTYPE) — the
+    GPU population evaluator, possibly sharded across ranks. ``on_generation``
+    (GaState) is called after every generation (checkpointing, logging)."""
+    state = ga_init(graph, mode, params, evaluate_fn)
+    if on_generation is not None:
+        on_generation(state)
+    while state.gen < params.generations:
+        state = ga_step(graph, state, evaluate_fn)
+        if on_generation is not None:
+            on_generation(state)
+    return ga_result(graph, state)

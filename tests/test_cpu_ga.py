@@ -105,3 +105,23 @@ def test_ler_paper_example():
     pred = [2] * 18 + [3] * 26
     assert FR.levenshtein(pred, truth) == 44
     assert abs(FR.ler(pred, truth) - 2.4444444444444446) < 1e-15
+
+
+def test_checkpoint_resume_is_bit_identical():
+    """A GaState pickled after generation k and resumed gives exactly the
+    uninterrupted run (RNG state, population, log): what the CLI's
+    --resume relies on."""
+    import pickle
+    g = fixtures.c1c2()
+    params = ga.GaParams(population=8, generations=5, seed=11)
+    ref = ga.run_ga(g, "dimension", 0.02, params, fake_eval)
+    st = ga.ga_init(g, "dimension", params, fake_eval)
+    for _ in range(2):
+        st = ga.ga_step(g, st, fake_eval)
+    st = pickle.loads(pickle.dumps(st))
+    while st.gen < params.generations:
+        st = ga.ga_step(g, st, fake_eval)
+    res = ga.ga_result(g, st)
+    assert res.best_reward == ref.best_reward
+    assert np.array_equal(res.best_genome, ref.best_genome)
+    assert res.log == ref.log
