@@ -44,7 +44,27 @@ def _parse(argv):
     g.add_argument("--micro", type=int, default=16, help="micro-batch size of the evaluator")
     g.add_argument("--out", type=Path, required=True)
     g.add_argument("--resume", action="store_true")
+    g.add_argument("--attackers", type=Path, default=None,
+                   help="npz of trained predictors (train-attacker); default: seeded random-init")
+    t = sub.add_parser("train-attacker", help="train the bagged LSTM attackers on random architectures")
+    t.add_argument("--n", type=int, default=2000, help="random networks in the dataset (4:1 split)")
+    t.add_argument("--size", type=int, default=32, help="input resolution (32: CIFAR-like, 224: ImageNet-like)")
+    t.add_argument("--epochs", type=int, default=30)
+    t.add_argument("--seed", type=int, default=0)
+    t.add_argument("--out", type=Path, required=True)
     return ap.parse_args(argv)
+
+
+def train_attacker_cli(args) -> int:
+    from .attacker_train import ArchGenConfig, save_predictors, train_bagged
+    from .engine import device
+    device()
+    classes = 1000 if args.size >= 224 else 10
+    cfg = ArchGenConfig(input_shape=(1, 3, args.size, args.size), num_classes=classes, seed=args.seed)
+    preds, lers = train_bagged(args.n, cfg, epochs=args.epochs, seed=args.seed)
+    save_predictors(args.out, preds)
+    print(json.dumps({"out": str(args.out), "hiddens": [p.hidden for p in preds], "val_ler": lers}), flush=True)
+    return 0
 
 
 def _save(out: Path, state, memo: dict) -> None:
@@ -85,7 +105,11 @@ def run_ga_cli(args) -> int:
         if (state.mode, same) != (args.mode, params):
             raise SystemExit(f"checkpoint {ck} is for {state.mode} {state.params}, not {args.mode} {params}")
         state.params = params  # --generations may extend the run
-    pe = PopulationEvaluator(vanilla, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed,
+    ev = Evaluator()
+    if args.attackers is not None:
+        from .attacker_train import load_predictors
+        ev = Evaluator(predictors=load_predictors(args.attackers))
+    pe = PopulationEvaluator(vanilla, ev, budget=args.budget, trials=args.trials, seed=args.seed,
                              memo=memo, exchange=tdist.exchange_signatures if world > 1 else None)
 
     def evaluate(plans):
@@ -132,6 +156,8 @@ def main(argv=None) -> int:
     args = _parse(sys.argv[1:] if argv is None else argv)
     if args.cmd == "ga":
         return run_ga_cli(args)
+    if args.cmd == "train-attacker":
+        return train_attacker_cli(args)
     return 2
 
 
