@@ -299,11 +299,20 @@ class CandidateTrace:
     sig_keys: np.ndarray | None = None  # 64-bit content digest per signature (process-independent)
 
 
+_DIGESTS: dict[tuple, int] = {}
+
+
 def sig_digest(sig: tuple) -> int:
     """Deterministic 64-bit digest of a schedule signature (unlike hash(),
     equal across the host worker processes), so a batch's signatures are
-    deduplicated with numpy instead of one dict lookup per kernel."""
-    return int.from_bytes(hashlib.blake2b(repr(sig).encode(), digest_size=8).digest(), "little")
+    deduplicated with numpy instead of one dict lookup per kernel. Memoised
+    per process (signatures repeat across a population)."""
+    d = _DIGESTS.get(sig)
+    if d is None:
+        if len(_DIGESTS) > 1 << 18:
+            _DIGESTS.clear()
+        d = _DIGESTS[sig] = int.from_bytes(hashlib.blake2b(repr(sig).encode(), digest_size=8).digest(), "little")
+    return d
 
 
 def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | None, pname: str,
@@ -321,9 +330,7 @@ def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | N
         sigs.append((pname, a.kind.value, canonical_attrs(a.attrs), ins._t, shapes[k.anchor]._t))
         rows.append(kernel_tuple(graph, shapes, k, None, strategies.get(k.anchor, 0), -1))
     recs = np.array(rows, dtype=KERN_DTYPE) if rows else np.zeros(0, KERN_DTYPE)
-    memo_keys: dict = {}
-    keys = np.array([memo_keys[sg] if sg in memo_keys else memo_keys.setdefault(sg, sig_digest(sg)) for sg in sigs],
-                    dtype=np.uint64)
+    keys = np.array([sig_digest(sg) for sg in sigs], dtype=np.uint64)
     return CandidateTrace(recs, sigs, keys), kernels, shapes
 
 
