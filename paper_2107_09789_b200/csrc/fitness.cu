@@ -238,10 +238,15 @@ __global__ void __launch_bounds__(TPC * 32, 1)
   const uint32_t hv_local = static_cast<uint32_t>(__cvta_generic_to_shared(hv));
   float c = 0.0f;
   int prev = 0, cnt = 0;
+  // x_t is software-pipelined one step ahead: the global load and the fp64
+  // log1p of step t+1's features run during step t's gate products instead of
+  // at the head of step t+1 (same values: identical rounding, earlier)
+  float x_cur = (u < F && 0 < len) ? (float)tobf_log1p_d(feats[(int64_t)row0 * 9 + u]) : 0.0f;
   for (int t = 0; t < tmax; ++t) {
     float* hcur = hv + (t & 1) * TPC * Lp + q * Lp;
     const int nxt = (t + 1) & 1;
-    if (u < F) hcur[u] = t < len ? (float)tobf_log1p_d(feats[(int64_t)(row0 + t) * 9 + u]) : 0.0f;
+    if (u < F) hcur[u] = x_cur;
+    const double f_next = (u < F && t + 1 < len) ? feats[(int64_t)(row0 + t + 1) * 9 + u] : 0.0;
     __syncwarp();
     float acc0 = bsm[u], acc1 = bsm[32 + u], acc2 = bsm[64 + u], acc3 = bsm[96 + u];
     const uint2* wrow = wq + u;
@@ -276,6 +281,7 @@ __global__ void __launch_bounds__(TPC * 32, 1)
       c = fmaf(fg, c, ig * gg);
       hval = og * tobf_tanh(c);
     }
+    x_cur = (u < F && t + 1 < len) ? (float)tobf_log1p_d(f_next) : 0.0f;
     const uint32_t slot = hv_local + 4u * (uint32_t)(nxt * TPC * Lp + q * Lp + F + unit);
     for (int rr = 0; rr < CS; ++rr) st_cluster_f32(map_shared(slot, rr), hval);
     cluster_sync_all();

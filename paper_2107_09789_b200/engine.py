@@ -49,10 +49,15 @@ class DeviceContext:
         self.h2d_bytes = 0     # host->device bytes staged through this context
 
     def side_streams(self, n: int) -> list:
-        """``n`` extra engine streams (created once, reused)."""
+        """``n`` extra engine streams (created once, reused), at the highest
+        stream priority: the work put on them (the latency-bound attacker
+        recurrences) is dispatched ahead of the persistent conv grids whenever
+        SMs free up, so it overlaps the forward instead of queueing behind it."""
         ss = self.__dict__.setdefault("_side", [])
+        if not ss:
+            self._side_priority = torch.cuda.Stream.priority_range()[1]  # (low, high): high is the smaller
         while len(ss) < n:
-            ss.append(torch.cuda.Stream(self.device))
+            ss.append(torch.cuda.Stream(self.device, priority=self._side_priority))
         return ss[:n]
 
     @property
