@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=1, help="cpu_baseline sample: rounds of one candidate per core")
-    ap.add_argument("--micro", type=lambda v: [int(x) for x in v.split(",")], default=[16],
+    ap.add_argument("--micro", type=lambda v: [int(x) for x in v.split(",")], default=[32],
                     help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run)")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")

@@ -254,7 +254,7 @@ class PopulationEvaluator:
         self.ctx.sync()
         return rec
 
-    def evaluate_records(self, plans: list[ObfuscationPlan], micro=16, memo: dict | None = None,
+    def evaluate_records(self, plans: list[ObfuscationPlan], micro=32, memo: dict | None = None,
                          workers: int | None = None) -> np.ndarray:
         """Records for ``plans`` with host preparation of micro-batch i+1
         overlapping the device pipeline of micro-batch i (launches are async;
