@@ -120,10 +120,12 @@ class PopulationEvaluator:
             self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers)
 
     def prepare_encoded(self, plans: list[ObfuscationPlan], results: list, memo: dict | None = None,
-                        first_seen: dict | None = None) -> dict:
+                        first_seen: dict | None = None, link: bool = True) -> dict:
         """Host half from worker results (hostpipe.encode_candidate tuples, in
-        candidate order): link forward plans, resolve the schedule memo,
-        stage everything into HBM."""
+        candidate order): resolve the schedule memo and stage the trace records,
+        then (``link``) link the forward plans and stage them into HBM.
+        ``link=False`` leaves the forward to ``link_forward``, so the caller
+        can start the trace + attacker stage on the device first."""
         t0 = time.perf_counter()
         cands, feas, fps, cts = [], [], [], []
         base = results[0][0] if results else 0
@@ -140,17 +142,24 @@ class PopulationEvaluator:
             fps.append(fp)
             cts.append(ct)
         t1 = time.perf_counter()
-        run = PopulationRun(self.ctx, None, reps=self.trials, plans=[self.vanilla_plan] + fps, refs=self.prefs)
-        t2 = time.perf_counter()
         tp = prepare_trace_records(cts, self.ev.profile, self.memo if memo is None else memo,
                                    exchange=self.exchange, first_seen=first_seen) if cts else None
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
-        t3 = time.perf_counter()
-        return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
+        t2 = time.perf_counter()
+        prep = {"cands": cands, "feas": feas, "run": None, "fps": fps, "trace": tp, "idx": idx,
                 "feasible": [c.error is None for c in cands],
                 "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
-                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
-                            "trace_prep": 1e3 * (t3 - t2)}}
+                "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 0.0, "trace_prep": 1e3 * (t2 - t1)}}
+        if link:
+            self.link_forward(prep)
+        return prep
+
+    def link_forward(self, prep: dict) -> None:
+        """Link the batch's forward plans (weights, arena, descriptor tables)."""
+        t0 = time.perf_counter()
+        prep["run"] = PopulationRun(self.ctx, None, reps=self.trials, plans=[self.vanilla_plan] + prep.pop("fps"),
+                                    refs=self.prefs)
+        prep["host_ms"]["lower_pack"] = 1e3 * (time.perf_counter() - t0)
 
     # ---------------------------------------------------------------- host
     def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None) -> dict:
@@ -181,66 +190,81 @@ class PopulationEvaluator:
             cold_schedules: bool = False) -> dict:
         """Device pipeline over a prepared batch; returns device tensors.
         ``cold_schedules`` re-runs the full schedule search for every
-        signature (benchmark: no memo carried between steps)."""
-        ctx = self.ctx
-        cands, feas, run, tp = prep["cands"], prep["feas"], prep["run"], prep["trace"]
+        signature (benchmark: no memo carried between steps).
+
+        The trace features and the attacker's fitness stage do not depend on
+        the forward: trace first, then the three bagged predictors (LSTM + CTC +
+        LER, GPU-latency-bound recurrences) on high-priority side streams
+        running concurrently with the forward + verdict on the main stream;
+        joined before Eq. 10, which needs both."""
         ev = {}
         mark = (lambda k: ev.setdefault(k, torch.cuda.Event(enable_timing=True)).record()) if timing else \
             (lambda k: None)
         mark("start")
-        # The trace features and the attacker's fitness stage do not depend on
-        # the forward: trace first, then the three bagged predictors (LSTM +
-        # CTC + LER, GPU-latency-bound recurrences) on side streams running
-        # concurrently with the forward + verdict on the main stream; joined
-        # before Eq. 10, which needs both.
+        att = self.run_attack(prep, cold_schedules, mark)
+        return self.run_forward(prep, att, x_dev, mark, ev)
+
+    def run_attack(self, prep: dict, cold_schedules: bool = False, mark=None) -> dict:
+        """Trace (main stream) and the bagged attackers (side streams) of a batch."""
+        ctx = self.ctx
+        cands, feas, tp = prep["cands"], prep["feas"], prep["trace"]
         if tp is not None:
             run_trace(tp, restore=cold_schedules)
-        mark("trace")
+        if mark is not None:
+            mark("trace")
         n = len(cands)
         ncf = len(feas)
-        lers = torch.zeros((len(self.ev.predictors), n), dtype=torch.float64, device=ctx.device)
-        T = torch.zeros(n, dtype=torch.float64, device=ctx.device)
-        ok = torch.zeros(n, dtype=torch.int32, device=ctx.device)
-        worst = torch.zeros(n, dtype=torch.float32, device=ctx.device)
-        ntok0 = torch.zeros(n, dtype=torch.int32, device=ctx.device)
-        main = ctx.stream
-        joins = []
+        att = {"lers": torch.zeros((len(self.ev.predictors), n), dtype=torch.float64, device=ctx.device),
+               "ntok": torch.zeros(n, dtype=torch.int32, device=ctx.device), "joins": []}
         if ncf:
             idx = prep["idx"]
             if not hasattr(self, "_truth_dev"):
                 self._truth_dev = ctx.upload_array(self.truth)
             side = ctx.side_streams(len(self.ev.predictors))
             fork = torch.cuda.Event()
-            fork.record(main)
+            fork.record(ctx.stream)
             for p, pred in enumerate(self.ev.predictors):
                 s = side[p]
                 with torch.cuda.stream(s):
                     s.wait_event(fork)
                     toks, ntok = decode(tp.feats, tp.offsets, ncf, max(prep["t_max"], 1), pred, s.cuda_stream)
                     _, lr, _ = edit_distances(toks, ntok, self._truth_dev, s.cuda_stream)
-                    lers[p].index_copy_(0, idx, lr)
+                    att["lers"][p].index_copy_(0, idx, lr)
                     if p == 0:
-                        ntok0.index_copy_(0, idx, ntok)
+                        att["ntok"].index_copy_(0, idx, ntok)
                 join = torch.cuda.Event()
                 join.record(s)
-                joins.append(join)
+                att["joins"].append(join)
+        return att
+
+    def run_forward(self, prep: dict, att: dict, x_dev: torch.Tensor | None = None, mark=None,
+                    ev: dict | None = None) -> dict:
+        """Forward + verdicts (main stream), join with the attackers, Eq. 10."""
+        ctx = self.ctx
+        cands, feas, run, tp = prep["cands"], prep["feas"], prep["run"], prep["trace"]
+        mark = mark or (lambda k: None)
+        n = len(cands)
+        T = torch.zeros(n, dtype=torch.float64, device=ctx.device)
+        ok = torch.zeros(n, dtype=torch.int32, device=ctx.device)
+        worst = torch.zeros(n, dtype=torch.float32, device=ctx.device)
         if x_dev is None:
             x_dev = self.x_host.to(ctx.device, non_blocking=True)
         run.set_input(x_dev)
         run.run()
         ok_f, worst_f = compare_outputs(ctx, run, 0, list(range(1, len(feas) + 1)), self.tol)
         mark("forward")
-        for join in joins:
-            main.wait_event(join)
-        if ncf:
+        for join in att["joins"]:
+            ctx.stream.wait_event(join)
+        if feas:
+            idx = prep["idx"]
             T.index_copy_(0, idx, tp.totals)
             ok.index_copy_(0, idx, ok_f)
             worst.index_copy_(0, idx, worst_f)
         mark("fitness")
-        R, mean = reward(lers, T, ok, self.t_star, self.budget, self.eps)
+        R, mean = reward(att["lers"], T, ok, self.t_star, self.budget, self.eps)
         mark("reward")
-        return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": ntok0, "trace": tp, "events": ev,
-                "feasible": prep["feasible"], "lers": lers}
+        return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": att["ntok"], "trace": tp,
+                "events": ev if ev is not None else {}, "feasible": prep["feasible"], "lers": att["lers"]}
 
     def collect(self, out: dict) -> np.ndarray:
         rec = np.zeros(len(out["feasible"]), dtype=RECORD_DTYPE)
@@ -288,12 +312,18 @@ class PopulationEvaluator:
                     nxt += 1
                 wait += time.perf_counter() - t0
                 prep = self.prepare_encoded(plans[lo:hi], [got.pop(c) for c in range(lo, hi)], memo=memo,
-                                            first_seen=first_seen)
+                                            first_seen=first_seen, link=False)
                 prep["host_ms"]["wait_workers"] = 1e3 * wait
                 wait = 0.0
+                # the trace + attacker stage starts on the device while the host
+                # links the forward plans
                 t1 = time.perf_counter()
-                jobs.append((prep, self.run(prep, cold_schedules=False)))
-                prep["host_ms"]["launch"] = 1e3 * (time.perf_counter() - t1)
+                att = self.run_attack(prep)
+                t2 = time.perf_counter()
+                self.link_forward(prep)
+                t3 = time.perf_counter()
+                jobs.append((prep, self.run_forward(prep, att)))
+                prep["host_ms"]["launch"] = 1e3 * (t2 - t1 + time.perf_counter() - t3)
         else:
             for lo, hi in bounds:
                 prep = self.prepare(plans[lo:hi], memo=memo, first_seen=first_seen)
