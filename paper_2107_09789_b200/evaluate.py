@@ -135,6 +135,7 @@ class PopulationEvaluator:
                 cands.append(Candidate(plan, None, None, err))
                 continue
             fp, ct, new = payload
+            ct.expand(self.prefs.sig_table)
             if new:
                 self.prefs.adopt(c, new)
             feas.append(len(cands))
@@ -299,7 +300,7 @@ class PopulationEvaluator:
             workers = default_workers() if os.environ.get("TOBF_HOST_WORKERS", "") != "0" else 0
         if workers and len(plans) > 1:
             self._ensure_pool(workers)
-            per_job = 2
+            per_job = 1  # 32 candidates over 14 workers: at most 3 each (2-candidate jobs: 4)
             handles = self.pool.submit(plans, per_job=per_job)
             got: dict[int, tuple] = {}
             nxt = 0  # next handle to receive

@@ -363,6 +363,26 @@ class ForwardPlan:
     gemm_weight_bytes: int = 0          # conv/linear weights, fp32, once
 
 
+def _plan_getstate(self) -> dict:
+    """Pickle the descriptor tables as raw bytes: numpy rebuilds nested
+    structured dtypes field by field on unpickling (~20 us per array), which
+    the parent pays for every candidate a host worker sends."""
+    st = dict(self.__dict__)
+    st["conv"], st["ew"] = self.conv.tobytes(), self.ew.tobytes()
+    return st
+
+
+def _plan_setstate(self, st: dict) -> None:
+    st = dict(st)
+    st["conv"] = np.frombuffer(st["conv"], dtype=CONV_DTYPE).copy()
+    st["ew"] = np.frombuffer(st["ew"], dtype=EW_DTYPE).copy()
+    self.__dict__.update(st)
+
+
+ForwardPlan.__getstate__ = _plan_getstate
+ForwardPlan.__setstate__ = _plan_setstate
+
+
 def _gemm_geom(lw: Lowered, op: Op, s_in: TensorShape):
     n = lw.graph.nodes[op.node]
     j = op.j or n.attrs["j"]

@@ -84,6 +84,7 @@ class ParentRefs(ArrayRefs):
         self.vanilla = {("v", nid): _root(n.weights) for nid, n in vanilla.nodes.items()
                         if isinstance(n.weights, np.ndarray)}
         self.new: dict[tuple, np.ndarray] = {}
+        self.sig_table: dict[int, tuple] = {}  # digest -> schedule signature (workers send each once)
 
     def root(self, key) -> np.ndarray:
         tag = key[0]
@@ -115,6 +116,7 @@ def _worker_init(vanilla: Graph, reps: int, pname: str) -> None:
     _W["pname"] = pname
     _W["roots"] = {id(_root(n.weights)): ("v", nid) for nid, n in vanilla.nodes.items()
                    if isinstance(n.weights, np.ndarray)}
+    _W["sent_sigs"] = set()  # signature digests this worker has sent to its parent
 
 
 # knob weights as device-packed gathers (derived.py); TOBF_EAGER_KNOBS=1 ships
@@ -123,7 +125,7 @@ LAZY_KNOBS = os.environ.get("TOBF_EAGER_KNOBS", "") != "1"
 
 
 def encode_candidate(cand: int, plan: ObfuscationPlan, vanilla: Graph, vanilla_analysis, reps: int, pname: str,
-                     roots: dict):
+                     roots: dict, sent_sigs: set | None = None):
     """(cand, error, payload): payload = (ForwardPlan, CandidateTrace, new arrays)."""
     try:
         g, d, ana = apply_plan_analyzed(vanilla, plan, vanilla_analysis, lazy=LAZY_KNOBS)
@@ -132,12 +134,14 @@ def encode_candidate(cand: int, plan: ObfuscationPlan, vanilla: Graph, vanilla_a
     refs = WorkerRefs(roots, cand)
     fp = plan_forward(lower(g, ana), reps, refs)
     ct, _, _ = trace_records(g, d.fusion_limits, d.schedule_strategies, pname, ana)
+    if sent_sigs is not None:
+        ct = ct.compact(sent_sigs)
     return cand, None, (fp, ct, refs.new)
 
 
 def _worker_job(job: list[tuple[int, ObfuscationPlan]]) -> list:
-    return [encode_candidate(c, p, _W["vanilla"], _W["analysis"], _W["reps"], _W["pname"], _W["roots"])
-            for c, p in job]
+    return [encode_candidate(c, p, _W["vanilla"], _W["analysis"], _W["reps"], _W["pname"], _W["roots"],
+                             _W["sent_sigs"]) for c, p in job]
 
 
 def _worker_main(rfd: int, wfd: int) -> None:

@@ -295,8 +295,38 @@ class CandidateTrace:
     each kernel's schedule signature (costmodel.py:251-256)."""
 
     recs: np.ndarray
-    sigs: list
+    sigs: list | None
     sig_keys: np.ndarray | None = None  # 64-bit content digest per signature (process-independent)
+    new_sigs: dict | None = None        # wire form: digest -> signature for digests not sent before
+
+    def __getstate__(self):
+        st = dict(self.__dict__)
+        st["recs"] = self.recs.tobytes()  # raw bytes: see executor._plan_getstate
+        return st
+
+    def __setstate__(self, st):
+        st = dict(st)
+        st["recs"] = np.frombuffer(st["recs"], dtype=KERN_DTYPE).copy()
+        self.__dict__.update(st)
+
+    def compact(self, sent: set) -> "CandidateTrace":
+        """Wire form for a host worker: the signature tuples are replaced by
+        their digests, plus the tuples of digests this worker has not sent
+        before (signatures repeat across a population)."""
+        new = {}
+        for k, sg in zip(self.sig_keys.tolist(), self.sigs):
+            if k not in sent:
+                sent.add(k)
+                new[k] = sg
+        return CandidateTrace(self.recs, None, self.sig_keys, new)
+
+    def expand(self, table: dict) -> "CandidateTrace":
+        """Parent side: fold the new signatures into ``table`` and rebuild the list."""
+        if self.sigs is None:
+            table.update(self.new_sigs or {})
+            self.sigs = [table[k] for k in self.sig_keys.tolist()]
+            self.new_sigs = None
+        return self
 
 
 _DIGESTS: dict[tuple, int] = {}

@@ -56,6 +56,9 @@ def test_pool_matches_in_process(population):
         for x, y in zip(a1, a2):
             assert np.array_equal(x, y)
         ref_ct, _, _ = trace_records(og, d.fusion_limits, d.schedule_strategies, "default", ana)
+        # workers send signature digests + only the tuples they have not sent before
+        assert ct.sigs is None and len(ct.new_sigs) <= len(set(ref_ct.sigs))
+        ct.expand(prefs.sig_table)
         assert np.array_equal(ct.recs, ref_ct.recs) and ct.sigs == ref_ct.sigs
 
 
