@@ -76,6 +76,7 @@ from .trace import (
     profile_kernel,
     profile_pipeline,
 )
+from .formats import GraphParseError, dump_graph, dump_plan, dump_trace, load_graph, load_plan, load_trace
 from .executor import equivalence_check, evaluate_equivalence, execute
 from .attacker import FitnessReport, Predictor, bagged_predictors, init_predictor, ler, levenshtein
 from .evaluate import Evaluator, PopulationEvaluator, fitness

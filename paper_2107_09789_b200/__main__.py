@@ -1,7 +1,14 @@
-"""Command-line GA driver (SURVEY §8(f)4; SPEC.md:572-607 search loop, :600 log).
+"""Command line (SURVEY §8(f)4; SPEC.md:609-659 cli_persistence, :572-607 GA loop).
 
     python -m paper_2107_09789_b200 ga --fixture resnet18 --mode sequence \
         --population 32 --generations 20 --out runs/rn18 [--resume]
+    python -m paper_2107_09789_b200 obfuscate --graph net.graph --budget 0.02 --out runs/net
+    python -m paper_2107_09789_b200 evaluate --graph net.graph [--plan p.plan] [--attackers a.npz]
+    python -m paper_2107_09789_b200 profile --graph net.graph [--plan p.plan] --case C --out t.trace
+    python -m paper_2107_09789_b200 train-attacker --n 2000 --out attackers.npz
+
+Graph, plan and trace files are the reference's formats (formats.py). Exit
+codes follow SPEC.md:659: 0 success, 1 usage, 2 data/model error.
 
 One GA generation per step: the population is evaluated on the GPU(s) by
 ``PopulationEvaluator`` (forward + verdict, trace, bagged attackers, Eq. 10)
@@ -29,12 +36,49 @@ from pathlib import Path
 import numpy as np
 
 
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):  # usage errors exit 1, not argparse's 2
+        self.print_usage(sys.stderr)
+        self.exit(1, f"{self.prog}: error: {message}\n")
+
+
+class DataError(Exception):
+    """Unreadable graph / plan / model file or an inapplicable plan: exit 2."""
+
+
 def _parse(argv):
-    ap = argparse.ArgumentParser(prog="python -m paper_2107_09789_b200")
-    sub = ap.add_subparsers(dest="cmd", required=True)
+    ap = _Parser(prog="python -m paper_2107_09789_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True, parser_class=_Parser)
     g = sub.add_parser("ga", help="run the obfuscation GA on a fixture network")
+    o = sub.add_parser("obfuscate", help="run the GA on a graph file; write the obfuscated graph and plan")
     g.add_argument("--fixture", choices=("resnet18", "vgg16", "c1c2"), default="resnet18")
     g.add_argument("--size", type=int, default=None, help="input resolution (fixture default if omitted)")
+    o.add_argument("--graph", type=Path, required=True)
+    for g in (g, o):
+        _ga_args(g)
+    e = sub.add_parser("evaluate", help="attack a graph (or graph + plan): per-predictor LER, T/T*, reward")
+    p = sub.add_parser("profile", help="write the case-masked cost-model trace of a graph (or graph + plan)")
+    for x in (e, p):
+        x.add_argument("--graph", type=Path, required=True)
+        x.add_argument("--plan", type=Path, default=None)
+        x.add_argument("--profile", default="default")
+    e.add_argument("--attackers", type=Path, default=None)
+    e.add_argument("--budget", type=float, default=0.02)
+    e.add_argument("--trials", type=int, default=8)
+    e.add_argument("--seed", type=int, default=0)
+    p.add_argument("--case", choices=("A", "B", "C"), default="C")
+    p.add_argument("--labels", action="store_true")
+    p.add_argument("--out", type=Path, required=True)
+    t = sub.add_parser("train-attacker", help="train the bagged LSTM attackers on random architectures")
+    t.add_argument("--n", type=int, default=2000, help="random networks in the dataset (4:1 split)")
+    t.add_argument("--size", type=int, default=32, help="input resolution (32: CIFAR-like, 224: ImageNet-like)")
+    t.add_argument("--epochs", type=int, default=30)
+    t.add_argument("--seed", type=int, default=0)
+    t.add_argument("--out", type=Path, required=True)
+    return ap.parse_args(argv)
+
+
+def _ga_args(g):
     g.add_argument("--mode", choices=("sequence", "dimension"), default="sequence")
     g.add_argument("--population", type=int, default=32)
     g.add_argument("--generations", type=int, default=20)
@@ -46,13 +90,6 @@ def _parse(argv):
     g.add_argument("--resume", action="store_true")
     g.add_argument("--attackers", type=Path, default=None,
                    help="npz of trained predictors (train-attacker); default: seeded random-init")
-    t = sub.add_parser("train-attacker", help="train the bagged LSTM attackers on random architectures")
-    t.add_argument("--n", type=int, default=2000, help="random networks in the dataset (4:1 split)")
-    t.add_argument("--size", type=int, default=32, help="input resolution (32: CIFAR-like, 224: ImageNet-like)")
-    t.add_argument("--epochs", type=int, default=30)
-    t.add_argument("--seed", type=int, default=0)
-    t.add_argument("--out", type=Path, required=True)
-    return ap.parse_args(argv)
 
 
 def train_attacker_cli(args) -> int:
@@ -81,7 +118,7 @@ def run_ga_cli(args) -> int:
     from . import dist as tdist
     from . import fixtures, ga
     from .engine import device
-    from .evaluate import Evaluator, PopulationEvaluator
+    from .evaluate import PopulationEvaluator
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -90,8 +127,11 @@ def run_ga_cli(args) -> int:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device(local)
-    kw = {} if args.size is None else {"size": args.size}
-    vanilla = fixtures.FIXTURES[args.fixture](**kw)
+    if args.cmd == "obfuscate":
+        vanilla = _load_graph(args.graph)
+    else:
+        kw = {} if args.size is None else {"size": args.size}
+        vanilla = fixtures.FIXTURES[args.fixture](**kw)
     params = ga.GaParams(population=args.population, generations=args.generations, seed=args.seed)
     args.out.mkdir(parents=True, exist_ok=True)
     memo: dict = {}
@@ -105,10 +145,7 @@ def run_ga_cli(args) -> int:
         if (state.mode, same) != (args.mode, params):
             raise SystemExit(f"checkpoint {ck} is for {state.mode} {state.params}, not {args.mode} {params}")
         state.params = params  # --generations may extend the run
-    ev = Evaluator()
-    if args.attackers is not None:
-        from .attacker_train import load_predictors
-        ev = Evaluator(predictors=load_predictors(args.attackers))
+    ev = _evaluator(args.attackers)
     pe = PopulationEvaluator(vanilla, ev, budget=args.budget, trials=args.trials, seed=args.seed,
                              memo=memo, exchange=tdist.exchange_signatures if world > 1 else None)
 
@@ -145,20 +182,114 @@ def run_ga_cli(args) -> int:
     if rank == 0:
         out = {"best_reward": res.best_reward, "best_genome": [int(x) for x in res.best_genome],
                "best_plan": [e.__dict__ for e in res.best_plan.entries], "mode": args.mode,
-               "fixture": args.fixture, "generations": params.generations, "population": params.population}
+               "source": str(args.graph) if args.cmd == "obfuscate" else args.fixture,
+               "generations": params.generations, "population": params.population}
+        if args.cmd == "obfuscate":
+            from .formats import dump_graph, dump_plan
+            from .knobs import apply_plan
+            obf, _ = apply_plan(vanilla, res.best_plan)
+            dump_plan(res.best_plan, args.out / "best.plan")
+            dump_graph(obf, args.out / "obfuscated.graph")
+            rep = pe.evaluate([res.best_plan]).reports[0] if world == 1 else None
+            if rep is not None:
+                out["report"] = _report_json(rep, args.budget)
+                print(json.dumps({"mean_ler": rep.mean_metric, "overhead": out["report"]["overhead"]}), flush=True)
         (args.out / "result.json").write_text(json.dumps(out, indent=1) + "\n")
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+def _load_graph(path: Path):
+    from .formats import GraphParseError, load_graph
+    try:
+        return load_graph(path)
+    except (OSError, GraphParseError) as e:
+        raise DataError(str(e)) from e
+
+
+def _load_plan(path: Path | None, graph):
+    from .formats import load_plan
+    from .knobs import identity_plan
+    if path is None:
+        return identity_plan(graph)
+    try:
+        return load_plan(path)
+    except (OSError, ValueError, TypeError) as e:
+        raise DataError(f"{path}: {e}") from e
+
+
+def _evaluator(attackers: Path | None):
+    from .evaluate import Evaluator
+    if attackers is None:
+        return Evaluator()
+    from .attacker_train import load_predictors
+    try:
+        return Evaluator(predictors=load_predictors(attackers))
+    except (OSError, KeyError, ValueError) as e:
+        raise DataError(f"attacker models {attackers}: {e}") from e
+
+
+def _report_json(rep, budget: float) -> dict:
+    return {"feasible": rep.feasible, "equivalent": rep.equivalent, "worst_rel": rep.worst_rel,
+            "latency": rep.latency, "clean_latency": rep.clean_latency,
+            "overhead": rep.latency / rep.clean_latency - 1.0 if rep.feasible else None, "budget": budget,
+            "lers": rep.metrics, "mean_ler": rep.mean_metric, "reward": rep.reward}
+
+
+def evaluate_cli(args) -> int:
+    """cmd_evaluate: the bagged attacker replayed against one
+    graph (the identity plan) or graph + plan."""
+    from .engine import device
+    from .evaluate import PopulationEvaluator
+    g = _load_graph(args.graph)
+    plan = _load_plan(args.plan, g)
+    ev = _evaluator(args.attackers)
+    device()
+    from .trace import BUILTIN_PROFILES
+    ev.profile = BUILTIN_PROFILES[args.profile]
+    pe = PopulationEvaluator(g, ev, budget=args.budget, trials=args.trials, seed=args.seed)
+    try:
+        rep = pe.evaluate([plan]).reports[0]
+    finally:
+        pe.close()
+    if not rep.feasible:
+        raise DataError(f"plan does not apply to {args.graph}")
+    print(json.dumps(_report_json(rep, args.budget)), flush=True)
+    return 0
+
+
+def profile_cli(args) -> int:
+    """cmd_profile: case-masked trace in the reference's
+    trace format, from the device cost model."""
+    from .engine import device
+    from .formats import dump_trace
+    from .knobs import TransformError, apply_plan
+    from .trace import BUILTIN_PROFILES, LeakageCase, profile_pipeline
+    g = _load_graph(args.graph)
+    lim = strat = None
+    if args.plan is not None:
+        try:
+            g, d = apply_plan(g, _load_plan(args.plan, g))
+        except TransformError as e:
+            raise DataError(str(e)) from e
+        lim, strat = d.fusion_limits, d.schedule_strategies
+    device()
+    t = profile_pipeline(g, LeakageCase(args.case), BUILTIN_PROFILES[args.profile], lim, strat)
+    dump_trace(t, args.out, include_labels=args.labels)
+    print(json.dumps({"out": str(args.out), "kernels": len(t.steps), "total_latency": t.total_latency}), flush=True)
+    return 0
+
+
 def main(argv=None) -> int:
     args = _parse(sys.argv[1:] if argv is None else argv)
-    if args.cmd == "ga":
-        return run_ga_cli(args)
-    if args.cmd == "train-attacker":
-        return train_attacker_cli(args)
-    return 2
+    cmds = {"ga": run_ga_cli, "obfuscate": run_ga_cli, "evaluate": evaluate_cli, "profile": profile_cli,
+            "train-attacker": train_attacker_cli}
+    try:
+        return cmds[args.cmd](args)
+    except DataError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
 
 
 if __name__ == "__main__":

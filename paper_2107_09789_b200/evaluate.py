@@ -350,10 +350,12 @@ class PopulationEvaluator:
         keys = list(evs)
         stage = {b: evs[a].elapsed_time(evs[b]) for a, b in zip(keys, keys[1:])}
         stage.update(prep["host_ms"])
+        lers = out["lers"].cpu().numpy()  # (predictors, candidates)
         reports = []
         for i, c in enumerate(prep["cands"]):
             r = rec[i]
-            reports.append(FitnessReport(c.plan, float(r["latency"]), self.t_star, [], float(r["mean_ler"]),
+            per = [float(v) for v in lers[:, i]] if c.graph is not None else []
+            reports.append(FitnessReport(c.plan, float(r["latency"]), self.t_star, per, float(r["mean_ler"]),
                                          float(r["reward"]), feasible=c.graph is not None,
                                          equivalent=bool(r["ok"]) if c.graph is not None else None,
                                          worst_rel=float(r["worst"]) if c.graph is not None else None))
