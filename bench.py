@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=1, help="cpu_baseline sample: rounds of one candidate per core")
-    ap.add_argument("--micro", type=lambda v: [int(x) for x in v.split(",")], default=[32],
-                    help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run)")
+    ap.add_argument("--micro", type=lambda v: v if v == "auto" else [int(x) for x in v.split(",")], default="auto",
+                    help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run); "
+                         "auto = evaluate.auto_micro")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
     ap.add_argument("--cfg4-pop", type=int, default=16, help="cfg4 (VGG-16 dimension) candidates per step; 0 = skip")
@@ -333,7 +334,7 @@ def main_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2107_09789_b200 import fixtures
     from paper_2107_09789_b200.engine import device
-    from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
+    from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator, auto_micro
 
     ctx = device(local)
     vanilla = fixtures.resnet18()
@@ -446,7 +447,7 @@ def main_ours(args):
                "h2d_bytes_per_step": int((ctx.h2d_bytes - h0) / args.steps) + x_bytes,
                "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms,
                "host_ms_per_step": {k: round(v / args.steps, 2) for k, v in host_ms.items()},
-               "micro_batch": args.micro, "host_workers": pe.pool.workers if pe.pool is not None else 0}
+               "micro_batch": list(auto_micro(P)) if args.micro == "auto" else args.micro, "host_workers": pe.pool.workers if pe.pool is not None else 0}
         pe.close()
 
     # ---- cpu baseline (rank 0, N == 1 only)

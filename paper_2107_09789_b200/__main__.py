@@ -85,7 +85,8 @@ def _ga_args(g):
     g.add_argument("--budget", type=float, default=0.02)
     g.add_argument("--trials", type=int, default=8)
     g.add_argument("--seed", type=int, default=0)
-    g.add_argument("--micro", type=int, default=32, help="micro-batch size of the evaluator")
+    g.add_argument("--micro", type=lambda v: v if v == "auto" else int(v), default="auto",
+                   help="micro-batch size of the evaluator (auto: evaluate.auto_micro)")
     g.add_argument("--out", type=Path, required=True)
     g.add_argument("--resume", action="store_true")
     g.add_argument("--attackers", type=Path, default=None,

@@ -7,6 +7,7 @@ without a CUDA device or the native library, :func:`device` raises.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 import weakref
@@ -15,6 +16,13 @@ import numpy as np
 import torch
 
 from . import _native
+
+
+_TORCH_DTYPE = {np.dtype(k): v for k, v in ((np.float32, torch.float32), (np.float64, torch.float64),
+                                               (np.int32, torch.int32), (np.int64, torch.int64),
+                                               (np.uint8, torch.uint8), (np.int8, torch.int8),
+                                               (np.int16, torch.int16), (np.uint64, torch.uint64),
+                                               (np.uint32, torch.uint32), (np.bool_, torch.bool))}
 
 
 class DeviceUnavailable(RuntimeError):
@@ -69,18 +77,49 @@ class DeviceContext:
         _native.check(rc, what)
 
     # -- host arrays -> device ----------------------------------------------
+    RING_BYTES = 64 << 20
+
+    def _staged(self, raw: np.ndarray) -> torch.Tensor:
+        """Stream-ordered H2D of ``raw`` (uint8) through a pinned staging ring
+        allocated once: no per-upload page pinning (a cudaHostAlloc can stall
+        the host behind queued device work) and no pageable copy. A ring
+        region is rewritten only after the copy that last read it completed."""
+        n = raw.nbytes
+        self.h2d_bytes += n
+        if n > self.RING_BYTES // 4:
+            return torch.from_numpy(raw.copy()).pin_memory().to(self.device, non_blocking=True)
+        ring = self.__dict__.get("_ring")
+        if ring is None:
+            ring = self._ring = torch.empty(self.RING_BYTES, dtype=torch.uint8, pin_memory=True)
+            self._ring_np, self._ring_off, self._ring_busy = ring.numpy(), 0, collections.deque()
+        lo = self._ring_off if self._ring_off + n <= self.RING_BYTES else 0
+        hi = lo + n
+        busy = self._ring_busy
+        while busy and busy[0][2].query():
+            busy.popleft()
+        for blo, bhi, ev in busy:
+            if blo < hi and lo < bhi:
+                ev.synchronize()
+        self._ring_np[lo:hi] = raw
+        dev = torch.empty(n, dtype=torch.uint8, device=self.device)
+        dev.copy_(ring[lo:hi], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))  # the stream the copy was issued on
+        busy.append((lo, hi, ev))
+        self._ring_off = (hi + 255) & ~255
+        return dev
+
     def upload_bytes(self, buf: bytes | bytearray | memoryview) -> torch.Tensor:
-        host = torch.frombuffer(bytearray(buf), dtype=torch.uint8)
-        self.h2d_bytes += host.numel()
-        return host.pin_memory().to(self.device, non_blocking=True)
+        return self._staged(np.frombuffer(buf, dtype=np.uint8))
 
     def upload_array(self, a: np.ndarray) -> torch.Tensor:
-        """Pinned, stream-ordered H2D of a small host array (never a hidden
+        """Stream-ordered H2D of a small host array (never a hidden
         synchronising pageable copy)."""
         a = np.ascontiguousarray(a)
-        host = torch.from_numpy(a).pin_memory()
-        self.h2d_bytes += a.nbytes
-        return host.to(self.device, non_blocking=True)
+        td = _TORCH_DTYPE.get(a.dtype)
+        if td is None:
+            raise TypeError(f"upload_array: unsupported dtype {a.dtype}")
+        return self._staged(a.reshape(-1).view(np.uint8)).view(td).reshape(a.shape)
 
     def upload_struct_array(self, arr) -> torch.Tensor:
         return self.upload_bytes(memoryview(arr).cast("B"))

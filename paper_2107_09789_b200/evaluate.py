@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from .engine import cat_records, device
-from .executor import PopulationRun, compare_outputs, lower, plan_forward, trial_inputs
+from .executor import PlanTables, PopulationRun, compare_outputs, lower, plan_forward, trial_inputs
 from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
@@ -119,25 +119,40 @@ class PopulationEvaluator:
             self.vanilla_plan = plan_forward(self.lowered_vanilla, self.trials, self.prefs)
             self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers)
 
+    def receive(self, result: tuple, tables: PlanTables | None = None) -> None:
+        """Parent side of one worker result, as soon as it arrives: fold in its
+        new signatures and arrays, and (``tables``) resolve its forward plan's
+        weight images / BatchNorms / constants, launching their packing."""
+        c, err, payload = result
+        if err is not None:
+            return
+        fp, ct, new = payload
+        ct.expand(self.prefs.sig_table)
+        if new:
+            self.prefs.adopt(c, new)
+        if tables is not None:
+            tables.add([fp])
+
     def prepare_encoded(self, plans: list[ObfuscationPlan], results: list, memo: dict | None = None,
-                        first_seen: dict | None = None, link: bool = True) -> dict:
+                        first_seen: dict | None = None, link: bool = True, received: bool = False) -> dict:
         """Host half from worker results (hostpipe.encode_candidate tuples, in
         candidate order): resolve the schedule memo and stage the trace records,
         then (``link``) link the forward plans and stage them into HBM.
         ``link=False`` leaves the forward to ``link_forward``, so the caller
-        can start the trace + attacker stage on the device first."""
+        can start the trace + attacker stage on the device first.
+        ``received``: ``receive`` already ran on every result."""
         t0 = time.perf_counter()
         cands, feas, fps, cts = [], [], [], []
         base = results[0][0] if results else 0
-        for c, err, payload in results:
+        for r in results:
+            c, err, payload = r
             plan = plans[c - base]
             if err is not None:
                 cands.append(Candidate(plan, None, None, err))
                 continue
-            fp, ct, new = payload
-            ct.expand(self.prefs.sig_table)
-            if new:
-                self.prefs.adopt(c, new)
+            if not received:
+                self.receive(r)
+            fp, ct, _ = payload
             feas.append(len(cands))
             cands.append(Candidate(plan, None, None))
             fps.append(fp)
@@ -155,12 +170,15 @@ class PopulationEvaluator:
             self.link_forward(prep)
         return prep
 
-    def link_forward(self, prep: dict) -> None:
-        """Link the batch's forward plans (weights, arena, descriptor tables)."""
+    def link_forward(self, prep: dict, tables: PlanTables | None = None) -> None:
+        """Link the batch's forward plans (weights, arena, descriptor tables);
+        ``tables``: their requirement tables, already resolved (vanilla first)."""
         t0 = time.perf_counter()
         prep["run"] = PopulationRun(self.ctx, None, reps=self.trials, plans=[self.vanilla_plan] + prep.pop("fps"),
-                                    refs=self.prefs)
+                                    refs=self.prefs, tables=tables)
         prep["host_ms"]["lower_pack"] = 1e3 * (time.perf_counter() - t0)
+        for k, v in prep["run"].link_ms.items():
+            prep["host_ms"]["link_" + k] = v
 
     # ---------------------------------------------------------------- host
     def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None) -> dict:
@@ -279,7 +297,7 @@ class PopulationEvaluator:
         self.ctx.sync()
         return rec
 
-    def evaluate_records(self, plans: list[ObfuscationPlan], micro=32, memo: dict | None = None,
+    def evaluate_records(self, plans: list[ObfuscationPlan], micro="auto", memo: dict | None = None,
                          workers: int | None = None) -> np.ndarray:
         """Records for ``plans`` with host preparation of micro-batch i+1
         overlapping the device pipeline of micro-batch i (launches are async;
@@ -304,24 +322,34 @@ class PopulationEvaluator:
             handles = self.pool.submit(plans, per_job=per_job)
             got: dict[int, tuple] = {}
             nxt = 0  # next handle to receive
-            wait = 0.0
             for lo, hi in bounds:
-                t0 = time.perf_counter()
-                while nxt * per_job < hi:
-                    for r in self.pool.result(handles[nxt]):
-                        got[r[0]] = r
-                    nxt += 1
-                wait += time.perf_counter() - t0
+                # each result is folded in and its tables resolved while the
+                # workers are still preparing the later candidates
+                tables = PlanTables(self.ctx, self.prefs)
+                tables.add([self.vanilla_plan])
+                wait = busy = 0.0
+                c = lo
+                while c < hi:
+                    t0 = time.perf_counter()
+                    while c not in got:
+                        for r in self.pool.result(handles[nxt]):
+                            got[r[0]] = r
+                        nxt += 1
+                    t1 = time.perf_counter()
+                    self.receive(got[c], tables)
+                    c += 1
+                    busy += time.perf_counter() - t1
+                    wait += t1 - t0
                 prep = self.prepare_encoded(plans[lo:hi], [got.pop(c) for c in range(lo, hi)], memo=memo,
-                                            first_seen=first_seen, link=False)
+                                            first_seen=first_seen, link=False, received=True)
                 prep["host_ms"]["wait_workers"] = 1e3 * wait
-                wait = 0.0
+                prep["host_ms"]["receive"] = 1e3 * busy
                 # the trace + attacker stage starts on the device while the host
                 # links the forward plans
                 t1 = time.perf_counter()
                 att = self.run_attack(prep)
                 t2 = time.perf_counter()
-                self.link_forward(prep)
+                self.link_forward(prep, tables)
                 t3 = time.perf_counter()
                 jobs.append((prep, self.run_forward(prep, att)))
                 prep["host_ms"]["launch"] = 1e3 * (t2 - t1 + time.perf_counter() - t3)
@@ -362,10 +390,22 @@ class PopulationEvaluator:
         return PopulationResult(rec, self.t_star, stage, prep["run"].gemm_flops(), reports)
 
 
+def auto_micro(n: int) -> tuple[int, int]:
+    """``micro="auto"``: a quarter-size lead batch, then batches of 32. The
+    lead batch's forward starts while the host workers finish the rest
+    (measured on RN18, P = 32: (8, 24) 1391-1412 cand/s e2e vs 1210-1302 for
+    one batch of 32, profiles/r01_bench.jsonl)."""
+    return (max(1, min(n, 32) // 4), 32)
+
+
 def _micro_bounds(n: int, micro) -> list[tuple[int, int]]:
     """Micro-batch [lo, hi) ranges: ``micro`` is a size (every batch that big,
     the last one ragged) or a sequence of sizes (the last one repeats), e.g.
     (8, 24): a small first batch gets the device busy early."""
+    if isinstance(micro, str):
+        if micro != "auto":
+            raise ValueError(f"bad micro-batch sizes {micro!r}")
+        micro = auto_micro(n)
     sizes = [int(micro)] if isinstance(micro, (int, np.integer)) else [int(m) for m in micro]
     if not sizes or min(sizes) < 1:
         raise ValueError(f"bad micro-batch sizes {micro!r}")

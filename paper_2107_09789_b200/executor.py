@@ -23,6 +23,7 @@ multiple of 4 with zeros (16-B vector / bulk-copy alignment).
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -537,38 +538,49 @@ def splitk_workspace(ctx: DeviceContext, floats: int, counters: int):
     return ws, cnt
 
 
-class PopulationRun:
-    """Runs the forward of several graphs on the same stacked input.
+class PlanTables:
+    """Requirement tables of ForwardPlans resolved to device pointers, one
+    plan at a time: packed weight images (cached per weight view in the
+    context: every candidate reusing a vanilla layer, a branch slice of it or
+    a shared knob constant shares one image), folded BatchNorms, staged
+    constants. ``add`` may run while later plans are still being prepared
+    (evaluate_records resolves each candidate as its worker result arrives);
+    the pack / staging kernels it launches are stream-ordered before the
+    forward."""
 
-    Each graph is a ForwardPlan (built here, or in host worker processes);
-    linking resolves the plans' requirement tables — packed weight images
-    cached per weight view (every candidate that reuses a vanilla layer, a
-    branch slice of it or a shared knob constant shares one image), folded
-    BatchNorms, staged constants — lays the activation blocks out in one
-    arena reused across runs, rewrites every symbolic pointer with
-    vectorised numpy, groups rows into one launch per (level, BN) / level,
-    and uploads all descriptors in one H2D.
-    """
+    def __init__(self, ctx: DeviceContext, refs: ArrayRefs):
+        self.ctx, self.refs = ctx, refs
+        self.rows: list[tuple[list, list, list]] = []  # per plan: (wimg, affine, const) pointers
+        self._wimg_memo: dict = {}
+        self._const_memo: dict = {}
 
-    conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
-
-    def __init__(self, ctx: DeviceContext, lowered: list[Lowered] | None, reps: int,
-                 plans: list[ForwardPlan] | None = None, refs: ArrayRefs | None = None):
-        self.ctx = ctx
-        self.reps = reps
-        if plans is None:
-            refs = ArrayRefs()
-            plans = [plan_forward(lw, reps, refs) for lw in lowered]
-        self.plans, self.refs = plans, refs
-        ishape = plans[0].input_shape
+    def add(self, plans: list) -> None:
+        aff = self._affine_ptrs(list({r for p in plans for r in p.affine}))
+        wm, cm = self._wimg_memo, self._const_memo
         for p in plans:
-            if p.input_shape != ishape:
-                raise ShapeMismatch(-1, "population graphs disagree on the input shape")
-        self.input_shape = ishape
-        self.batch = ishape.batch * reps
-        self._link_all()
+            w = []
+            for e in p.wimg:
+                v = wm.get(e)
+                if v is None:
+                    v = wm[e] = self._wimg_ptr(e)
+                w.append(v)
+            c = []
+            for e in p.const:
+                v = cm.get(e)
+                if v is None:
+                    v = cm[e] = self._const_ptr(e)
+                c.append(v)
+            self.rows.append((w, [aff[e] for e in p.affine], c))
 
-    # -------------------------------------------------------------- tables
+    def table(self, i: int) -> tuple[np.ndarray, np.ndarray]:
+        """Column ``i`` (0 wimg, 1 affine, 2 const) of every plan concatenated
+        (+ a 0 sentinel) and each plan's offset into it."""
+        lens = np.array([len(r[i]) for r in self.rows], np.int64)
+        offsets = np.zeros(len(self.rows), np.int64)
+        np.cumsum(lens[:-1], out=offsets[1:])
+        flat = [v for r in self.rows for v in r[i]]
+        return np.array(flat + [0], np.uint64), offsets
+
     def _wimg_ptr(self, entry: tuple) -> int:
         ctx, lib = self.ctx, self.ctx.lib
         ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn = entry
@@ -679,8 +691,50 @@ class PopulationRun:
         cache[id(w)] = (w, dev)
         return dev.data_ptr()
 
+
+class PopulationRun:
+    """Runs the forward of several graphs on the same stacked input.
+
+    Each graph is a ForwardPlan (built here, or in host worker processes);
+    linking resolves the plans' requirement tables — packed weight images
+    cached per weight view (every candidate that reuses a vanilla layer, a
+    branch slice of it or a shared knob constant shares one image), folded
+    BatchNorms, staged constants — lays the activation blocks out in one
+    arena reused across runs, rewrites every symbolic pointer with
+    vectorised numpy, groups rows into one launch per (level, BN) / level,
+    and uploads all descriptors in one H2D.
+    """
+
+    conv_events = None  # optional list collecting (start, end) CUDA events per conv launch
+
+    def __init__(self, ctx: DeviceContext, lowered: list[Lowered] | None, reps: int,
+                 plans: list[ForwardPlan] | None = None, refs: ArrayRefs | None = None,
+                 tables: "PlanTables | None" = None):
+        """``tables``: the plans' requirement tables already resolved (built
+        incrementally while the plans arrive from host workers); resolved
+        here otherwise."""
+        self.ctx = ctx
+        self.reps = reps
+        if plans is None:
+            refs = ArrayRefs()
+            plans = [plan_forward(lw, reps, refs) for lw in lowered]
+        self.plans, self.refs = plans, refs
+        ishape = plans[0].input_shape
+        for p in plans:
+            if p.input_shape != ishape:
+                raise ShapeMismatch(-1, "population graphs disagree on the input shape")
+        self.input_shape = ishape
+        self.batch = ishape.batch * reps
+        if tables is None:
+            tables = PlanTables(ctx, refs)
+            tables.add(plans)
+        elif len(tables.rows) != len(plans):
+            raise ValueError(f"{len(tables.rows)} resolved tables for {len(plans)} plans")
+        self._link_all(tables)
+
     # -------------------------------------------------------------- link
-    def _link_all(self) -> None:
+    def _link_all(self, tables: "PlanTables") -> None:
+        ta = time.perf_counter()
         ctx, lib, plans = self.ctx, self.ctx.lib, self.plans
         s = self.input_shape
         in_floats = Arena.round(self.batch * s.height * s.width * _rup4(s.channels))
@@ -694,28 +748,9 @@ class PopulationRun:
             cur += p.arena_bytes
         self.arena.used = (cur - self.arena.base) // 4
         self.out_ptrs = [int(bases[i]) + p.out_off for i, p in enumerate(plans)]
-        # requirement tables -> device pointers (per plan, concatenated)
-        wimg_memo: dict = {}
-        const_memo: dict = {}
-        aff = self._affine_ptrs(list({r for p in plans for r in p.affine}))
-        tabs = {}
-        for sp, name in ((SP_WIMG, "wimg"), (SP_AFFINE, "affine"), (SP_CONST, "const")):
-            ptrs, offsets = [], np.zeros(len(plans), np.int64)
-            for i, p in enumerate(plans):
-                offsets[i] = len(ptrs)
-                for e in getattr(p, name):
-                    if sp == SP_WIMG:
-                        v = wimg_memo.get(e)
-                        if v is None:
-                            v = wimg_memo[e] = self._wimg_ptr(e)
-                    elif sp == SP_AFFINE:
-                        v = aff[e]
-                    else:
-                        v = const_memo.get(e)
-                        if v is None:
-                            v = const_memo[e] = self._const_ptr(e)
-                    ptrs.append(v)
-            tabs[sp] = (np.array(ptrs + [0], np.uint64), offsets)
+        t0 = time.perf_counter()
+        tabs = {sp: tables.table(i) for i, sp in enumerate((SP_WIMG, SP_AFFINE, SP_CONST))}
+        t1 = time.perf_counter()
         # rows of all plans, linked, grouped into launches
         conv = cat_records([p.conv for p in plans], CONV_DTYPE)
         ew = cat_records([p.ew for p in plans], EW_DTYPE)
@@ -738,6 +773,7 @@ class PopulationRun:
         eorder = np.argsort(ew_level, kind="stable")
         ew = ew[eorder]
         ekey = ew_level[eorder]
+        t2 = time.perf_counter()
         launches = []
         lo = 0
         ws_need = cnt_need = 0
@@ -769,6 +805,7 @@ class PopulationRun:
             launches.append((int(ekey[lo]), 1, "ew", lo, hi - lo, tot.value, 0))
             lo = hi
         launches.sort(key=lambda t: (t[0], t[1]))
+        t3 = time.perf_counter()
         conv_bytes = conv.tobytes()
         pad = (-len(conv_bytes)) % 256
         host = conv_bytes + bytes(pad) + ew.tobytes()
@@ -777,6 +814,8 @@ class PopulationRun:
         ew_base = base + len(conv_bytes) + pad
         self.launches = [(k, (base + lo * CONV_DTYPE.itemsize) if k == "conv" else (ew_base + lo * EW_DTYPE.itemsize),
                           n, tot, bn) for (_, _, k, lo, n, tot, bn) in launches]
+        self.link_ms = {"arena": 1e3 * (t0 - ta), "tables": 1e3 * (t1 - t0), "rows": 1e3 * (t2 - t1), "prepare": 1e3 * (t3 - t2),
+                        "upload": 1e3 * (time.perf_counter() - t3)}
 
     # -------------------------------------------------------------- run
     def set_input(self, x_nchw: torch.Tensor) -> None:

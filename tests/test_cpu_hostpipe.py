@@ -69,5 +69,8 @@ def test_micro_batch_bounds():
     assert _micro_bounds(32, (8, 24)) == [(0, 8), (8, 32)]
     assert _micro_bounds(30, [4, 12]) == [(0, 4), (4, 16), (16, 28), (28, 30)]
     assert _micro_bounds(0, 8) == []
+    assert _micro_bounds(32, "auto") == [(0, 8), (8, 32)]
+    assert _micro_bounds(3, "auto") == [(0, 1), (1, 3)]
+    assert _micro_bounds(80, "auto") == [(0, 8), (8, 40), (40, 72), (72, 80)]
     with pytest.raises(ValueError):
         _micro_bounds(4, 0)
