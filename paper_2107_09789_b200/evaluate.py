@@ -310,6 +310,7 @@ class PopulationEvaluator:
         if not plans:
             self.last_host_ms = {}
             return np.zeros(0, dtype=RECORD_DTYPE)
+        t_call = time.perf_counter()
         first_seen: dict = {}
         jobs = []
         bounds = _micro_bounds(len(plans), micro)
@@ -362,11 +363,15 @@ class PopulationEvaluator:
         t1 = time.perf_counter()
         recs = [self.collect(out) for _, out in jobs]
         jobs[0][0]["host_ms"]["collect"] = 1e3 * (time.perf_counter() - t1)
+        t2 = time.perf_counter()
         for prep, _ in jobs:
             if prep["trace"] is not None:
                 finish_trace(prep["trace"])
+        jobs[0][0]["host_ms"]["finish_trace"] = 1e3 * (time.perf_counter() - t2)
         self.last_host_ms = {k: sum(p["host_ms"].get(k, 0.0) for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
-        return cat_records(recs, RECORD_DTYPE)
+        out = cat_records(recs, RECORD_DTYPE)
+        self.last_host_ms["total"] = 1e3 * (time.perf_counter() - t_call)
+        return out
 
     def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
         prep = self.prepare(plans)

@@ -503,19 +503,26 @@ def finish_trace(tp: TracePlan) -> None:
     """Record newly searched schedules in the memo (first-seen) and attach the
     resolved schedules to the CompiledGraphs (one D2H)."""
     ctx = device()
-    host = torch.empty(tp.sigs.numel() + tp.kern.numel(), dtype=torch.uint8)
-    host[:tp.sigs.numel()].copy_(tp.sigs)
-    host[tp.sigs.numel():].copy_(tp.kern)
+    need_kern = any(cg is not None for cg in tp.compiled)
+    if not tp.pending and not need_kern:
+        return
+    ns = tp.sigs.numel()
+    host = torch.empty(ns + (tp.kern.numel() if need_kern else 0), dtype=torch.uint8)
+    host[:ns].copy_(tp.sigs)
+    if need_kern:
+        host[ns:].copy_(tp.kern)
     ctx.sync()
     raw = host.numpy().tobytes()
-    sigs = (N.KernDesc * max(tp.nsig, 1)).from_buffer_copy(raw[:tp.sigs.numel()])
-    kern = (N.KernDesc * max(tp.nk, 1)).from_buffer_copy(raw[tp.sigs.numel():])
+    sigs = (N.KernDesc * max(tp.nsig, 1)).from_buffer_copy(raw[:ns])
     for i, sig in tp.pending:
         if sig not in tp.memo:
             tp.memo[sig] = Schedule(tuple(sigs[i].ty), tuple(sigs[i].tx), sigs[i].unroll)
+    if not need_kern:
+        return  # records built out of process: no CompiledGraph to annotate
+    kern = (N.KernDesc * max(tp.nk, 1)).from_buffer_copy(raw[ns:])
     for cg, r in zip(tp.compiled, tp.offsets_host[:-1]):
         if cg is None:
-            continue  # records built out of process: no CompiledGraph to annotate
+            continue
         cg.schedules = [Schedule(tuple(kern[q].ty), tuple(kern[q].tx), kern[q].unroll)
                         for q in range(r, r + len(cg.kernels))]
 
