@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
     ap.add_argument("--cfg4-pop", type=int, default=16, help="cfg4 (VGG-16 dimension) candidates per step; 0 = skip")
+    ap.add_argument("--gen-pop", type=int, default=256,
+                    help="also measure one full generation of this many candidates on one GPU "
+                         "(north-star target: 256; separate process, N = 1 only); 0 = skip")
     return ap.parse_args()
 
 
@@ -263,6 +266,28 @@ def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
                            "peak": round(ffma_peak, 1), "peak_source": "derived 148 SM x 128 lanes x 2 x 1.965 GHz",
                            "frac": round(flops / (ms / 1e3) / 1e12 / ffma_peak, 4)}
     return out
+
+
+# ----------------------------------------------------------------------------- generation
+def workload_generation(args) -> dict | None:
+    """The north-star target workload: one full GA generation of
+    ``--gen-pop`` (256) ResNet-18 candidates on one GPU — the same step as the
+    headline at a larger population (bigger grouped launches; the host
+    workers prepare micro-batch i+1 while the device runs micro-batch i).
+    Run as a separate bench process so its arenas do not stack on this one's."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--pop", str(args.gen_pop), "--steps", "5", "--warmup", "3",
+           "--no-sweeps", "--no-cpu-baseline", "--cfg4-pop", "0", "--gen-pop", "0", "--seed", str(args.seed)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except (subprocess.TimeoutExpired, ValueError, IndexError) as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    e = d.get("e2e") or {}
+    return {"workload": f"resnet18_seq_generation, {args.gen_pop} candidates in one step (north-star target)",
+            "value": d["value"], "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
+            "e2e": {k: e.get(k) for k in ("value", "ms_per_step", "micro_batch", "h2d_bytes_per_step",
+                                          "d2h_bytes_per_step")},
+            "roofline_frac": d["roofline"]["frac"], "clocks": d["clocks"]}
 
 
 # ----------------------------------------------------------------------------- cfg4
@@ -476,6 +501,9 @@ def main_ours(args):
     cfg4 = None
     if rank == 0 and world == 1 and args.cfg4_pop > 0:
         cfg4 = workload_cfg4(args)
+    gen = None
+    if rank == 0 and world == 1 and args.gen_pop > 0 and args.gen_pop != P:
+        gen = workload_generation(args)
 
     if rank == 0:
         bf16 = peaks.get("bf16_tflops_sustained", 1387.4)
@@ -509,7 +537,7 @@ def main_ours(args):
                            "schedule_memo": "cold every step", "l2": "inputs > L2 (weights+activations ~6 GB/step)",
                            "parallelism": f"population sharded over {world} GPU(s), NCCL all-gather of records"},
                 "gpu_launches": launches, "stages_ms": stages, "roofline": roofline, "clocks": clk,
-                "e2e": e2e, "cpu_baseline": cpu, "kernels": sweeps, "workloads": {"cfg4": cfg4}}
+                "e2e": e2e, "cpu_baseline": cpu, "kernels": sweeps, "workloads": {"cfg4": cfg4, "generation": gen}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -71,6 +71,19 @@ def test_micro_batch_bounds():
     assert _micro_bounds(0, 8) == []
     assert _micro_bounds(32, "auto") == [(0, 8), (8, 32)]
     assert _micro_bounds(3, "auto") == [(0, 1), (1, 3)]
-    assert _micro_bounds(80, "auto") == [(0, 8), (8, 40), (40, 72), (72, 80)]
+    assert _micro_bounds(80, "auto") == [(0, 8), (8, 32), (32, 80)]
+    assert _micro_bounds(256, "auto") == [(0, 8), (8, 32), (32, 80), (80, 144), (144, 208), (208, 256)]
     with pytest.raises(ValueError):
         _micro_bounds(4, 0)
+
+
+def test_plan_wire_round_trip():
+    from paper_2107_09789_b200 import fixtures, ga
+    from paper_2107_09789_b200.hostpipe import plan_unwire, plan_wire
+    g = fixtures.c1c2(size=8)
+    for mode in ("sequence", "dimension"):
+        space = ga.search_space(g, mode)
+        rng = np.random.default_rng(1)
+        for x in ga.random_genomes(rng, ga.domain_sizes(mode, space), 5):
+            p = ga.decode_genome(g, mode, space, x)
+            assert plan_unwire(plan_wire(p)) == p
