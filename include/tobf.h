@@ -213,6 +213,22 @@ int tobf_levenshtein(const int8_t* pred, const int32_t* ntok, int32_t B, int32_t
 int tobf_fitness_eq10(const double* ler, int32_t npred, int32_t ncand, const double* T, const int32_t* feasible,
                       double Tstar, double budget, double eps, double* R, double* mean_ler, void* stream);
 
+/* Dimension attacker (no reference code): R bagged
+ * random-forest regressors (forest 2r predicts c, 2r+1 predicts j) on the
+ * feature rows (F fp64 per kernel step, compared as float32) of each
+ * candidate's Conv2D steps conv_rows[cand_off[c] .. cand_off[c+1]); forests
+ * are flat CART node tables (left < 0 = leaf), trees of forest f are
+ * tree_root[forest_off[f] .. forest_off[f+1]); a forest predicts
+ * max(1, floor(mean of its trees' leaf values, summed in tree order, + 0.5)).
+ * pred: (R, ncand, n_layers, 2) int32; der[r*ncand + c] = mean over layers of
+ * |c-c*|/c* + |j-j*|/j* against truth (n_layers x 2: c*, j*), or -1 when the
+ * candidate's conv step count != n_layers. */
+int tobf_forest_der(const double* feats, int32_t F, const int32_t* conv_rows, const int32_t* cand_off,
+                    int32_t ncand, int32_t n_layers, const int32_t* truth, const int32_t* node_feat,
+                    const double* node_thr, const int32_t* node_left, const int32_t* node_right,
+                    const double* node_value, const int32_t* tree_root, const int32_t* forest_off, int32_t R,
+                    int32_t* pred, double* der, void* stream);
+
 /* ------------------------------------------------------------------ misc */
 const char* tobf_last_error(void);
 int tobf_version(void);

@@ -74,7 +74,11 @@ def _parse(argv):
     t.add_argument("--size", type=int, default=32, help="input resolution (32: CIFAR-like, 224: ImageNet-like)")
     t.add_argument("--epochs", type=int, default=30)
     t.add_argument("--seed", type=int, default=0)
+    t.add_argument("--dimension", action="store_true",
+                   help="train the dimension attacker (bagged RF (c, j) regressors, 30/50/100/200 trees) instead")
     t.add_argument("--out", type=Path, required=True)
+    e.add_argument("--dim-attackers", type=Path, default=None,
+                   help="npz of dimension regressors (train-attacker --dimension): dimension plans score DER")
     return ap.parse_args(argv)
 
 
@@ -91,14 +95,22 @@ def _ga_args(g):
     g.add_argument("--resume", action="store_true")
     g.add_argument("--attackers", type=Path, default=None,
                    help="npz of trained predictors (train-attacker); default: seeded random-init")
+    g.add_argument("--dim-attackers", type=Path, default=None,
+                   help="npz of dimension regressors (train-attacker --dimension): dimension mode maximises DER")
 
 
 def train_attacker_cli(args) -> int:
-    from .attacker_train import ArchGenConfig, save_predictors, train_bagged
+    from .attacker_train import ArchGenConfig, build_dataset, save_predictors, train_bagged
     from .engine import device
     device()
     classes = 1000 if args.size >= 224 else 10
     cfg = ArchGenConfig(input_shape=(1, 3, args.size, args.size), num_classes=classes, seed=args.seed)
+    if args.dimension:
+        from .dimattack import save_dim_regressors, train_dim_regressors
+        regs, ders = train_dim_regressors(build_dataset(args.n, cfg), seed=args.seed)
+        save_dim_regressors(args.out, regs)
+        print(json.dumps({"out": str(args.out), "trees": [r.trees for r in regs], "val_der": ders}), flush=True)
+        return 0
     preds, lers = train_bagged(args.n, cfg, epochs=args.epochs, seed=args.seed)
     save_predictors(args.out, preds)
     print(json.dumps({"out": str(args.out), "hiddens": [p.hidden for p in preds], "val_ler": lers}), flush=True)
@@ -146,7 +158,7 @@ def run_ga_cli(args) -> int:
         if (state.mode, same) != (args.mode, params):
             raise SystemExit(f"checkpoint {ck} is for {state.mode} {state.params}, not {args.mode} {params}")
         state.params = params  # --generations may extend the run
-    ev = _evaluator(args.attackers)
+    ev = _evaluator(args.attackers, args.dim_attackers)
     pe = PopulationEvaluator(vanilla, ev, budget=args.budget, trials=args.trials, seed=args.seed,
                              memo=memo, exchange=tdist.exchange_signatures if world > 1 else None)
 
@@ -220,15 +232,19 @@ def _load_plan(path: Path | None, graph):
         raise DataError(f"{path}: {e}") from e
 
 
-def _evaluator(attackers: Path | None):
+def _evaluator(attackers: Path | None, dim_attackers: Path | None = None):
     from .evaluate import Evaluator
-    if attackers is None:
-        return Evaluator()
-    from .attacker_train import load_predictors
+    ev = Evaluator()
     try:
-        return Evaluator(predictors=load_predictors(attackers))
+        if attackers is not None:
+            from .attacker_train import load_predictors
+            ev.predictors = load_predictors(attackers)
+        if dim_attackers is not None:
+            from .dimattack import load_dim_regressors
+            ev.dim_regressors = load_dim_regressors(dim_attackers)
     except (OSError, KeyError, ValueError) as e:
-        raise DataError(f"attacker models {attackers}: {e}") from e
+        raise DataError(f"attacker models: {e}") from e
+    return ev
 
 
 def _report_json(rep, budget: float) -> dict:
@@ -245,7 +261,7 @@ def evaluate_cli(args) -> int:
     from .evaluate import PopulationEvaluator
     g = _load_graph(args.graph)
     plan = _load_plan(args.plan, g)
-    ev = _evaluator(args.attackers)
+    ev = _evaluator(args.attackers, args.dim_attackers)
     device()
     from .trace import BUILTIN_PROFILES
     ev.profile = BUILTIN_PROFILES[args.profile]

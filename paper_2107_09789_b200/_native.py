@@ -107,6 +107,8 @@ SIGNATURES = {
     "tobf_lstm_ctc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "tobf_levenshtein": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
     "tobf_fitness_eq10": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _f64, _f64, _f64, _vp, _vp, _vp]),
+    "tobf_forest_der": (C.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                  _vp, _vp, _vp]),
     "tobf_last_error": (C.c_char_p, []),
     "tobf_version": (C.c_int, []),
     "tobf_check_fault": (C.c_int, [_vp]),

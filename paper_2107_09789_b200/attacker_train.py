@@ -40,7 +40,7 @@ import torch
 
 from .attacker import NUM_CLASSES, Predictor, _bf16_round, encode_labels
 from .fixtures import _Builder
-from .ir import Graph, TensorShape, label_sequence, shape_map, validate
+from .ir import Graph, OperatorKind as K, TensorShape, label_sequence, shape_map, validate
 
 
 @dataclass
@@ -113,6 +113,7 @@ class TraceDataset:
     labels: list            # n arrays of int8 label codes (L*)
     graphs: list
     step_labels: np.ndarray | None = None  # (rows,) int8: each kernel anchor's code, 0 = not complex
+    step_cj: np.ndarray | None = None      # (rows, 2) int32: a Conv2D anchor's (c, j), else 0 (dimension attacker)
 
 
 def build_dataset(n: int, config: ArchGenConfig, profile=None, start: int = 0) -> TraceDataset:
@@ -125,9 +126,11 @@ def build_dataset(n: int, config: ArchGenConfig, profile=None, start: int = 0) -
     feats = pt.feats.cpu().numpy()[: int(pt.offsets_host[-1])]
     labels = [encode_labels(label_sequence(g)) for g in graphs]
     from .attacker import LABEL_CODES
-    steps = np.array([LABEL_CODES.get(g.nodes[k.anchor].kind, 0) for g, cg in zip(graphs, pt.compiled)
-                      for k in cg.kernels], dtype=np.int8)
-    return TraceDataset(feats, pt.offsets_host.astype(np.int32), labels, graphs, steps)
+    anchors = [g.nodes[k.anchor] for g, cg in zip(graphs, pt.compiled) for k in cg.kernels]
+    steps = np.array([LABEL_CODES.get(a.kind, 0) for a in anchors], dtype=np.int8)
+    cj = np.array([(a.attrs["c"], a.attrs["j"]) if a.kind is K.Conv2D else (0, 0) for a in anchors],
+                  dtype=np.int32).reshape(-1, 2)
+    return TraceDataset(feats, pt.offsets_host.astype(np.int32), labels, graphs, steps, cj)
 
 
 @dataclass

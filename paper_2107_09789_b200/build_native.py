@@ -23,7 +23,7 @@ BUILD = PKG.parent / "build" / "native"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}", f"-I{CSRC}"]
 # Units whose arithmetic must match a CPU restatement bit for bit.
-NO_FMA_UNITS = {"trace.cu", "fitness.cu"}
+NO_FMA_UNITS = {"trace.cu", "fitness.cu", "forest.cu"}
 
 
 def _nvcc() -> str:

@@ -46,6 +46,9 @@ class Evaluator:
 
     predictors: list[Predictor] = field(default_factory=bagged_predictors)
     case: LeakageCase = LeakageCase.C
+    #: dimension attacker (dimattack.DimRegressor list): when set, dimension-mode
+    #: plans are scored by bagged mean DER instead of LER
+    dim_regressors: list | None = None
     profile: DeviceProfile = BUILTIN_PROFILES["default"]
 
 
@@ -103,6 +106,10 @@ class PopulationEvaluator:
         # T* = latency of the unobfuscated graph under the same profile (Eq. 10)
         pt = trace_population([(vanilla, None, None)], self.ev.profile, self.memo)
         self.t_star = float(pt.totals.cpu()[0])
+        self.dim_truth = self._dim_forests = None
+        if self.ev.dim_regressors:
+            from .dimattack import conv_truth
+            self.dim_truth = conv_truth(vanilla, self.vanilla_analysis, self.ev.profile.name)
         self.pool = None          # hostpipe.HostPool, started on the first pooled batch
         self.prefs = None         # hostpipe.ParentRefs (weights of worker results)
         self.vanilla_plan = None
@@ -158,11 +165,12 @@ class PopulationEvaluator:
             fps.append(fp)
             cts.append(ct)
         t1 = time.perf_counter()
+        dim = self._dimension(plans)
         tp = prepare_trace_records(cts, self.ev.profile, self.memo if memo is None else memo,
-                                   exchange=self.exchange, first_seen=first_seen) if cts else None
+                                   exchange=self.exchange, first_seen=first_seen, conv_index=dim) if cts else None
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t2 = time.perf_counter()
-        prep = {"cands": cands, "feas": feas, "run": None, "fps": fps, "trace": tp, "idx": idx,
+        prep = {"cands": cands, "feas": feas, "run": None, "fps": fps, "trace": tp, "idx": idx, "dim": dim,
                 "feasible": [c.error is None for c in cands],
                 "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
                 "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 0.0, "trace_prep": 1e3 * (t2 - t1)}}
@@ -194,11 +202,12 @@ class PopulationEvaluator:
         t2 = time.perf_counter()
         items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies,
                   cands[i].analysis) for i in feas]
+        dim = self._dimension(plans)
         tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo,
-                           exchange=self.exchange, first_seen=first_seen) if items else None
+                           exchange=self.exchange, first_seen=first_seen, conv_index=dim) if items else None
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t3 = time.perf_counter()
-        return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx,
+        return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx, "dim": dim,
                 "feasible": [c.graph is not None for c in cands],
                 "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
                 "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
@@ -233,6 +242,8 @@ class PopulationEvaluator:
             mark("trace")
         n = len(cands)
         ncf = len(feas)
+        if prep.get("dim"):
+            return self._run_dim_attack(prep, n, ncf)
         att = {"lers": torch.zeros((len(self.ev.predictors), n), dtype=torch.float64, device=ctx.device),
                "ntok": torch.zeros(n, dtype=torch.int32, device=ctx.device), "joins": []}
         if ncf:
@@ -254,6 +265,38 @@ class PopulationEvaluator:
                 join = torch.cuda.Event()
                 join.record(s)
                 att["joins"].append(join)
+        return att
+
+    def _dimension(self, plans) -> bool:
+        """Dimension-mode batch scored by the DER attacker (Evaluator.dim_regressors)."""
+        return bool(self.ev.dim_regressors) and bool(plans) and plans[0].mode == "dimension"
+
+    def _run_dim_attack(self, prep: dict, n: int, ncf: int) -> dict:
+        """Bagged RF (c, j) regressors over every candidate's Conv2D trace steps
+        and DER vs the vanilla dimensions (dimattack.py), on a side stream; the
+        metric rows replace the LSTM LERs in Eq. 10."""
+        from .dimattack import DeviceForests, forest_der
+        ctx = self.ctx
+        if self._dim_forests is None:
+            self._dim_forests = DeviceForests(self.ev.dim_regressors)
+            self._dim_truth_dev = ctx.upload_array(self.dim_truth)
+        R = self._dim_forests.R
+        att = {"lers": torch.zeros((R, n), dtype=torch.float64, device=ctx.device),
+               "ntok": torch.zeros(n, dtype=torch.int32, device=ctx.device), "joins": []}
+        if ncf:
+            tp = prep["trace"]
+            s = ctx.side_streams(1)[0]
+            fork = torch.cuda.Event()
+            fork.record(ctx.stream)
+            with torch.cuda.stream(s):
+                s.wait_event(fork)
+                _, d = forest_der(self._dim_forests, tp.feats, tp.conv_rows, tp.conv_off, ncf, self._dim_truth_dev,
+                                  s.cuda_stream)
+                att["lers"].index_copy_(1, prep["idx"], d.clamp_min(0.0))  # unaligned (-1): metric 0
+                att["der"] = d
+            join = torch.cuda.Event()
+            join.record(s)
+            att["joins"].append(join)
         return att
 
     def run_forward(self, prep: dict, att: dict, x_dev: torch.Tensor | None = None, mark=None,

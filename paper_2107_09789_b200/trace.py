@@ -365,7 +365,7 @@ def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | N
 
 
 def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
-                  exchange=None, first_seen: dict | None = None) -> TracePlan:
+                  exchange=None, first_seen: dict | None = None, conv_index: bool = False) -> TracePlan:
     """Host half of compile_graph for many graphs: fuse, signatures, integer
     descriptors (one H2D for all). ``items``: (graph, fusion_limits,
     strategies[, ir.Analysis])."""
@@ -376,12 +376,12 @@ def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None 
         ct, kernels, shapes = trace_records(graph, limits, strategies, profile.name, ana)
         cts.append(ct)
         compiled.append(CompiledGraph(kernels=kernels, source=graph, shapes=shapes))
-    return prepare_trace_records(cts, profile, memo, exchange, first_seen, compiled)
+    return prepare_trace_records(cts, profile, memo, exchange, first_seen, compiled, conv_index)
 
 
 def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, memo: dict | None = None,
                           exchange=None, first_seen: dict | None = None,
-                          compiled: list[CompiledGraph] | None = None) -> TracePlan:
+                          compiled: list[CompiledGraph] | None = None, conv_index: bool = False) -> TracePlan:
     """Memo resolution and upload of a batch's kernel records.
 
     Signatures already in the memo resolve to their schedule; the others are
@@ -461,6 +461,11 @@ def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, mem
                    dev[:len(sig_blob)], nk, nsig, pending, offsets, offs, profile, memo)
     tp._blob = dev
     tp._sig_template = sig_blob
+    if conv_index:
+        # the Conv2D steps of every candidate, for the dimension attacker
+        rows = np.flatnonzero(kern["label"][:nk] == _LABEL_CODE[K.Conv2D]).astype(np.int32)
+        tp.conv_rows = ctx.upload_array(rows if len(rows) else np.zeros(1, np.int32))
+        tp.conv_off = ctx.upload_array(np.searchsorted(rows, offsets).astype(np.int32))
     return tp
 
 
