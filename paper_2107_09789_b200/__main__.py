@@ -63,6 +63,8 @@ def _parse(argv):
         x.add_argument("--plan", type=Path, default=None)
         x.add_argument("--profile", default="default")
     e.add_argument("--attackers", type=Path, default=None)
+    e.add_argument("--mode", choices=("sequence", "dimension"), default="sequence",
+                   help="mode of the identity plan used when --plan is omitted")
     e.add_argument("--budget", type=float, default=0.02)
     e.add_argument("--trials", type=int, default=8)
     e.add_argument("--seed", type=int, default=0)
@@ -221,11 +223,11 @@ def _load_graph(path: Path):
         raise DataError(str(e)) from e
 
 
-def _load_plan(path: Path | None, graph):
+def _load_plan(path: Path | None, graph, mode: str = "sequence"):
     from .formats import load_plan
     from .knobs import identity_plan
     if path is None:
-        return identity_plan(graph)
+        return identity_plan(graph, mode)
     try:
         return load_plan(path)
     except (OSError, ValueError, TypeError) as e:
@@ -260,7 +262,7 @@ def evaluate_cli(args) -> int:
     from .engine import device
     from .evaluate import PopulationEvaluator
     g = _load_graph(args.graph)
-    plan = _load_plan(args.plan, g)
+    plan = _load_plan(args.plan, g, args.mode)
     ev = _evaluator(args.attackers, args.dim_attackers)
     device()
     from .trace import BUILTIN_PROFILES
