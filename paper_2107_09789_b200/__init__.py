@@ -80,6 +80,7 @@ from .formats import GraphParseError, dump_graph, dump_plan, dump_trace, load_gr
 from .executor import equivalence_check, evaluate_equivalence, execute
 from .attacker import FitnessReport, Predictor, bagged_predictors, init_predictor, ler, levenshtein
 from .evaluate import Evaluator, PopulationEvaluator, fitness
+from .dimattack import DimRegressor, ZeroTruth, der, load_dim_regressors, train_dim_regressors
 from .ga import GaParams, GaResult, run_ga, search_space
 
 __version__ = "0.1.0"
