@@ -55,6 +55,7 @@ class DeviceContext:
         self.pinned_bytes = 0
         self.launches = 0      # libtobf kernel launches issued (bench evidence)
         self.h2d_bytes = 0     # host->device bytes staged through this context
+        self.wimg_bytes = 0    # bytes of packed weight images in wimg_cache
 
     def side_streams(self, n: int) -> list:
         """``n`` extra engine streams (created once, reused), at the highest
@@ -172,14 +173,24 @@ class DeviceContext:
         self.weight_cache[key] = (base, dev)
         self.weight_cache_bytes += dev.numel() * 4
 
+    WIMG_LIMIT = int(os.environ.get("TOBF_WIMG_CACHE_BYTES", str(32 << 30)))
+
+    def reset_wimg(self) -> None:
+        """Forget every packed weight image (their memory returns to torch's
+        stream-ordered caching allocator: reuse waits for the engine-stream
+        work already queued)."""
+        self.__dict__.pop("wimg_cache", None)
+        self.wimg_bytes = 0
+
     def clear_cache(self) -> None:
         """Drop every device copy of host arrays (weights, folded BatchNorm,
-        staged constants): the next run re-uploads everything it needs."""
+        staged constants, packed images): the next run re-uploads everything
+        it needs."""
         self.weight_cache.clear()
         self.weight_cache_bytes = 0
         self.__dict__.pop("affine_cache", None)
         self.__dict__.pop("const_cache", None)
-        self.__dict__.pop("wimg_cache", None)
+        self.reset_wimg()
 
     def sync(self) -> None:
         self.stream.synchronize()

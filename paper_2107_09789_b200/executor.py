@@ -550,6 +550,8 @@ class PlanTables:
 
     def __init__(self, ctx: DeviceContext, refs: ArrayRefs):
         self.ctx, self.refs = ctx, refs
+        if ctx.wimg_bytes > ctx.WIMG_LIMIT:
+            ctx.reset_wimg()  # a long GA run: bound the packed-image cache between batches
         self.rows: list[tuple[list, list, list]] = []  # per plan: (wimg, affine, const) pointers
         self._wimg_memo: dict = {}
         self._const_memo: dict = {}
@@ -600,6 +602,7 @@ class PlanTables:
             return hit.data_ptr()
         nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
+        ctx.wimg_bytes += nbytes
         ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn, bn,
                                         C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
         ctx.launches += 1
@@ -627,10 +630,13 @@ class PlanTables:
         if (len(mu), len(mv), len(mc), len(mn)) != (k1, k2, in_c, j):
             raise ShapeMismatch(-1, f"derived weight maps {(len(mu), len(mv), len(mc), len(mn))} "
                                     f"!= conv geometry {(k1, k2, in_c, j)}")
-        maps = ctx.upload_array(np.concatenate([mu, mv, mc, mn]).astype(np.int32))
-        scales = ctx.upload_array(np.concatenate([s_c, s_n]).astype(np.float32))
+        # maps (int32) and scales (float32) in one upload
+        imaps = np.concatenate([mu, mv, mc, mn]).astype(np.int32)
+        blob = ctx.upload_array(np.concatenate([imaps, np.concatenate([s_c, s_n]).astype(np.float32).view(np.int32)]))
+        maps, scales = blob, blob[len(imaps):]
         nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
+        ctx.wimg_bytes += nbytes
         ctx.check(lib.tobf_pack_weights_gather(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn,
                                                C.c_void_p(maps.data_ptr()), C.c_void_p(scales.data_ptr()), bn,
                                                C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack derived weights")
