@@ -427,18 +427,25 @@ def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, mem
                 first_seen[sig] = blob
         local_pending[sig] = blob
     pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
-    rows: dict[tuple, int] = {}
-    sig_recs = []
-    for sig, sch in hits.items():
-        rows[sig] = len(sig_recs)
-        sig_recs.append(np.array([(0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, tuple(sch.tile_y), tuple(sch.tile_x),
-                                   sch.unroll, 0, 1, 0, -1, 1)], dtype=KERN_DTYPE).tobytes())
+    rows: dict[tuple, int] = {sig: i for i, sig in enumerate(hits)}
+    # memoised signatures: resolved rows carrying their schedule (vectorised)
+    hit_recs = np.zeros(len(hits), KERN_DTYPE)
+    if hits:
+        sch = list(hits.values())
+        hit_recs["ty"] = [s.tile_y for s in sch]
+        hit_recs["tx"] = [s.tile_x for s in sch]
+        hit_recs["unroll"] = [s.unroll for s in sch]
+        hit_recs["has_shape"] = 1
+        hit_recs["sig_index"] = -1
+        hit_recs["resolved"] = 1
+    sig_recs = [hit_recs.tobytes()] if hits else []
     pending = []
+    nsig = len(hits)
     for sig, blob in pending_all.items():
-        rows[sig] = len(sig_recs)
-        pending.append((rows[sig], sig))
+        rows[sig] = nsig
+        pending.append((nsig, sig))
         sig_recs.append(blob)
-    nsig = len(sig_recs)
+        nsig += 1
     counts = [len(ct.sigs) for ct in cts]
     nk = sum(counts)
     if nk:
