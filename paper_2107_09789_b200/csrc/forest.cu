@@ -12,10 +12,11 @@
 // nearest positive integer. Features are compared as float32 (sklearn casts
 // X to float32 before the traversal).
 //
-// Latency-bound pointer chasing over a few hundred KB of node tables that sit
-// in L2: one thread per (regressor, candidate, conv layer, target) walks all
-// of its forest's trees sequentially (the fp64 sum order is part of the
-// contract); a second tiny kernel folds the layers into DER in layer order.
+// Latency-bound pointer chasing over a few MB of node tables that sit in L2:
+// one warp per (regressor, candidate, conv layer, target), its lanes walking
+// 32 trees at once; the leaf values are summed in tree order (the fp64 sum
+// order is part of the contract); a second tiny kernel folds the layers into
+// DER in layer order.
 #include <cmath>
 #include <cstdint>
 
@@ -29,8 +30,13 @@ __global__ void __launch_bounds__(128) forest_predict_kernel(
     const double* __restrict__ node_thr, const int32_t* __restrict__ node_left, const int32_t* __restrict__ node_right,
     const double* __restrict__ node_value, const int32_t* __restrict__ tree_root,
     const int32_t* __restrict__ forest_off, int32_t R, int32_t* __restrict__ pred) {
+  // one warp per (regressor, candidate, layer, target); the lanes walk 32
+  // trees at a time, then every lane sums the 32 leaf values in tree order
+  // (shuffles), so the fp64 sum order is the sequential one
+  const int lane = threadIdx.x & 31;
   const int64_t total = (int64_t)R * ncand * n_layers * 2;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += warps) {
     const int target = (int)(t & 1);  // 0: c, 1: j
     int64_t q = t >> 1;
     const int layer = (int)(q % n_layers);
@@ -39,23 +45,27 @@ __global__ void __launch_bounds__(128) forest_predict_kernel(
     const int r = (int)(q / ncand);
     const int32_t lo = cand_off[cand], hi = cand_off[cand + 1];
     if (hi - lo != n_layers) {  // conv steps do not line up with the vanilla layers
-      pred[t] = 0;
+      if (lane == 0) pred[t] = 0;
       continue;
     }
     const double* x = feats + (int64_t)conv_rows[lo + layer] * F;
     const int f = 2 * r + target;
     const int32_t t0 = forest_off[f], t1 = forest_off[f + 1];
     double sum = 0.0;
-    for (int32_t tr = t0; tr < t1; ++tr) {
-      int32_t n = tree_root[tr];
-      while (node_left[n] >= 0) {
-        const double v = (double)(float)__ldg(x + node_feat[n]);
-        n = v <= node_thr[n] ? node_left[n] : node_right[n];
+    for (int32_t base = t0; base < t1; base += 32) {
+      double leaf = 0.0;
+      if (base + lane < t1) {
+        int32_t n = tree_root[base + lane];
+        while (node_left[n] >= 0) {
+          const double v = (double)(float)__ldg(x + node_feat[n]);
+          n = v <= node_thr[n] ? node_left[n] : node_right[n];
+        }
+        leaf = node_value[n];
       }
-      sum += node_value[n];
+      const int cnt = min(32, (int)(t1 - base));
+      for (int k = 0; k < cnt; ++k) sum += __shfl_sync(0xffffffffu, leaf, k);
     }
-    const double mean = sum / (double)(t1 - t0);
-    pred[t] = (int32_t)fmax(1.0, floor(mean + 0.5));
+    if (lane == 0) pred[t] = (int32_t)fmax(1.0, floor(sum / (double)(t1 - t0) + 0.5));
   }
 }
 
@@ -88,8 +98,8 @@ extern "C" int tobf_forest_der(const double* feats, int32_t F, const int32_t* co
       !node_value || !tree_root || !forest_off || !pred || !der || F < 1 || n_layers < 1 || R < 1)
     return tobf_fail(TOBF_E_INVALID, "tobf_forest_der: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t threads = (int64_t)R * ncand * n_layers * 2;
-  const int grid = (int)std::min<int64_t>((threads + 127) / 128, 148 * 16);
+  const int64_t outputs = (int64_t)R * ncand * n_layers * 2;  // one warp each, 4 warps per CTA
+  const int grid = (int)std::min<int64_t>((outputs + 3) / 4, 148 * 16);
   forest_predict_kernel<<<grid, 128, 0, st>>>(feats, F, conv_rows, cand_off, ncand, n_layers, node_feat, node_thr,
                                               node_left, node_right, node_value, tree_root, forest_off, R, pred);
   der_kernel<<<(int)(((int64_t)R * ncand + 127) / 128), 128, 0, st>>>(pred, truth, ncand, n_layers, R, der);
