@@ -538,6 +538,15 @@ def splitk_workspace(ctx: DeviceContext, floats: int, counters: int):
     return ws, cnt
 
 
+def _runs(keys: np.ndarray) -> list[tuple[int, int]]:
+    """[lo, hi) runs of equal consecutive rows of a sorted (n, k) key array."""
+    n = len(keys)
+    if not n:
+        return []
+    b = (np.flatnonzero(np.any(keys[1:] != keys[:-1], axis=1)) + 1).tolist()
+    return list(zip([0] + b, b + [n]))
+
+
 class PlanTables:
     """Requirement tables of ForwardPlans resolved to device pointers, one
     plan at a time: packed weight images (cached per weight view in the
@@ -781,35 +790,28 @@ class PopulationRun:
         ekey = ew_level[eorder]
         t2 = time.perf_counter()
         launches = []
-        lo = 0
         ws_need = cnt_need = 0
-        while lo < len(conv):
-            hi = lo + 1
-            while hi < len(conv) and ckey[hi, 0] == ckey[lo, 0] and ckey[hi, 1] == ckey[lo, 1]:
-                hi += 1
-            tot, wsf, cnts = C.c_int64(), C.c_int64(), C.c_int64()
+        tot, wsf, cnts = C.c_int64(), C.c_int64(), C.c_int64()
+        conv_ptr = conv.ctypes.data
+        for lo, hi in _runs(ckey):
+            bn = int(ckey[lo, 1])
             # split-K for groups too small to fill the SMs; workspace offsets
             # now, one workspace shared by every (stream-ordered) conv launch
-            ctx.check(lib.tobf_conv_prepare_split(C.c_void_p(conv[lo:].ctypes.data), hi - lo, int(ckey[lo, 1]),
+            ctx.check(lib.tobf_conv_prepare_split(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
                                                   ctx.sms, SPLITK_MAX, None, None, C.byref(tot), C.byref(wsf),
                                                   C.byref(cnts)), "conv prepare")
             ws_need, cnt_need = max(ws_need, wsf.value), max(cnt_need, cnts.value)
-            launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, int(ckey[lo, 1])))
-            lo = hi
+            launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, bn))
         if ws_need:
             ws, cnt = splitk_workspace(ctx, ws_need, cnt_need)
             split = conv["ksplit"] > 1
             conv["ws"][split] += np.uint64(ws.data_ptr())
             conv["cnt"][split] += np.uint64(cnt.data_ptr())
-        lo = 0
-        while lo < len(ew):
-            hi = lo + 1
-            while hi < len(ew) and ekey[hi] == ekey[lo]:
-                hi += 1
-            tot = C.c_int64()
-            ctx.check(lib.tobf_ew_prepare(C.c_void_p(ew[lo:].ctypes.data), hi - lo, C.byref(tot)), "ew prepare")
+        ew_ptr = ew.ctypes.data
+        for lo, hi in _runs(ekey.reshape(-1, 1)):
+            ctx.check(lib.tobf_ew_prepare(C.c_void_p(ew_ptr + lo * EW_DTYPE.itemsize), hi - lo, C.byref(tot)),
+                      "ew prepare")
             launches.append((int(ekey[lo]), 1, "ew", lo, hi - lo, tot.value, 0))
-            lo = hi
         launches.sort(key=lambda t: (t[0], t[1]))
         t3 = time.perf_counter()
         conv_bytes = conv.tobytes()
