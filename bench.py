@@ -392,7 +392,7 @@ def main_ours(args):
         return float(t.item())
 
     # ---- value: resident inputs, device-timed
-    prep = pe.prepare(mine, memo={})
+    prep = pe.prepare(mine, memo={}, base=rank * P)
     x_dev = pe.x_host.to(ctx.device)
     for _ in range(args.warmup):
         gather(pe.run(prep, x_dev=x_dev, cold_schedules=True))
@@ -442,7 +442,7 @@ def main_ours(args):
         def e2e_step(s):
             ctx.clear_cache()
             shard = plans_e2e[s * per_step + rank * P: s * per_step + (rank + 1) * P]
-            rec = pe.evaluate_records(shard, micro=args.micro, memo={})
+            rec = pe.evaluate_records(shard, micro=args.micro, memo={}, base=rank * P)
             for k, v in pe.last_host_ms.items():
                 host_ms[k] = host_ms.get(k, 0.0) + v
             if world > 1:

@@ -119,11 +119,29 @@ def train_attacker_cli(args) -> int:
     return 0
 
 
-def _save(out: Path, state, memo: dict) -> None:
+def _save(out: Path, state, memo: dict, run: dict) -> None:
     tmp = out / "ckpt.pkl.tmp"
     with open(tmp, "wb") as f:
-        pickle.dump({"state": state, "memo": dict(memo)}, f)
+        pickle.dump({"state": state, "memo": dict(memo), "run": run}, f)
     os.replace(tmp, out / "ckpt.pkl")
+
+
+def _digest(path: Path | None) -> str | None:
+    if path is None:
+        return None
+    import hashlib
+    return hashlib.sha256(Path(path).read_bytes()).hexdigest()
+
+
+def _run_config(args) -> dict:
+    """Everything that fixes the reward scale of a run besides the GA params:
+    a resumed run must match it exactly (mixing budgets, trial counts or
+    attackers in one search would compare incomparable rewards)."""
+    return {"budget": args.budget, "trials": args.trials, "seed": args.seed,
+            "source": str(args.graph) if args.cmd == "obfuscate" else args.fixture,
+            "source_digest": _digest(args.graph) if args.cmd == "obfuscate" else None,
+            "size": getattr(args, "size", None),
+            "attackers": _digest(args.attackers), "dim_attackers": _digest(args.dim_attackers)}
 
 
 def run_ga_cli(args) -> int:
@@ -151,6 +169,7 @@ def run_ga_cli(args) -> int:
     args.out.mkdir(parents=True, exist_ok=True)
     memo: dict = {}
     state = None
+    run_cfg = _run_config(args)
     ck = args.out / "ckpt.pkl"
     if args.resume and ck.exists():
         with open(ck, "rb") as f:
@@ -159,22 +178,37 @@ def run_ga_cli(args) -> int:
         same = dataclasses.replace(state.params, generations=params.generations)
         if (state.mode, same) != (args.mode, params):
             raise SystemExit(f"checkpoint {ck} is for {state.mode} {state.params}, not {args.mode} {params}")
+        if blob.get("run") != run_cfg:
+            raise SystemExit(f"checkpoint {ck} was written with {blob.get('run')}, not {run_cfg}")
         state.params = params  # --generations may extend the run
     ev = _evaluator(args.attackers, args.dim_attackers)
     pe = PopulationEvaluator(vanilla, ev, budget=args.budget, trials=args.trials, seed=args.seed,
                              memo=memo, exchange=tdist.exchange_signatures if world > 1 else None)
 
+    last_plans: list = []
+
     def evaluate(plans):
-        mine = [plans[i] for i in tdist.shard(len(plans), world, rank)]
-        rec = pe.evaluate_records(mine, micro=args.micro, memo=memo)
+        last_plans[:] = [plans]
+        rng = tdist.shard(len(plans), world, rank)
+        mine = [plans[i] for i in rng]
+        rec = pe.evaluate_records(mine, micro=args.micro, memo=memo, base=rng.start)
         return tdist.gather_records(rec, len(plans)) if world > 1 else rec
 
     t0 = time.perf_counter()
 
     def checkpoint(st):
         if rank == 0:
-            _save(args.out, st, memo)
+            _save(args.out, st, memo, run_cfg)
             gen_rows = [r for r in st.log if r[0] == st.gen]
+            # one row per evaluated candidate: its genome, reward,
+            # mean attack metric, latency T and the overhead ratio T/T*
+            with open(args.out / "candidates.jsonl", "a") as f:
+                for g_, i, r, m, T in gen_rows:
+                    plan = last_plans[0][i] if last_plans and i < len(last_plans[0]) else None
+                    f.write(json.dumps({"generation": g_, "index": i, "reward": r, "mean_metric": m, "latency": T,
+                                        "overhead": T / pe.t_star,
+                                        "plan": [dataclasses.asdict(e) for e in plan.entries] if plan else None})
+                            + "\n")
             line = {"generation": st.gen, "best_reward": st.best_reward,
                     "generation_best": max(r[2] for r in gen_rows) if gen_rows else None,
                     "generation_mean": float(np.mean([r[2] for r in gen_rows])) if gen_rows else None,

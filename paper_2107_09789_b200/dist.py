@@ -7,14 +7,16 @@ GA candidates are independent: rank r evaluates the contiguous block
   * ``gather_records``  — all-gather of the fixed-size fitness records
     (R, mean LER, T, verdict) so every rank holds the whole generation;
   * ``broadcast_genomes`` — rank 0's next-generation genomes to all ranks;
-  * ``exchange_signatures`` — the schedule-memo first-seen exchange: the
-    reference memoises default schedules process-globally in candidate order
-    (costmodel.py:248-285). Each rank publishes the
-    signatures it has not memoised yet, with the kernel descriptor of its
-    first occurrence; every rank then adopts, per signature, the descriptor
-    of the globally first occurrence (rank order = candidate order), so the
-    searched schedules — and hence every trace — are bit-identical to a
-    single process evaluating the whole generation in order.
+  * ``exchange_signatures`` — the schedule-memo first-seen exchange, once
+    per shard evaluation: the reference memoises default schedules
+    process-globally in candidate order (costmodel.py:248-285, SURVEY App.
+    A-5). Each rank publishes, for its WHOLE shard (before any micro-batch
+    runs), the signatures it has not memoised yet with the global index of
+    the candidate they first occur in and that kernel's descriptor; every
+    rank adopts, per signature, the descriptor of the lowest global index,
+    searches the same union table and memoises all of it — so memos stay
+    identical across ranks and every trace is bit-identical to one process
+    evaluating the whole generation in order.
 """
 
 from __future__ import annotations
@@ -73,17 +75,24 @@ def broadcast_genomes(genomes: np.ndarray | None, shape: tuple[int, int]) -> np.
     return t.cpu().numpy()
 
 
-def exchange_signatures(local: list[tuple[tuple, bytes]]) -> dict[tuple, bytes]:
-    """``local``: this rank's unmemoised (signature, descriptor bytes) in its
-    first-seen order. Returns signature -> descriptor of the global first
-    occurrence, for every signature any rank reported."""
+def exchange_signatures(local: list[tuple[tuple, int, bytes]]) -> dict[tuple, bytes]:
+    """``local``: this rank's unmemoised (signature, global candidate index of
+    its first occurrence, descriptor bytes), from ``trace.shard_first_seen``.
+    Returns signature -> descriptor of the globally first occurrence (lowest
+    candidate index; rank, then position break ties), for every signature any
+    rank reported, in that global order. ONE collective per call: callers
+    make exactly one call per shard evaluation on every rank, whatever the
+    shard holds (trace.resolve_first_seen)."""
     ws, _ = world()
-    if ws == 1:
-        return dict(local)
-    gathered: list = [None] * ws
-    dist.all_gather_object(gathered, local)
-    first: dict[tuple, bytes] = {}
-    for part in gathered:  # rank order == candidate order (contiguous shards)
-        for sig, blob in part:
-            first.setdefault(sig, blob)
-    return first
+    parts = [local]
+    if ws > 1:
+        parts = [None] * ws
+        dist.all_gather_object(parts, local)
+    best: dict[tuple, tuple] = {}
+    for r, part in enumerate(parts):
+        for pos, (sig, gi, blob) in enumerate(part):
+            key = (int(gi), r, pos)
+            cur = best.get(sig)
+            if cur is None or key < cur[0]:
+                best[sig] = (key, blob)
+    return {sig: kb[1] for sig, kb in sorted(best.items(), key=lambda it: it[1][0])}

@@ -170,6 +170,12 @@ class DeviceContext:
         if self.weight_cache_bytes > self.weight_cache_limit:
             self.weight_cache.clear()
             self.weight_cache_bytes = 0
+            # packed images and staged constants are keyed by the DEVICE address
+            # of their source upload: once those uploads are dropped a new one
+            # can land at the same address, so the derived caches go too (runs
+            # already linked hold their own buffers: PlanTables.keep)
+            self.reset_wimg()
+            self.__dict__.pop("const_cache", None)
         self.weight_cache[key] = (base, dev)
         self.weight_cache_bytes += dev.numel() * 4
 

@@ -32,8 +32,7 @@ from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, deco
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
 from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,
-                    prepare_trace_records,
-                    run_trace, trace_population)
+                    prepare_trace_records, resolve_first_seen, run_trace, trace_population, trace_records)
 
 RECORD_DTYPE = np.dtype([("reward", "<f8"), ("mean_ler", "<f8"), ("latency", "<f8"), ("worst", "<f4"),
                          ("ok", "<i4"), ("feasible", "<i4"), ("ntok", "<i4")])
@@ -59,6 +58,15 @@ class Candidate:
     directives: object | None
     error: str | None = None
     analysis: object | None = None
+    trace: tuple | None = None   # (CandidateTrace, kernels, shapes) once computed
+
+
+def _candidate_traces(cands: list[Candidate], pname: str) -> None:
+    """Host trace records of every feasible candidate (computed once)."""
+    for c in cands:
+        if c.graph is not None and c.trace is None:
+            c.trace = trace_records(c.graph, c.directives.fusion_limits, c.directives.schedule_strategies, pname,
+                                    c.analysis)
 
 
 def build_candidates(vanilla: Graph, plans: list[ObfuscationPlan], vanilla_analysis=None) -> list[Candidate]:
@@ -141,13 +149,16 @@ class PopulationEvaluator:
             tables.add([fp])
 
     def prepare_encoded(self, plans: list[ObfuscationPlan], results: list, memo: dict | None = None,
-                        first_seen: dict | None = None, link: bool = True, received: bool = False) -> dict:
+                        first_seen: dict | None = None, link: bool = True, received: bool = False,
+                        extra: dict | None = None) -> dict:
         """Host half from worker results (hostpipe.encode_candidate tuples, in
         candidate order): resolve the schedule memo and stage the trace records,
         then (``link``) link the forward plans and stage them into HBM.
         ``link=False`` leaves the forward to ``link_forward``, so the caller
         can start the trace + attacker stage on the device first.
-        ``received``: ``receive`` already ran on every result."""
+        ``received``: ``receive`` already ran on every result. ``extra``:
+        signatures first seen on other ranks, searched and memoised here
+        (trace.prepare_trace_records)."""
         t0 = time.perf_counter()
         cands, feas, fps, cts = [], [], [], []
         base = results[0][0] if results else 0
@@ -167,7 +178,7 @@ class PopulationEvaluator:
         t1 = time.perf_counter()
         dim = self._dimension(plans)
         tp = prepare_trace_records(cts, self.ev.profile, self.memo if memo is None else memo,
-                                   exchange=self.exchange, first_seen=first_seen, conv_index=dim) if cts else None
+                                   first_seen=first_seen, conv_index=dim, extra=extra) if cts or extra else None
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t2 = time.perf_counter()
         prep = {"cands": cands, "feas": feas, "run": None, "fps": fps, "trace": tp, "idx": idx, "dim": dim,
@@ -189,29 +200,59 @@ class PopulationEvaluator:
             prep["host_ms"]["link_" + k] = v
 
     # ---------------------------------------------------------------- host
-    def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None) -> dict:
+    def prepare(self, plans: list[ObfuscationPlan], memo: dict | None = None, first_seen: dict | None = None,
+                extra: dict | None = None, cands: list[Candidate] | None = None, base: int | None = None,
+                shard: bool = True) -> dict:
         """Host half: apply_plan, lowering, weight upload + packing, trace
         descriptors, all staged into HBM. ``memo`` defaults to the
-        process-global schedule memo; pass {} for a cold schedule search."""
+        process-global schedule memo; pass {} for a cold schedule search.
+        ``shard``: ``plans`` are this rank's whole shard, so a sharded
+        evaluator resolves the first-seen memo across ranks here (one
+        collective); evaluate_records resolves it itself and passes
+        ``first_seen``/``extra`` per micro-batch. ``base``: global index of
+        ``plans[0]`` (default: contiguous shards in rank order)."""
+        memo = self.memo if memo is None else memo
         t0 = time.perf_counter()
-        cands = build_candidates(self.vanilla, plans, self.vanilla_analysis)
+        if cands is None:
+            cands = build_candidates(self.vanilla, plans, self.vanilla_analysis)
         t1 = time.perf_counter()
         feas = [i for i, c in enumerate(cands) if c.graph is not None]
         run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph, cands[i].analysis) for i in feas],
                             reps=self.trials)
         t2 = time.perf_counter()
+        if shard and self.exchange is not None:
+            _candidate_traces(cands, self.ev.profile.name)
+            glob = self._resolve([cands[i].trace[0] for i in feas], feas, base, memo)
+            first_seen = dict(glob) if first_seen is None else {**first_seen, **glob}
+            extra = glob
         items = [(cands[i].graph, cands[i].directives.fusion_limits, cands[i].directives.schedule_strategies,
-                  cands[i].analysis) for i in feas]
+                  cands[i].analysis, cands[i].trace) for i in feas]
         dim = self._dimension(plans)
-        tp = prepare_trace(items, self.ev.profile, self.memo if memo is None else memo,
-                           exchange=self.exchange, first_seen=first_seen, conv_index=dim) if items else None
+        tp = prepare_trace(items, self.ev.profile, memo, first_seen=first_seen, conv_index=dim,
+                           extra=extra) if items or extra else None
         idx = self.ctx.upload_array(np.asarray(feas, dtype=np.int64))
         t3 = time.perf_counter()
         return {"cands": cands, "feas": feas, "run": run, "trace": tp, "idx": idx, "dim": dim,
                 "feasible": [c.graph is not None for c in cands],
-                "t_max": int(np.diff(tp.offsets_host).max()) if tp else 1,
+                "t_max": int(np.diff(tp.offsets_host).max()) if tp and len(tp.offsets_host) > 1 else 1,
                 "host_ms": {"apply_plan": 1e3 * (t1 - t0), "lower_pack": 1e3 * (t2 - t1),
                             "trace_prep": 1e3 * (t3 - t2)}}
+
+    def _memoise_remote(self, glob: dict, memo: dict) -> None:
+        """An empty shard still searches and memoises the signatures the other
+        ranks first saw, so every rank's memo stays identical."""
+        if glob:
+            tp = prepare_trace_records([], self.ev.profile, memo, extra=glob)
+            run_trace(tp, profile=False)
+            finish_trace(tp)
+
+    def _resolve(self, cts: list, local_idx: list[int], base: int | None, memo: dict) -> dict:
+        """The shard's one first-seen memo exchange (trace.resolve_first_seen):
+        global candidate index = ``base`` + local index; without ``base`` every
+        candidate is tagged 0, so ranks order by rank then local first-seen
+        order — the global order for contiguous shards (dist.shard)."""
+        gidx = [(base + i) if base is not None else 0 for i in local_idx]
+        return resolve_first_seen(cts, gidx, memo, self.exchange)
 
     # ---------------------------------------------------------------- device
     def run(self, prep: dict, x_dev: torch.Tensor | None = None, timing: bool = False,
@@ -341,7 +382,7 @@ class PopulationEvaluator:
         return rec
 
     def evaluate_records(self, plans: list[ObfuscationPlan], micro="auto", memo: dict | None = None,
-                         workers: int | None = None) -> np.ndarray:
+                         workers: int | None = None, base: int | None = None) -> np.ndarray:
         """Records for ``plans`` with host preparation of micro-batch i+1
         overlapping the device pipeline of micro-batch i (launches are async;
         the only host waits are the final read-backs). With ``workers`` != 0
@@ -349,12 +390,24 @@ class PopulationEvaluator:
         the per-candidate host work runs in a process pool and the parent only
         links and launches. First-seen schedule semantics hold across
         micro-batches: a signature pending in several of them is searched
-        from its first occurrence's descriptor everywhere."""
+        from its first occurrence's descriptor everywhere.
+
+        Sharded (``exchange`` set): ``plans`` is this rank's whole shard and
+        ``base`` its global index. The first-seen memo is resolved across
+        ranks ONCE per call, before any micro-batch runs and whatever the
+        shard holds (empty, all infeasible, any split), so every rank makes
+        the same collective calls; the trace stage of the first micro-batch
+        then waits for the whole shard's host records."""
+        memo = self.memo if memo is None else memo
+        t_call = time.perf_counter()
+        sharded = self.exchange is not None
         if not plans:
             self.last_host_ms = {}
+            if sharded:
+                self._memoise_remote(self._resolve([], [], base, memo), memo)
             return np.zeros(0, dtype=RECORD_DTYPE)
-        t_call = time.perf_counter()
         first_seen: dict = {}
+        extra = None
         jobs = []
         bounds = _micro_bounds(len(plans), micro)
         if workers is None:
@@ -371,9 +424,11 @@ class PopulationEvaluator:
             sent = min(len(plans), 2 * self.pool.workers)
             got: dict[int, tuple] = {}
             nxt = 0  # next handle to receive
-            for lo, hi in bounds:
+
+            def receive_range(lo, hi):
                 # each result is folded in and its tables resolved while the
                 # workers are still preparing the later candidates
+                nonlocal sent, handles, nxt
                 tables = PlanTables(self.ctx, self.prefs)
                 tables.add([self.vanilla_plan])
                 wait = busy = 0.0
@@ -393,8 +448,19 @@ class PopulationEvaluator:
                     c += 1
                     busy += time.perf_counter() - t1
                     wait += t1 - t0
+                return tables, wait, busy
+
+            received = None
+            if sharded:
+                received = [receive_range(lo, hi) for lo, hi in bounds]
+                ok_idx = [c for c in range(len(plans)) if got[c][1] is None]
+                glob = self._resolve([got[c][2][1] for c in ok_idx], ok_idx, base, memo)
+                first_seen, extra = dict(glob), glob
+            for b, (lo, hi) in enumerate(bounds):
+                tables, wait, busy = received[b] if received is not None else receive_range(lo, hi)
                 prep = self.prepare_encoded(plans[lo:hi], [got.pop(c) for c in range(lo, hi)], memo=memo,
-                                            first_seen=first_seen, link=False, received=True)
+                                            first_seen=first_seen, link=False, received=True,
+                                            extra=extra if b == 0 else None)
                 prep["host_ms"]["wait_workers"] = 1e3 * wait
                 prep["host_ms"]["receive"] = 1e3 * busy
                 # the trace + attacker stage starts on the device while the host
@@ -407,8 +473,17 @@ class PopulationEvaluator:
                 jobs.append((prep, self.run_forward(prep, att)))
                 prep["host_ms"]["launch"] = 1e3 * (t2 - t1 + time.perf_counter() - t3)
         else:
-            for lo, hi in bounds:
-                prep = self.prepare(plans[lo:hi], memo=memo, first_seen=first_seen)
+            cands = None
+            if sharded:
+                cands = build_candidates(self.vanilla, plans, self.vanilla_analysis)
+                _candidate_traces(cands, self.ev.profile.name)
+                ok_idx = [c for c, cd in enumerate(cands) if cd.graph is not None]
+                glob = self._resolve([cands[c].trace[0] for c in ok_idx], ok_idx, base, memo)
+                first_seen, extra = dict(glob), glob
+            for b, (lo, hi) in enumerate(bounds):
+                prep = self.prepare(plans[lo:hi], memo=memo, first_seen=first_seen,
+                                    extra=extra if b == 0 else None,
+                                    cands=cands[lo:hi] if cands is not None else None, shard=False)
                 t1 = time.perf_counter()
                 jobs.append((prep, self.run(prep, cold_schedules=False)))
                 prep["host_ms"]["launch"] = 1e3 * (time.perf_counter() - t1)

@@ -562,6 +562,9 @@ class PlanTables:
         if ctx.wimg_bytes > ctx.WIMG_LIMIT:
             ctx.reset_wimg()  # a long GA run: bound the packed-image cache between batches
         self.rows: list[tuple[list, list, list]] = []  # per plan: (wimg, affine, const) pointers
+        # every device buffer a pointer was handed out for, held for the life of
+        # the run: a context cache may drop its entry (size bound) mid-batch
+        self.keep: list = []
         self._wimg_memo: dict = {}
         self._const_memo: dict = {}
 
@@ -608,6 +611,7 @@ class PlanTables:
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
+            self.keep.append(hit)
             return hit.data_ptr()
         nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
@@ -616,6 +620,7 @@ class PlanTables:
                                         C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
         ctx.launches += 1
         cache[key] = img
+        self.keep.append(img)
         return img.data_ptr()
 
     def _derived_wimg_ptr(self, w: DerivedWeight, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn) -> int:
@@ -634,6 +639,7 @@ class PlanTables:
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
+            self.keep.append(hit[0])
             return hit[0].data_ptr()
         mu, mv, mc, mn, s_c, s_n = w.maps()
         if (len(mu), len(mv), len(mc), len(mn)) != (k1, k2, in_c, j):
@@ -651,6 +657,7 @@ class PlanTables:
                                                C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack derived weights")
         ctx.launches += 1
         cache[key] = (img, maps, scales)  # maps stay alive until the (async) pack has run
+        self.keep.append(img)
         return img.data_ptr()
 
     def _affine_ptrs(self, refs_needed: list) -> dict:
@@ -664,6 +671,7 @@ class PlanTables:
             hit = cache.get(id(w))
             if hit is not None and hit[0] is w:
                 out[ref] = hit[2]
+                self.keep.append(hit[1])
             else:
                 misses[ref] = w
         if misses:
@@ -683,6 +691,7 @@ class PlanTables:
             for o, blk in zip(offs, blocks):
                 host[o:o + blk.size] = blk
             dev = self.ctx.upload_array(host)
+            self.keep.append(dev)
             if len(cache) > 200000:
                 cache.clear()
             for (ref, w), o in zip(misses.items(), offs):
@@ -697,6 +706,7 @@ class PlanTables:
         cache = self.ctx.__dict__.setdefault("const_cache", {})
         hit = cache.get(id(w))
         if hit is not None and hit[0] is w:
+            self.keep.append(hit[1])
             return hit[1].data_ptr()
         src_ptr, _ = self.ctx.cached_view(np.ascontiguousarray(w, dtype=np.float32))
         dev = torch.empty(b0 * h * w_ * cp, dtype=torch.float32, device=self.ctx.device)
@@ -704,6 +714,7 @@ class PlanTables:
                                                       w_, cp, C.c_void_p(self.ctx.sp)), "const staging")
         self.ctx.launches += 1
         cache[id(w)] = (w, dev)
+        self.keep.append(dev)
         return dev.data_ptr()
 
 
@@ -745,6 +756,7 @@ class PopulationRun:
             tables.add(plans)
         elif len(tables.rows) != len(plans):
             raise ValueError(f"{len(tables.rows)} resolved tables for {len(plans)} plans")
+        self._keep = tables.keep  # images / BatchNorms / constants this run's descriptors point at
         self._link_all(tables)
 
     # -------------------------------------------------------------- link

@@ -134,7 +134,7 @@ class GaResult:
     best_genome: np.ndarray
     best_plan: ObfuscationPlan
     best_reward: float
-    log: list = field(default_factory=list)   # (generation, index, reward, mean_ler, T/T*)
+    log: list = field(default_factory=list)   # (generation, index, reward, mean_ler, T) — raw latency T
 
 
 @dataclass

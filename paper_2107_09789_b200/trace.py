@@ -365,48 +365,110 @@ def trace_records(graph: Graph, fusion_limits: dict | None, strategies: dict | N
 
 
 def prepare_trace(items: list[tuple], profile: DeviceProfile, memo: dict | None = None,
-                  exchange=None, first_seen: dict | None = None, conv_index: bool = False) -> TracePlan:
+                  exchange=None, first_seen: dict | None = None, conv_index: bool = False,
+                  extra: dict | None = None) -> TracePlan:
     """Host half of compile_graph for many graphs: fuse, signatures, integer
     descriptors (one H2D for all). ``items``: (graph, fusion_limits,
-    strategies[, ir.Analysis])."""
+    strategies[, ir.Analysis[, (CandidateTrace, kernels, shapes)]])."""
     cts, compiled = [], []
     for item in items:
         graph, limits, strategies = item[0], item[1], item[2]
         ana = item[3] if len(item) > 3 and item[3] is not None else None
-        ct, kernels, shapes = trace_records(graph, limits, strategies, profile.name, ana)
+        pre = item[4] if len(item) > 4 else None
+        ct, kernels, shapes = pre if pre is not None else trace_records(graph, limits, strategies, profile.name, ana)
         cts.append(ct)
         compiled.append(CompiledGraph(kernels=kernels, source=graph, shapes=shapes))
-    return prepare_trace_records(cts, profile, memo, exchange, first_seen, compiled, conv_index)
+    return prepare_trace_records(cts, profile, memo, exchange, first_seen, compiled, conv_index, extra)
+
+
+def _distinct_sigs(cts: list[CandidateTrace]):
+    """(signature, candidate position, KERN record array, row) of every
+    distinct signature of ``cts`` in first-occurrence order (candidate order,
+    kernel order). Deduplicated by 64-bit digest with numpy when every record
+    carries digests, else one dict pass."""
+    flat = [(sg, c) for c, ct in enumerate(cts) for sg in ct.sigs]
+    if flat and all(ct.sig_keys is not None and len(ct.sig_keys) == len(ct.sigs) for ct in cts):
+        allk = np.concatenate([ct.sig_keys for ct in cts])
+        _, first = np.unique(allk, return_index=True)
+        recs_all = cat_records([ct.recs for ct in cts], KERN_DTYPE)
+        return [(flat[i][0], flat[i][1], recs_all, int(i)) for i in np.sort(first)]
+    out, seen = [], set()
+    for c, ct in enumerate(cts):
+        for r, sg in enumerate(ct.sigs):
+            if sg not in seen:
+                seen.add(sg)
+                out.append((sg, c, ct.recs, r))
+    return out
+
+
+def _first_blob(recs: np.ndarray, r: int) -> bytes:
+    """Descriptor a signature is searched from: its first occurrence's kernel
+    record with the strategy cleared (default_schedule runs before
+    modify_schedule, costmodel.py:277-283)."""
+    rec = recs[r:r + 1].copy()
+    rec["strategy"] = 0
+    return rec.tobytes()
+
+
+def shard_first_seen(cts: list[CandidateTrace], gidx, memo: dict) -> list[tuple[tuple, int, bytes]]:
+    """This process's part of the first-seen schedule memo (costmodel.py:
+    248-285) for a whole shard: every complex-kernel signature that is not
+    memoised yet, in first-occurrence order, tagged with the GLOBAL index of
+    the candidate it first occurs in and the descriptor it would be searched
+    from. Pure host (no device): ``dist.exchange_signatures`` merges the
+    parts of all ranks by global index."""
+    out = []
+    for sig, c, recs, r in _distinct_sigs(cts):
+        if sig in memo or sig[1] not in _COMPLEX_VALUES:
+            continue
+        out.append((sig, int(gidx[c]), _first_blob(recs, r)))
+    return out
+
+
+def resolve_first_seen(cts: list[CandidateTrace], gidx, memo: dict, exchange=None) -> dict[tuple, bytes]:
+    """signature -> descriptor of its globally first occurrence, for every
+    signature unmemoised on any rank. Exactly ONE ``exchange`` call whatever
+    this shard holds (empty, all infeasible, any micro-batch split), so the
+    ranks' collectives always pair up; every rank then searches the same
+    table and folds it into its memo, keeping the memos identical."""
+    local = shard_first_seen(cts, gidx, memo)
+    if exchange is None:
+        return {sig: blob for sig, _, blob in local}
+    return exchange(local)
 
 
 def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, memo: dict | None = None,
                           exchange=None, first_seen: dict | None = None,
-                          compiled: list[CompiledGraph] | None = None, conv_index: bool = False) -> TracePlan:
+                          compiled: list[CompiledGraph] | None = None, conv_index: bool = False,
+                          extra: dict | None = None) -> TracePlan:
     """Memo resolution and upload of a batch's kernel records.
 
     Signatures already in the memo resolve to their schedule; the others are
     searched on the device from their FIRST occurrence's descriptor
-    (costmodel.py:248 first-seen memo). ``exchange`` (dist.exchange_signatures)
-    merges this rank's unmemoised signatures with every other rank's in global
-    first-seen order, so all ranks search the same table and memos stay
-    equal. ``first_seen`` (sig -> descriptor bytes) carries first occurrences
-    across batches whose searches have not been folded into the memo yet."""
+    (costmodel.py:248 first-seen memo). ``first_seen`` (sig -> descriptor
+    bytes) carries first occurrences across the micro-batches of one call
+    (and, sharded, the globally first ones from ``resolve_first_seen``).
+    ``extra``: further (sig -> descriptor) rows to search and memoise although
+    no kernel of this batch uses them (signatures first seen on other ranks).
+    ``exchange``: this batch is a whole shard — resolve it across ranks here
+    (one collective; callers splitting a shard resolve it once themselves)."""
     ctx = device()
     memo = _SCHEDULE_CACHE if memo is None else memo
+    if exchange is not None:
+        glob = resolve_first_seen(cts, range(len(cts)), memo, exchange)
+        first_seen = dict(glob) if first_seen is None else first_seen
+        first_seen.update(glob)
+        extra = glob
     hits: dict[tuple, Schedule] = {}
     local_pending: dict[tuple, bytes] = {}
-    # Dedupe the batch's signatures by digest (numpy); only the distinct ones,
-    # in first-occurrence order, go through the memo (first-seen semantics
-    # unchanged). Records without digests take the per-kernel path.
     flat_sigs = [sg for ct in cts for sg in ct.sigs]
     nk_all = len(flat_sigs)
     use_keys = nk_all > 0 and all(ct.sig_keys is not None and len(ct.sig_keys) == len(ct.sigs) for ct in cts)
     if use_keys:
         allk = np.concatenate([ct.sig_keys for ct in cts])
         _, first, inverse = np.unique(allk, return_index=True, return_inverse=True)
-        order = np.sort(first)
         recs_all = cat_records([ct.recs for ct in cts], KERN_DTYPE)
-        visit = [(flat_sigs[i], recs_all, int(i)) for i in order]
+        visit = [(flat_sigs[i], recs_all, int(i)) for i in np.sort(first)]
     else:
         visit = [(sig, ct.recs, r) for ct in cts for r, sig in enumerate(ct.sigs)]
     for sig, recs_src, r in visit:
@@ -420,13 +482,16 @@ def prepare_trace_records(cts: list[CandidateTrace], profile: DeviceProfile, mem
             continue
         blob = first_seen.get(sig) if first_seen is not None else None
         if blob is None:
-            rec = recs_src[r:r + 1].copy()
-            rec["strategy"] = 0
-            blob = rec.tobytes()
+            blob = _first_blob(recs_src, r)
             if first_seen is not None:
                 first_seen[sig] = blob
         local_pending[sig] = blob
-    pending_all = exchange(list(local_pending.items())) if exchange is not None else local_pending
+    pending_all = local_pending
+    if extra:
+        pending_all = dict(local_pending)
+        for sig, blob in extra.items():
+            if sig not in hits and sig not in memo:
+                pending_all.setdefault(sig, blob)
     rows: dict[tuple, int] = {sig: i for i, sig in enumerate(hits)}
     # memoised signatures: resolved rows carrying their schedule (vectorised)
     hit_recs = np.zeros(len(hits), KERN_DTYPE)

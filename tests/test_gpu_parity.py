@@ -396,3 +396,25 @@ def test_micro_batched_records_match_single_batch(ctx):
     for i, p in enumerate(plans):
         og, d = knobs.apply_plan(g, p)
         assert many["latency"][i] == CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)[3]
+
+
+def test_weight_cache_eviction_is_exact(ctx):
+    """A weight cache bounded so tightly that it is dropped at every upload
+    (packed images keyed by a device address must go with it, and
+    a batch must keep the buffers its descriptors point at) gives records
+    identical to an unbounded cache, across several batches."""
+    g = fixtures.c1c2(size=24)
+    plans = _plans(g, "dimension", 6, seed=31)
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
+    want = PopulationEvaluator(g, ev, trials=2, memo={}).evaluate_records(plans, micro=2, memo={}, workers=0)
+    saved = ctx.weight_cache_limit
+    try:
+        ctx.clear_cache()
+        ctx.weight_cache_limit = 1
+        pe = PopulationEvaluator(g, ev, trials=2, memo={})
+        for _ in range(2):
+            got = pe.evaluate_records(plans, micro=2, memo={}, workers=0)
+            assert got.tobytes() == want.tobytes()
+    finally:
+        ctx.weight_cache_limit = saved
+        ctx.clear_cache()

@@ -46,7 +46,7 @@ def _worker(rank, world_size, port, q):
         res = ga.run_ga(g, "dimension", 0.02, params, sharded_eval)
         genomes = np.arange(12, dtype=np.int64).reshape(3, 4) * (rank + 1)
         got = D.broadcast_genomes(genomes if rank == 0 else None, (3, 4))
-        local = [((f"sig{rank}",), b"r%d" % rank), (("shared",), b"from%d" % rank)]
+        local = [((f"sig{rank}",), 4 * rank, b"r%d" % rank), (("shared",), 4 * rank + 1, b"from%d" % rank)]
         merged = D.exchange_signatures(local)
         q.put((rank, res.best_genome.tolist(), res.best_reward, [x[2] for x in res.log], got.tolist(),
                sorted(merged.items())))
