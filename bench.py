@@ -13,8 +13,10 @@ all-gather of the fitness records. Weak scaling: per-GPU work is fixed.
   e2e     through the public API (PopulationEvaluator.prepare + run + collect):
           host apply_plan, weight upload (H2D) + packing, descriptor staging,
           device pipeline, record read-back (D2H) — every step, cold caches
-  --impl reference   the reference path restated on the host CPU (oracle
-          port, one candidate per core in parallel, single-threaded BLAS)
+  --impl reference   the reference itself (traceobf 0.1.0 from baseline/_ref:
+          apply_plan, equivalence_check, profile_pipeline; restated fitness)
+          on the host CPU, one candidate per core in parallel with
+          single-threaded BLAS, plus one process with the default BLAS
 
 Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
 torch.distributed.run (one rank per GPU, NCCL).
@@ -60,7 +62,9 @@ def parse():
                          "auto = evaluate.auto_micro")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
-    ap.add_argument("--cfg4-pop", type=int, default=16, help="cfg4 (VGG-16 dimension) candidates per step; 0 = skip")
+    ap.add_argument("--cfg4-pop", type=int, default=256, help="cfg4 (VGG-16 dimension) population; 0 = skip")
+    ap.add_argument("--cfg4-batch", type=int, default=32, help="cfg4 resident batch (device-timed value)")
+    ap.add_argument("--cfg4-prec", choices=("bf16", "fp32"), default="bf16", help="cfg4 conv precision")
     ap.add_argument("--gen-pop", type=int, default=256,
                     help="also measure one full generation of this many candidates on one GPU "
                          "(north-star target: 256; separate process, N = 1 only); 0 = skip")
@@ -126,23 +130,31 @@ class ClockSampler:
                 "source": "NVML, 5 ms polling inside the timed region"}
 
 
-# ----------------------------------------------------------------------------- cpu (oracle port)
-def cpu_pool(vanilla, plans_for_workers, t_star, budget, trials, seed, predictors):
-    from oracle import candidate_ref
+# ----------------------------------------------------------------------------- cpu (the reference itself)
+def cpu_pool(vanilla, t_star, budget, trials, seed, predictors, use_reference=True):
+    """One worker per host core, single-threaded BLAS: the reference package
+    itself (oracle/reference_arm.py over baseline/_ref) when vendored, else
+    the restated port (oracle/candidate_ref.py). Returns (pool, cores, kind)."""
+    from oracle import candidate_ref, reference_arm
     cores = len(os.sched_getaffinity(0))
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
     pw = [{"F": p.features, "w": p.weights()} for p in predictors]
     ctx = mp.get_context("spawn")
-    pool = ctx.Pool(cores, initializer=candidate_ref.init_worker,
-                    initargs=(vanilla, pw, t_star, budget, trials, seed, 1))
-    return pool, cores
+    ref = use_reference and reference_arm.load_reference() is not None
+    mod = reference_arm if ref else candidate_ref
+    pool = ctx.Pool(cores, initializer=mod.init_worker, initargs=(vanilla, pw, t_star, budget, trials, seed, 1))
+    return pool, cores, ("reference" if ref else "port")
 
 
-def cpu_step(pool, plans):
-    from oracle import candidate_ref
+def cpu_step(pool, plans, kind, step):
+    from oracle import candidate_ref, reference_arm
     t0 = time.perf_counter()
-    res = pool.map(candidate_ref.evaluate_candidate, plans, chunksize=1)
+    if kind == "reference":
+        res = pool.map(reference_arm.evaluate_candidate, [(step, reference_arm.plan_wire(p)) for p in plans],
+                       chunksize=1)
+    else:
+        res = pool.map(candidate_ref.evaluate_candidate, plans, chunksize=1)
     return time.perf_counter() - t0, res
 
 
@@ -153,8 +165,30 @@ def host_predictors():
 
 
 def vanilla_t_star(vanilla):
-    from oracle import costmodel_ref
+    from oracle import costmodel_ref, reference_arm
+    if reference_arm.load_reference() is not None:
+        return reference_arm.vanilla_t_star(vanilla)
     return costmodel_ref.profile_pipeline(vanilla, "default", None, None, costmodel_ref.ScheduleMemo())[3]
+
+
+def single_process_mode(vanilla, t_star, args, preds, n: int) -> dict | None:
+    """SURVEY §8(d) CPU mode (i): the reference in ONE process with the default
+    (multi-threaded) BLAS, ``n`` candidates after one warm-up candidate."""
+    from oracle import reference_arm
+    if reference_arm.load_reference() is None or n < 1:
+        return None
+    pw = [{"F": p.features, "w": p.weights()} for p in preds]
+    reference_arm.init_worker(vanilla, pw, t_star, args.budget, args.trials, args.seed, blas_threads=0)
+    plans = population_plans(vanilla, n + 1, args.seed + 3)
+    reference_arm.evaluate_candidate((-1, reference_arm.plan_wire(plans[0])))
+    t0 = time.perf_counter()
+    res = [reference_arm.evaluate_candidate((s, reference_arm.plan_wire(p))) for s, p in enumerate(plans[1:])]
+    dt = time.perf_counter() - t0
+    stages = {k: round(sum(r.get("stages", {}).get(k, 0.0) for r in res) / n, 3)
+              for k in ("apply_plan", "forward", "trace", "fitness")}
+    return {"value": n / dt, "unit": UNIT, "candidates": n, "seconds_per_candidate": round(dt / n, 3),
+            "stage_seconds": stages, "blas_threads": "default (OpenBLAS, all host cores)",
+            "kind": "reference", "schedule_memo": "cold per candidate"}
 
 
 def reference_arm(args):
@@ -165,24 +199,38 @@ def reference_arm(args):
     vanilla = fixtures.resnet18()
     t_star = vanilla_t_star(vanilla)
     preds = host_predictors()
-    pool, cores = cpu_pool(vanilla, None, t_star, args.budget, args.trials, args.seed, preds)
+    pool, cores, kind = cpu_pool(vanilla, t_star, args.budget, args.trials, args.seed, preds)
     plans = population_plans(vanilla, cores * (args.warmup + args.steps), args.seed)
-    times = []
+    times, stage_tot, nres = [], {}, 0
     for s in range(args.warmup + args.steps):
-        dt, _ = cpu_step(pool, plans[s * cores:(s + 1) * cores])
+        dt, res = cpu_step(pool, plans[s * cores:(s + 1) * cores], kind, s)
         if s >= args.warmup:
             times.append(dt)
+            for r in res:
+                for k, v in r.get("stages", {}).items():
+                    stage_tot[k] = stage_tot.get(k, 0.0) + v
+                nres += 1
     pool.close()
     total = sum(times)
     value = cores * len(times) / total
+    mode_i = single_process_mode(vanilla, t_star, args, preds, min(args.steps, 3))
+    sample = (f"{cores} candidates per step, one per core (worker processes, single-threaded BLAS), "
+              f"ResNet-18 224x224, {args.trials} trials, cold schedule memo per step")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded N(0,1) inputs, random-init weights)",
             "config": {"workload": "resnet18_seq_generation", "fixture": "ResNet-18 224x224 batch 1",
-                       "candidates_per_step": cores, "trials": args.trials, "schedule_memo": "cold per candidate"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{cores} candidates per step (one per core, single-threaded BLAS)"},
+                       "candidates_per_step": cores, "trials": args.trials,
+                       "schedule_memo": "cold per step (reference module-global cache, per worker)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                             "code": ("traceobf 0.1.0 unmodified (baseline/_ref): apply_plan, equivalence_check, "
+                                      "profile_pipeline; restated LSTM/CTC/LER/Eq.10 (oracle/fitness_ref.c)")
+                             if kind == "reference" else "oracle port (baseline/_ref not vendored)",
+                             "stage_seconds_per_candidate": {k: round(v / max(nres, 1), 3)
+                                                             for k, v in stage_tot.items()}},
+            "cpu_modes": {"per_core_pool": {"value": value, "cores": cores, "blas_threads": 1},
+                          "single_process": mode_i},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -291,59 +339,94 @@ def workload_generation(args) -> dict | None:
 
 
 # ----------------------------------------------------------------------------- cfg4
-def workload_cfg4(args) -> dict:
-    """SURVEY cfg4: VGG-16 224x224 b1, dimension-mode candidates (widen, kernel
-    widen, dummy; widened weights synthesised on the device from the resident
-    vanilla arrays), 8 trials, full path (forward + verdict + trace + fitness).
-    Device-resident candidates/s and end-to-end candidates/s (public API,
-    cold caches, host apply_plan in worker processes), like the headline."""
+def workload_cfg4(args, peaks: dict) -> dict:
+    """SURVEY cfg4 as BASELINE specifies it: VGG-16 224x224 b1, a GA population
+    of ``--cfg4-pop`` (256) dimension-mode candidates (layer widening, kernel
+    widening, dummy adds; widened weights synthesised on the device from the
+    resident vanilla arrays), 8 trials, the bf16 conv path (``--cfg4-prec``),
+    full path (forward + verdict + trace + fitness).
+
+    value: device-resident candidates/s — 256 candidates x 8 trials of VGG-16
+    activations (~1 GB per candidate) do not fit in HBM at once, so the
+    population is timed in resident batches of ``--cfg4-batch`` (each prepared,
+    warmed up and timed in turn, cold schedule search) and value = P / sum of
+    the batch times. e2e: the whole population through evaluate_records (host
+    apply_plan in worker processes, micro-batched, H2D + D2H inside), cold
+    caches. Roofline: conv algorithmic FLOPs / conv launch time (CUDA events on
+    the launch stream) vs the measured bf16 peak."""
     import torch
     from paper_2107_09789_b200 import fixtures, ga
     from paper_2107_09789_b200.engine import device
     from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
     ctx = device()
-    P, steps, warm = args.cfg4_pop, 3, 2
+    P, PB, steps, warm = args.cfg4_pop, min(args.cfg4_batch, args.cfg4_pop), 3, 2
     g = fixtures.vgg16()
     space = ga.search_space(g, "dimension")
     sizes = ga.domain_sizes("dimension", space)
     rng = np.random.default_rng(args.seed)
-    plans = [ga.decode_genome(g, "dimension", space, x) for x in ga.random_genomes(rng, sizes, P * (steps + warm + 1))]
-    pe = PopulationEvaluator(g, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed, memo={})
-    prep = pe.prepare(plans[:P], memo={})
+    plans = [ga.decode_genome(g, "dimension", space, x) for x in ga.random_genomes(rng, sizes, 3 * P)]
+    prec = args.cfg4_prec
+    pe = PopulationEvaluator(g, Evaluator(), budget=args.budget, trials=args.trials, seed=args.seed, memo={},
+                             precision=prec)
     x = pe.x_host.to(ctx.device)
-    for _ in range(warm):
-        pe.run(prep, x_dev=x, cold_schedules=True)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        pe.run(prep, x_dev=x, cold_schedules=True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    flops = prep["run"].gemm_flops()
-    del prep
-    for s in range(warm):
+    total_ms = conv_ms = 0.0
+    flops = 0
+    clocks = ClockSampler(ctx.index)
+    clocks.start()
+    for lo in range(0, P, PB):
+        prep = pe.prepare(plans[lo:lo + PB], memo={})
+        for _ in range(warm):
+            pe.run(prep, x_dev=x, cold_schedules=True)
+        torch.cuda.synchronize()
+        run = prep["run"]
+        run.conv_events = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            pe.run(prep, x_dev=x, cold_schedules=True)
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1) / steps
+        conv_ms += sum(a.elapsed_time(b) for a, b in run.conv_events) / steps
+        run.conv_events = None
+        flops += run.gemm_flops()
+        del prep, run
         ctx.clear_cache()
-        pe.evaluate_records(plans[P * (1 + s):P * (2 + s)], memo={})
+    clk = clocks.stop()
+    # e2e: the whole population through the public API, cold caches
+    e2e_steps = 2
+    pe.evaluate_records(plans[2 * P:3 * P], memo={})  # warm-up (worker pool, arenas)
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
-    for s in range(steps):
+    for s in range(e2e_steps):
         ctx.clear_cache()
-        pe.evaluate_records(plans[P * (1 + warm + s):P * (2 + warm + s)], memo={})
+        pe.evaluate_records(plans[s * P:(s + 1) * P], memo={})
     f1.record()
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / steps
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    host = {k: round(v, 1) for k, v in pe.last_host_ms.items()}
     pe.close()
     ctx.clear_cache()
-    return {"workload": "vgg16_dimension_generation (SURVEY cfg4)", "candidates_per_step": P, "trials": args.trials,
-            "value": P / (ms / 1e3), "unit": UNIT, "ms_per_step": round(ms, 2),
-            "conv_alg_tflops": round(flops / (ms / 1e3) / 1e12, 1), "flops_per_step": flops,
-            "e2e": {"value": P / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": round(e2e_ms, 1),
-                    "host_ms_per_step": {k: round(v, 1) for k, v in pe.last_host_ms.items()}},
-            "note": "knob weights synthesised on the device (tobf_pack_weights_gather); no CPU baseline "
-                    "(the numpy port needs ~30 s per VGG-16 candidate per core)"}
+    bf16_peak = peaks.get("bf16_tflops", 1662.8)
+    achieved = flops / (conv_ms / 1e3) / 1e12
+    mmas = 2 if prec == "bf16" else 6  # bf16 mode: a_hi*b + a_lo*b; fp32: 3 tf32 MMAs at half the bf16 rate
+    return {"workload": "vgg16_dimension_generation (SURVEY cfg4: widen + kernel-widen, bf16 conv path)",
+            "population": P, "resident_batch": PB, "trials": args.trials, "precision": prec,
+            "value": P / (total_ms / 1e3), "unit": UNIT, "ms_per_generation": round(total_ms, 1),
+            "conv_ms_per_generation": round(conv_ms, 1), "flops_per_generation": flops,
+            "roofline": {"bound": "tensor", "kernel": f"conv_tc_kernel<BN, PREC={1 if prec == 'bf16' else 0}>",
+                         "achieved": round(achieved, 1), "peak": bf16_peak, "unit": "TFLOP/s",
+                         "frac": round(achieved / bf16_peak, 4),
+                         "tensor_pipe_equiv_frac": round(mmas * achieved / bf16_peak, 4),
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                         "note": "algorithmic FLOPs of the emitted convs/linears; bf16 mode issues 2 kind::f16 MMAs "
+                                 "per product (activation pair), so tensor-pipe work = 2x achieved/peak"},
+            "e2e": {"value": P / (e2e_ms / 1e3), "unit": UNIT, "ms_per_generation": round(e2e_ms, 1),
+                    "host_ms_per_generation": host},
+            "clocks": clk,
+            "note": "value: the population in resident batches (activations of 256 VGG-16 candidates x 8 trials "
+                    "exceed HBM); no CPU baseline (the numpy port needs ~30 s per VGG-16 candidate per core)"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -480,16 +563,17 @@ def main_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t_star = vanilla_t_star(vanilla)
         assert t_star == pe.t_star
-        pool, cores = cpu_pool(vanilla, None, t_star, args.budget, args.trials, args.seed, pe.ev.predictors)
+        pool, cores, kind = cpu_pool(vanilla, t_star, args.budget, args.trials, args.seed, pe.ev.predictors)
         cplans = population_plans(vanilla, cores * args.cpu_rounds, args.seed + 2)
         dt = 0.0
         for r in range(args.cpu_rounds):
-            t, _ = cpu_step(pool, cplans[r * cores:(r + 1) * cores])
+            t, _ = cpu_step(pool, cplans[r * cores:(r + 1) * cores], kind, r)
             dt += t
         pool.close()
-        cpu = {"value": cores * args.cpu_rounds / dt, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{cores * args.cpu_rounds} candidates, one per core in parallel (oracle port, "
-                         "single-threaded BLAS), same workload definition, cold schedule memo"}
+        cpu = {"value": cores * args.cpu_rounds / dt, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{cores * args.cpu_rounds} candidates, one per core in parallel (single-threaded BLAS), "
+                         "same workload definition, cold schedule memo"
+                         + (" — traceobf 0.1.0 itself (baseline/_ref)" if kind == "reference" else " — oracle port")}
 
     peaks = {}
     pp = ROOT / "MEASURED_PEAKS.json"
@@ -500,7 +584,7 @@ def main_ours(args):
         sweeps = kernel_sweeps(args, vanilla, pe.ev.predictors, peaks.get("hbm_gbs", 6546.9))
     cfg4 = None
     if rank == 0 and world == 1 and args.cfg4_pop > 0:
-        cfg4 = workload_cfg4(args)
+        cfg4 = workload_cfg4(args, peaks)
     gen = None
     if rank == 0 and world == 1 and args.gen_pop > 0 and args.gen_pop != P:
         gen = workload_generation(args)
@@ -517,7 +601,7 @@ def main_ours(args):
             tj = json.loads(tp.read_text())
             if tj.get("flops_per_step") == flops_step and tj.get("conv_launches_per_step") == conv_launches:
                 traffic, traffic_src = tj["dram_bytes_per_step"], tj["source"]
-        roofline = {"bound": "tensor", "kernel": "conv_tf32x3_kernel (grouped tcgen05 implicit GEMM)",
+        roofline = {"bound": "tensor", "kernel": "conv_tc_kernel<BN, PREC=0 3xTF32> (grouped tcgen05 implicit GEMM)",
                     "achieved": round(achieved, 2), "peak": bf16, "unit": "TFLOP/s",
                     "frac": round(achieved / bf16, 4), "traffic": traffic, "traffic_unit": "bytes per step",
                     "traffic_source": traffic_src, "algorithmic_bytes_per_step": gemm_bytes_step,

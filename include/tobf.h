@@ -73,10 +73,22 @@ typedef struct tobf_conv_desc {
   int32_t ksplit, kper;
 } tobf_conv_desc;
 
+/* Conv arithmetic (the `prec` argument of the *_ex entry points):
+ *   TOBF_PREC_TF32X3  fp32-faithful 3xTF32 tcgen05 kind::tf32 (the 1e-4 fp32
+ *                     contract of interpreter.py:93-118's comparisons)
+ *   TOBF_PREC_BF16    bf16 operands (activations rounded on the way into
+ *                     tensor memory, bf16 weight image), kind::f16, fp32
+ *                     accumulation (BASELINE's 2e-2 bf16 mode, cfg4)
+ * A weight image, a prepared descriptor group and a launch must agree on it. */
+#define TOBF_PREC_TF32X3 0
+#define TOBF_PREC_BF16 1
+
 /* Fill K/kblocks/mtiles/ntiles/tile_start for a group of descriptors (host
  * memory) for the given N tile width (64 or 128); returns total tile count
  * (no split-K: ksplit = 1). */
 int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles);
+
+int tobf_conv_prepare_ex(tobf_conv_desc* descs, int n, int block_n, int prec, int64_t* total_tiles);
 
 /* As tobf_conv_prepare, and, in groups with fewer than 2 tiles per SM, split
  * the K loop of tiles longer than ~1/4 of one SM's share of the group's work
@@ -89,8 +101,13 @@ int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_
 int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split, float* ws_base,
                             int32_t* cnt_base, int64_t* total_units, int64_t* ws_floats, int64_t* cnt_count);
 
+int tobf_conv_prepare_split_ex(tobf_conv_desc* descs, int n, int block_n, int prec, int sms, int max_split,
+                               float* ws_base, int32_t* cnt_base, int64_t* total_units, int64_t* ws_floats,
+                               int64_t* cnt_count);
+
 /* Bytes of the packed weight image for a conv with the given geometry. */
 int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n);
+int64_t tobf_wimg_bytes_ex(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n, int32_t prec);
 
 /* Pack a float32 weight tensor into the tile-major, tf32 hi/lo split,
  * 128B-swizzled operand image the conv kernel streams with bulk copies.
@@ -110,9 +127,22 @@ int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, int32_t c_r
                              int64_t su, int64_t sv, int64_t sc, int64_t sn, const int32_t* maps,
                              const float* scales, int32_t block_n, void* wimg, void* stream);
 
+/* Either precision; `maps`/`scales` both NULL (plain) or both set (gather). */
+int tobf_pack_weights_ex(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
+                         int64_t su, int64_t sv, int64_t sc, int64_t sn, const int32_t* maps, const float* scales,
+                         int32_t block_n, int32_t prec, void* wimg, void* stream);
+
 /* Grouped 3xTF32 tcgen05 implicit-GEMM convolution over `n` problems whose
  * descriptors live in DEVICE memory (prepared with tobf_conv_prepare). */
 int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, void* stream);
+
+/* Either precision. `sched`: two int32 of DEVICE memory, zero before the
+ * first launch, the launch-wide tile-claim counters (the launch's last CTA
+ * re-zeroes them); give every stream that may run conv launches concurrently
+ * its own pair. NULL: a module-global pair per kernel variant (launches of
+ * one variant must then be stream-ordered). */
+int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, int prec,
+                         int32_t* sched, void* stream);
 
 /* Generic fused element-wise / pooling / copy ops (one op per descriptor). */
 #define TOBF_OP_MAXPOOL 1  /* y = maxpool(x, window=a0, stride=a1) */

@@ -8,6 +8,12 @@ attacker / GA entry points the reference lacks (levenshtein, ler, fitness,
 run_ga, search_space) and the batched population evaluator.
 
     import paper_2107_09789_b200 as traceobf      # drop-in
+
+Every public function also accepts the reference's OWN objects (a
+``traceobf.Graph``, ``ObfuscationPlan``, ``DeviceProfile``, ``LeakageCase``
+...) and then answers in the reference's classes and exception types
+(refcompat.py); ``refcompat.install(traceobf)`` routes the reference
+package's hot entry points here.
 """
 
 from .ir import (
@@ -82,5 +88,20 @@ from .attacker import FitnessReport, Predictor, bagged_predictors, init_predicto
 from .evaluate import Evaluator, PopulationEvaluator, fitness
 from .dimattack import DimRegressor, ZeroTruth, der, load_dim_regressors, train_dim_regressors
 from .ga import GaParams, GaResult, run_ga, search_space
+
+from . import refcompat
+
+# the drop-in boundary: reference objects in, reference classes (and exception
+# types) out; engine objects pass straight through
+for _name in ("infer_shapes", "label_sequence", "topo_order", "validate",
+              "add_dummy", "apply_plan", "branch_layer", "deepen_layer", "identity_plan", "skip_layer",
+              "widen_kernel", "widen_layer", "widenable",
+              "default_schedule", "fuse", "modify_schedule",
+              "compile_graph", "profile_graph", "profile_kernel", "profile_pipeline",
+              "dump_graph", "dump_plan", "dump_trace",
+              "equivalence_check", "evaluate_equivalence", "execute",
+              "fitness", "run_ga", "search_space"):
+    globals()[_name] = refcompat.dropin(globals()[_name])
+del _name
 
 __version__ = "0.1.0"

@@ -18,6 +18,8 @@ TOBF_E_INVALID, TOBF_E_CUDA, TOBF_E_FAULT = -1, -2, -3
 TOBF_MAX_EPI = 6
 EPI_NONE, EPI_AFFINE, EPI_RELU, EPI_ADD_TENSOR, EPI_ADD_CONST = 0, 1, 2, 3, 4
 OP_MAXPOOL, OP_EPI, OP_COPYCH, OP_SOFTMAX = 1, 2, 3, 4
+PREC_TF32X3, PREC_BF16 = 0, 1
+PRECISIONS = {"fp32": PREC_TF32X3, "bf16": PREC_BF16}
 
 
 class NativeUnavailable(RuntimeError):
@@ -95,6 +97,13 @@ SIGNATURES = {
     "tobf_pack_weights_gather": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32,
                                            _vp, _vp]),
     "tobf_conv_grouped": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _vp]),
+    "tobf_conv_prepare_ex": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_i64)]),
+    "tobf_conv_prepare_split_ex": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp,
+                                             C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
+    "tobf_wimg_bytes_ex": (_i64, [_i32, _i32, _i32, _i32, _i32, _i32]),
+    "tobf_pack_weights_ex": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32,
+                                       _i32, _vp, _vp]),
+    "tobf_conv_grouped_ex": (C.c_int, [_vp, C.c_int, _i64, C.c_int, C.c_int, _vp, _vp]),
     "tobf_ew_prepare": (C.c_int, [_vp, C.c_int, C.POINTER(_i64)]),
     "tobf_ew_grouped": (C.c_int, [_vp, C.c_int, _i64, _vp]),
     "tobf_equiv_compare": (C.c_int, [_vp, _vp, C.c_int, _i64, _i32, _i32, _f32, _vp, _vp, _vp]),

@@ -1,5 +1,15 @@
 // Grouped implicit-GEMM convolution on sm_100a tensor cores (tcgen05 + TMEM),
-// fp32-faithful via 3xTF32 (a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi).
+// in two precisions (PREC template parameter):
+//   0  fp32-faithful via 3xTF32 (a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi),
+//      kind::tf32 — the 1e-4 contract of the fp32 mode;
+//   1  bf16 mode: bf16 weight image; activations enter tensor memory as a
+//      bf16 pair a = a_hi + a_lo (a_lo = bf16(a - a_hi)), two kind::f16 MMAs
+//      per 16 K (a_hi*b, a_lo*b), fp32 accumulation in TMEM — the 2e-2
+//      contract of BASELINE's bf16 mode (cfg4). Rounding the activations too
+//      (one MMA) doubles the error: a bf16 emulation of the config-1 stack
+//      gives 3.0e-2 max relative error vs fp32, the pair 1.7e-2 (weights'
+//      rounding only), so the pair is what keeps the contract on every
+//      fixture, at 1/3 of the tensor work of 3xTF32.
 //
 // Replaces interpreter.py:22-30 (conv2d: np.pad + sliding_window_view +
 // einsum -> OpenBLAS sgemm) and the Linear of interpreter.py:48-51 (expressed
@@ -23,14 +33,20 @@ constexpr int kBK = 32;           // fp32 elements per K block = one 128-B swizz
 constexpr int kRowBytes = 128;
 constexpr int kABytes = kBM * kRowBytes;  // 16 KB
 
-template <int BN>
+template <int BN, int PREC>
 struct ConvCfg {
+  static constexpr bool kBf16 = PREC == 1;
+  // A K block = kStgPerKB staging blocks of 32 fp32 per row; its GEMM K
+  // extent is kBKe (tf32: 32 elements = one 128-B row; bf16: 64 = one 128-B
+  // bf16 row of the B image, two fp32 staging blocks of A)
+  static constexpr int kStgPerKB = kBf16 ? 2 : 1;
+  static constexpr int kBKe = kBK * kStgPerKB;
   // The A tile (hi/lo) lives in tensor memory (tcgen05.st by the producer, A
   // operand read from TMEM by the MMA); shared memory carries only B, whose
   // three MMA reads per K step are what the tensor pipe pulls from it.
   static constexpr int kBBytes = BN * kRowBytes;
-  static constexpr int kStageBytes = 2 * kBBytes;  // B hi, B lo
-  static constexpr int kStages = BN >= 128 ? 2 : 4;
+  static constexpr int kStageBytes = kBf16 ? kBBytes : 2 * kBBytes;  // B (tf32: hi, lo)
+  static constexpr int kStages = kBf16 ? 4 : (BN >= 128 ? 2 : 4);
   // fp32 A blocks land here by cp.async (coalesced, zero-filled padding)
   // kStagingKB blocks ahead of the split into TMEM
   static constexpr int kStagingKB = 4;
@@ -45,11 +61,15 @@ struct ConvCfg {
   //   kTmemACol + 64*s             A stage s: 32 hi + 32 lo columns
   // BN=128 has room for one correction slot only: a tile's first MMA waits
   // until the drain has read the previous tile's correction.
-  static constexpr int kCorrSlots = BN >= 128 ? 1 : 2;
+  // bf16: no correction terms; the tile accumulates in one TMEM buffer (no
+  // chunked drain: bf16 rounding dominates the accumulation error), two
+  // buffers so tile i+1's MMAs overlap tile i's drain.
+  static constexpr int kCorrSlots = kBf16 ? 0 : (BN >= 128 ? 1 : 2);
   static constexpr int kTmemMainCol = kCorrSlots * BN;
   static constexpr int kTmemACol = kTmemMainCol + 2 * BN;
+  static constexpr int kAStageCols = 64;  // tf32: 32 hi + 32 lo; bf16: 64 K as 32 hi + 32 lo bf16x2 columns
   static constexpr int kTmemCols = 512;
-  static_assert(kTmemACol + 64 * kStages <= 512, "TMEM budget");
+  static_assert(kTmemACol + kAStageCols * kStages <= 512, "TMEM budget");
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
@@ -110,7 +130,7 @@ constexpr int kInfoSlots = TOBF_CONV_INFO_SLOTS;
 // Dynamic tile counters: [0] next tile (beyond the first gridDim.x), [1] CTAs
 // exited; the last CTA to exit resets both, so consecutive launches (stream
 // ordered: every conv of the executor runs on its engine stream) start at 0.
-__device__ int g_conv_sched[2][2];
+__device__ int g_conv_sched[2][2][2];  // [PREC][BN>=128]: fallback when the caller passes none
 constexpr int kInfoConsumers = 4 /*A warps*/ + 1 /*B*/ + 1 /*MMA*/ + 4 /*drain warps*/;
 
 __device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ descs, int lo, int nprob, int tile) {
@@ -268,11 +288,13 @@ __device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_co
   }
 }
 
-template <int BN>
+template <int BN, int PREC>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_tf32x3_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles) {
-  using Cfg = ConvCfg<BN>;
+    conv_tc_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles, int* __restrict__ sched) {
+  using Cfg = ConvCfg<BN, PREC>;
   constexpr int STAGES = Cfg::kStages;
+  constexpr bool kBf16 = Cfg::kBf16;
+  constexpr int kChunk = kBf16 ? (1 << 30) : kChunkKB;  // K blocks per main-accumulator drain
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_buf = reinterpret_cast<float*>(smem + Cfg::kEpiOff);
@@ -288,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_took + 1);
   volatile int* info_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kInfoSlots], -1 = no more tiles
   volatile int* split_last = info_tile + kInfoSlots;  // drain: this unit completes its split-K tile
-  int* sched = g_conv_sched[BN >= 128 ? 1 : 0];
+  // launch-wide tile counters: the caller's pair, else this variant's module pair
+  if (sched == nullptr) sched = g_conv_sched[PREC][BN >= 128 ? 1 : 0];
 
 #ifdef TOBF_CONV_PROF
   const unsigned long long _cta_t0 = globaltimer_ns();
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = (t2 / d.ntiles) * kBM + 32 * warp + rsub;
         const int HWo = d.Ho * d.Wo;
         const int M = d.batch * HWo;
-        ikblocks = min(d.kper, d.kblocks - kb0);
+        ikblocks = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);  // staging blocks
         Cp = d.Cp; k1 = d.k1; k2 = d.k2; H = d.H; W = d.W; ldx = d.ldx;
         x = d.x;
 #pragma unroll
@@ -387,8 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             rowp[i] = x;
           }
         }
-        {  // cursor at K element kb0*kBK + chunk*4 = ((u*k2 + v)*Cp + c0)
-          const int k0 = kb0 * kBK + chunk * 4;
+        {  // cursor at K element kb0*kBKe + chunk*4 = ((u*k2 + v)*Cp + c0)
+          const int k0 = kb0 * Cfg::kBKe + chunk * 4;
           const int tap = k0 / Cp;
           c0 = k0 - tap * Cp;
           u = tap / k2;
@@ -449,9 +472,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ensure()) { ++ikb; ++issued; }
       cp_async_commit();
       if (g >= issued) break;
-      PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
-      mbar_arrive(&full_bar[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      if (g % Cfg::kStgPerKB == Cfg::kStgPerKB - 1) {
+        PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
+        mbar_arrive(&full_bar[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
       continue;
 #endif
       PROF_WAIT(4, if (ensure()) issue());
@@ -462,6 +487,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 row[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      if constexpr (kBf16) {
+        // 32 fp32 -> 16 hi + 16 lo bf16x2 columns (round to nearest even),
+        // element k in the low half of column k/2; two staging blocks fill
+        // one 64-K stage (hi columns [0,32), lo columns [32,64))
+        uint32_t pk[16], pl[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 a = row[q];
+          pk[2 * q] = pack_bf16x2(a.x, a.y);
+          pk[2 * q + 1] = pack_bf16x2(a.z, a.w);
+          pl[2 * q] = pack_bf16x2(a.x - bf16lo_f(pk[2 * q]), a.y - bf16hi_f(pk[2 * q]));
+          pl[2 * q + 1] = pack_bf16x2(a.z - bf16lo_f(pk[2 * q + 1]), a.w - bf16hi_f(pk[2 * q + 1]));
+        }
+        const int half = g & 1;
+        if (half == 0) {
+          PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
+          tc_fence_after();
+        }
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + Cfg::kTmemACol +
+                            stage * Cfg::kAStageCols + half * 16;
+        tmem_st16u(ta, pk);
+        tmem_st16u(ta + 32, pl);
+        if (half == 1) {
+          PROF_WAIT(3, tmem_wait_st());
+          tc_fence_before();
+          mbar_arrive(&full_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        continue;
+      }
       // split hi/lo BEFORE waiting for the free TMEM stage: after the MMAs
       // release it only the four tcgen05.st are left on the critical path
       float hh[2][16], ll[2][16];
@@ -516,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_tile = t2 - (t2 / d.ntiles) * d.ntiles;
         const int kblocks = min(d.kper, d.kblocks - kb0);
         const uint8_t* wimg = reinterpret_cast<const uint8_t*>(d.wimg) +
-                              ((int64_t)n_tile * d.kblocks + kb0) * (2 * Cfg::kBBytes);
+                              ((int64_t)n_tile * d.kblocks + kb0) * Cfg::kStageBytes;
         mbar_arrive(&info_empty[islot]);
         for (int kb = 0; kb < kblocks; ++kb) {
           PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x104));
@@ -525,8 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           (void)dst;  // diagnostic build: no B stream (wrong results)
           mbar_arrive(&full_bar[stage]);
 #else
-          mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kBBytes);
-          bulk_g2s(dst, wimg + (int64_t)kb * (2 * Cfg::kBBytes), 2 * Cfg::kBBytes, &full_bar[stage]);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          bulk_g2s(dst, wimg + (int64_t)kb * Cfg::kStageBytes, Cfg::kStageBytes, &full_bar[stage]);
 #endif
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -540,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The whole warp runs the schedule so stage addresses, descriptors and
     // TMEM addresses are warp-uniform (uniform registers: no per-MMA
     // register->uniform broadcast loop); one elected lane issues.
-    constexpr uint32_t idesc = idesc_make(2u /*tf32*/, kBM, BN);
+    constexpr uint32_t idesc = idesc_make(kBf16 ? 1u /*bf16*/ : 2u /*tf32*/, kBM, BN);
     const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
     int stage = 0;
@@ -563,23 +618,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_empty[islot]);
-      const int slot = it % Cfg::kCorrSlots;
+      const int slot = kBf16 ? 0 : it % Cfg::kCorrSlots;
       const uint32_t acc_small = tb + slot * BN;
-      PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it / Cfg::kCorrSlots) & 1) ^ 1, 0x107));
-      tc_fence_after();
-      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
+      if constexpr (!kBf16) {
+        PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it / Cfg::kCorrSlots) & 1) ^ 1, 0x107));
+        tc_fence_after();
+      }
+      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunk, ++gc) {
         const int buf = gc & 1;
         const uint32_t acc = tb + Cfg::kTmemMainCol + buf * BN;
         PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106));
         tc_fence_after();
-        const int kend = min(kblocks, kb0 + kChunkKB);
+        const int kend = kblocks - kb0 > kChunk ? kb0 + kChunk : kblocks;
         for (int kb = kb0; kb < kend; ++kb) {
           PROF_WAIT(3, mbar_wait(&full_bar[stage], phase, 0x105));
           tc_fence_after();
           const uint32_t b_hi = sbase + stage * Cfg::kStageBytes;
           const uint32_t b_lo = b_hi + Cfg::kBBytes;
-          const uint32_t ta = tb + Cfg::kTmemACol + stage * 64;  // A hi columns, lo at +32
-          if (elect_one()) {
+          const uint32_t ta = tb + Cfg::kTmemACol + stage * Cfg::kAStageCols;  // tf32: A hi, lo at +32
+          if constexpr (kBf16) {
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < Cfg::kBKe / 16; ++kk) {  // 16 bf16 = 32 B of the B row, 8 A columns
+                const uint64_t db = sdesc_k128(b_hi + kk * 32);
+                mma_bf16_ts(acc, ta + kk * 8, db, idesc, (kb - kb0 | kk) != 0);  // a_hi * b
+                mma_bf16_ts(acc, ta + 32 + kk * 8, db, idesc, 1u);               // a_lo * b
+              }
+              mma_commit(&empty_bar[stage]);
+            }
+          } else if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 8; ++kk) {
               const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
@@ -626,11 +693,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int HWo = d.Ho * d.Wo;
       const int M = d.batch * HWo;
       const int kblocks = min(d.kper, d.kblocks - ks * d.kper);
-      const int slot = it % Cfg::kCorrSlots;
+      const int slot = kBf16 ? 0 : it % Cfg::kCorrSlots;
       float sum[BN];
 #pragma unroll
       for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
-      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKB, ++gc) {
+      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunk, ++gc) {
         const int buf = gc & 1;
         if (ew == 0) PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103));
         asm volatile("bar.sync 2, 128;" ::: "memory");
@@ -648,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
       }
-      {
+      if constexpr (!kBf16) {
         // the tile's last acc_full commit covered every MMA of the tile, so the
         // correction accumulator of this slot is complete as well
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + slot * BN;
@@ -853,17 +920,39 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------ weight packing
-// Image layout: [ntiles][kblocks][hi|lo][BN rows][128 B swizzled], element
-// (k, n) of the GEMM B operand (k = (u*k2 + v)*Cp + c) in row n%BN, column k%32.
+// Image layout: [ntiles][kblocks][plane][BN rows][128 B swizzled] with, per
+// precision, element (k, n) of the GEMM B operand (k = (u*k2 + v)*Cp + c) in
+// row n%BN of K block k / kBKe:
+//   tf32x3  planes hi | lo, column k%32 as fp32 (tf32-rounded hi, exact lo)
+//   bf16    one plane, column k%64 as bf16 (round to nearest even)
 // maps (optional, knob-derived weights, derived.py): [mu(k1) | mv(k2) | mc(c_real) | mn(j)]
 // source indices into the vanilla array (-1 = zero) and scales [sc(c_real) | sn(j)]:
 // element (u, v, c, n) = w[mu[u]*su + mv[v]*sv + mc[c]*sc + mn[n]*sn] * sc[c] * sn[n].
+__device__ __forceinline__ float weight_at(const float* __restrict__ w, int k, int n, int k1, int k2, int c_real,
+                                           int Cp, int j, int K, int64_t su, int64_t sv, int64_t sc, int64_t sn,
+                                           const int32_t* __restrict__ maps, const float* __restrict__ scales) {
+  if (n >= j || k >= K) return 0.f;
+  const int uv = k / Cp;
+  const int c = k - uv * Cp;
+  const int uu = uv / k2;
+  const int vv = uv - uu * k2;
+  if (c >= c_real) return 0.f;
+  if (maps == nullptr) return w[uu * su + vv * sv + c * sc + n * sn];
+  const int mu = __ldg(maps + uu), mv = __ldg(maps + k1 + vv);
+  const int mc = __ldg(maps + k1 + k2 + c), mn = __ldg(maps + k1 + k2 + c_real + n);
+  if ((mu | mv | mc | mn) < 0) return 0.f;
+  return w[mu * su + mv * sv + mc * sc + mn * sn] * __ldg(scales + c) * __ldg(scales + c_real + n);
+}
+
+template <int PREC>
 __global__ void pack_weights_kernel(const float* __restrict__ w, int k1, int k2, int c_real, int Cp, int j,
                                     int64_t su, int64_t sv, int64_t sc, int64_t sn, int BN, int kblocks,
                                     int ntiles, float* __restrict__ img, const int32_t* __restrict__ maps,
                                     const float* __restrict__ scales) {
-  const int64_t total = (int64_t)ntiles * kblocks * BN * 8;  // 16-B chunks of the hi plane
+  const int64_t total = (int64_t)ntiles * kblocks * BN * 8;  // 16-B chunks of one plane
   const int K = k1 * k2 * Cp;
+  constexpr int kPer = PREC ? 8 : 4;       // elements per 16-B chunk
+  constexpr int kBKe = PREC ? 64 : 32;     // elements per K block
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int chunk = q & 7;
@@ -873,35 +962,32 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int k1, int k2,
     const int kb = tk % kblocks;
     const int nt = tk / kblocks;
     const int n = nt * BN + r;
-    float hv[4], lv[4];
+    float v[kPer];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = kb * 32 + chunk * 4 + e;
-      float val = 0.f;
-      if (n < j && k < K) {
-        const int uv = k / Cp;
-        const int c = k - uv * Cp;
-        const int uu = uv / k2;
-        const int vv = uv - uu * k2;
-        if (c < c_real) {
-          if (maps == nullptr) {
-            val = w[uu * su + vv * sv + c * sc + n * sn];
-          } else {
-            const int mu = __ldg(maps + uu), mv = __ldg(maps + k1 + vv);
-            const int mc = __ldg(maps + k1 + k2 + c), mn = __ldg(maps + k1 + k2 + c_real + n);
-            if ((mu | mv | mc | mn) >= 0)
-              val = w[mu * su + mv * sv + mc * sc + mn * sn] * __ldg(scales + c) * __ldg(scales + c_real + n);
-          }
-        }
+    for (int e = 0; e < kPer; ++e)
+      v[e] = weight_at(w, kb * kBKe + chunk * kPer + e, n, k1, k2, c_real, Cp, j, K, su, sv, sc, sn, maps, scales);
+    const uint32_t off = sw128_off(r, chunk) / 4;  // in floats
+    if constexpr (PREC == 1) {
+      const int64_t plane = (int64_t)BN * 32;  // floats (= 128-B rows) per plane
+      float* base = img + ((int64_t)nt * kblocks + kb) * plane;
+      uint4 pk;
+      pk.x = pack_bf16x2(v[0], v[1]);
+      pk.y = pack_bf16x2(v[2], v[3]);
+      pk.z = pack_bf16x2(v[4], v[5]);
+      pk.w = pack_bf16x2(v[6], v[7]);
+      *reinterpret_cast<uint4*>(base + off) = pk;
+    } else {
+      float hv[4], lv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hv[e] = __uint_as_float(to_tf32_rna(v[e]));
+        lv[e] = v[e] - hv[e];
       }
-      hv[e] = __uint_as_float(to_tf32_rna(val));
-      lv[e] = val - hv[e];
+      const int64_t plane = (int64_t)BN * 32;  // floats per hi (or lo) plane
+      float* base = img + ((int64_t)nt * kblocks + kb) * 2 * plane;
+      *reinterpret_cast<float4*>(base + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<float4*>(base + plane + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
     }
-    const int64_t plane = (int64_t)BN * 32;  // floats per hi (or lo) plane
-    float* base = img + ((int64_t)nt * kblocks + kb) * 2 * plane;
-    const uint32_t off = sw128_off(r, chunk) / 4;
-    *reinterpret_cast<float4*>(base + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-    *reinterpret_cast<float4*>(base + plane + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
   }
 }
 
@@ -909,10 +995,14 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int k1, int k2,
 
 using namespace tobf;
 
-extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles) {
-  if (n < 0 || (block_n != 64 && block_n != 128) || (n > 0 && !descs)) {
+static inline int prec_kbk(int prec) { return prec == TOBF_PREC_BF16 ? 64 : 32; }
+static inline bool prec_ok(int prec) { return prec == TOBF_PREC_TF32X3 || prec == TOBF_PREC_BF16; }
+
+extern "C" int tobf_conv_prepare_ex(tobf_conv_desc* descs, int n, int block_n, int prec, int64_t* total_tiles) {
+  if (n < 0 || (block_n != 64 && block_n != 128) || (n > 0 && !descs) || !prec_ok(prec) || !total_tiles) {
     return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare: bad arguments");
   }
+  const int kbk = prec_kbk(prec);
   int64_t acc = 0;
   for (int i = 0; i < n; ++i) {
     tobf_conv_desc& d = descs[i];
@@ -921,7 +1011,7 @@ extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int6
       return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare: descriptor %d violates layout invariants", i);
     }
     d.K = d.k1 * d.k2 * d.Cp;
-    d.kblocks = (d.K + kBK - 1) / kBK;
+    d.kblocks = (d.K + kbk - 1) / kbk;
     const int64_t M = (int64_t)d.batch * d.Ho * d.Wo;
     d.mtiles = (int)((M + kBM - 1) / kBM);
     d.ntiles = (d.j + block_n - 1) / block_n;
@@ -937,6 +1027,10 @@ extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int6
   return TOBF_OK;
 }
 
+extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int64_t* total_tiles) {
+  return tobf_conv_prepare_ex(descs, n, block_n, TOBF_PREC_TF32X3, total_tiles);
+}
+
 #ifndef TOBF_SPLIT_TILES_PER_SM
 #define TOBF_SPLIT_TILES_PER_SM 2
 #endif
@@ -946,11 +1040,11 @@ extern "C" int tobf_conv_prepare(tobf_conv_desc* descs, int n, int block_n, int6
 // write + read of a 128 x BN fp32 tile costs about as much as 3-4 K blocks of
 // MMAs, hence the floor). Measured: splitting also in groups of 2-8 tiles per
 // SM cost more in partial traffic than it won in balance (10.8 vs 10.6 ms).
-extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split,
-                                       float* ws_base, int32_t* cnt_base, int64_t* total_units,
-                                       int64_t* ws_floats, int64_t* cnt_count) {
+extern "C" int tobf_conv_prepare_split_ex(tobf_conv_desc* descs, int n, int block_n, int prec, int sms,
+                                          int max_split, float* ws_base, int32_t* cnt_base, int64_t* total_units,
+                                          int64_t* ws_floats, int64_t* cnt_count) {
   int64_t tiles = 0;
-  int rc = tobf_conv_prepare(descs, n, block_n, &tiles);
+  int rc = tobf_conv_prepare_ex(descs, n, block_n, prec, &tiles);
   if (rc != TOBF_OK) return rc;
   if (sms < 1 || max_split < 1 || !total_units || !ws_floats || !cnt_count)
     return tobf_fail(TOBF_E_INVALID, "tobf_conv_prepare_split: bad arguments");
@@ -995,21 +1089,54 @@ extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n
   return TOBF_OK;
 }
 
-extern "C" int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n) {
-  const int64_t K = (int64_t)k1 * k2 * Cp;
-  const int64_t kblocks = (K + kBK - 1) / kBK;
-  const int64_t ntiles = (j + block_n - 1) / block_n;
-  return ntiles * kblocks * 2 * block_n * kRowBytes;
+extern "C" int tobf_conv_prepare_split(tobf_conv_desc* descs, int n, int block_n, int sms, int max_split,
+                                       float* ws_base, int32_t* cnt_base, int64_t* total_units,
+                                       int64_t* ws_floats, int64_t* cnt_count) {
+  return tobf_conv_prepare_split_ex(descs, n, block_n, TOBF_PREC_TF32X3, sms, max_split, ws_base, cnt_base,
+                                    total_units, ws_floats, cnt_count);
 }
 
-static int pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j, int64_t su,
-                        int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg, const int32_t* maps,
-                        const float* scales, void* stream);
+extern "C" int64_t tobf_wimg_bytes_ex(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n, int32_t prec) {
+  if (!prec_ok(prec)) return -1;
+  const int kbk = prec_kbk(prec);
+  const int64_t K = (int64_t)k1 * k2 * Cp;
+  const int64_t kblocks = (K + kbk - 1) / kbk;
+  const int64_t ntiles = (j + block_n - 1) / block_n;
+  return ntiles * kblocks * (prec == TOBF_PREC_BF16 ? 1 : 2) * block_n * kRowBytes;
+}
+
+extern "C" int64_t tobf_wimg_bytes(int32_t k1, int32_t k2, int32_t Cp, int32_t j, int32_t block_n) {
+  return tobf_wimg_bytes_ex(k1, k2, Cp, j, block_n, TOBF_PREC_TF32X3);
+}
+
+extern "C" int tobf_pack_weights_ex(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
+                                    int64_t su, int64_t sv, int64_t sc, int64_t sn, const int32_t* maps,
+                                    const float* scales, int32_t block_n, int32_t prec, void* wimg, void* stream) {
+  if (!w || !wimg || Cp % 4 || c_real > Cp || (block_n != 64 && block_n != 128) || !prec_ok(prec) ||
+      (maps == nullptr) != (scales == nullptr)) {
+    return tobf_fail(TOBF_E_INVALID, "tobf_pack_weights: bad arguments");
+  }
+  const int kbk = prec_kbk(prec);
+  const int K = k1 * k2 * Cp;
+  const int kblocks = (K + kbk - 1) / kbk;
+  const int ntiles = (j + block_n - 1) / block_n;
+  const int64_t chunks = (int64_t)ntiles * kblocks * block_n * 8;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((chunks + threads - 1) / threads, 148 * 16);
+  if (prec == TOBF_PREC_BF16)
+    pack_weights_kernel<1><<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+        w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, kblocks, ntiles, static_cast<float*>(wimg), maps, scales);
+  else
+    pack_weights_kernel<0><<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+        w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, kblocks, ntiles, static_cast<float*>(wimg), maps, scales);
+  return tobf_cuda_check("tobf_pack_weights");
+}
 
 extern "C" int tobf_pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j,
                                  int64_t su, int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg,
                                  void* stream) {
-  return pack_weights(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, wimg, nullptr, nullptr, stream);
+  return tobf_pack_weights_ex(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, nullptr, nullptr, block_n,
+                              TOBF_PREC_TF32X3, wimg, stream);
 }
 
 extern "C" int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp,
@@ -1017,53 +1144,53 @@ extern "C" int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, 
                                         const int32_t* maps, const float* scales, int32_t block_n, void* wimg,
                                         void* stream) {
   if (!maps || !scales) return tobf_fail(TOBF_E_INVALID, "tobf_pack_weights_gather: null maps");
-  return pack_weights(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, wimg, maps, scales, stream);
+  return tobf_pack_weights_ex(w, k1, k2, c_real, Cp, j, su, sv, sc, sn, maps, scales, block_n, TOBF_PREC_TF32X3,
+                              wimg, stream);
 }
 
-static int pack_weights(const float* w, int32_t k1, int32_t k2, int32_t c_real, int32_t Cp, int32_t j, int64_t su,
-                        int64_t sv, int64_t sc, int64_t sn, int32_t block_n, void* wimg, const int32_t* maps,
-                        const float* scales, void* stream) {
-  if (!w || !wimg || Cp % 4 || c_real > Cp || (block_n != 64 && block_n != 128)) {
-    return tobf_fail(TOBF_E_INVALID, "tobf_pack_weights: bad arguments");
+// Per-device launch state of one kernel variant: SM count and the one-time
+// dynamic shared-memory opt-in (a context may drive several devices).
+template <int BN, int PREC>
+static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int32_t* sched, cudaStream_t st) {
+  constexpr int kMaxDev = 64;
+  static int sms[kMaxDev] = {0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= kMaxDev)
+    return tobf_fail(TOBF_E_CUDA, "tobf_conv_grouped: no current device");
+  if (sms[dev] == 0) {
+    int count = 0;
+    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaFuncSetAttribute(conv_tc_kernel<BN, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ConvCfg<BN, PREC>::kSmem);
+    if (e != cudaSuccess || count < 1) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    sms[dev] = count;
   }
-  const int K = k1 * k2 * Cp;
-  const int kblocks = (K + kBK - 1) / kBK;
-  const int ntiles = (j + block_n - 1) / block_n;
-  const int64_t chunks = (int64_t)ntiles * kblocks * block_n * 8;
-  const int threads = 256;
-  const int64_t blocks = std::min<int64_t>((chunks + threads - 1) / threads, 148 * 16);
-  pack_weights_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-      w, k1, k2, c_real, Cp, j, su, sv, sc, sn, block_n, kblocks, ntiles, static_cast<float*>(wimg), maps, scales);
-  return tobf_cuda_check("tobf_pack_weights");
-}
-
-template <int BN>
-static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, cudaStream_t st) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(conv_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ConvCfg<BN>::kSmem);
-    if (e != cudaSuccess) {
-      sms = 0;
-      return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    }
-  }
-  const int grid = (int)std::min<int64_t>(total_tiles, sms);
-  conv_tf32x3_kernel<BN><<<grid, kThreads, ConvCfg<BN>::kSmem, st>>>(d_descs, n, (int)total_tiles);
+  const int grid = (int)std::min<int64_t>(total_tiles, sms[dev]);
+  conv_tc_kernel<BN, PREC><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles, sched);
   return tobf_cuda_check("tobf_conv_grouped");
+}
+
+extern "C" int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n,
+                                    int prec, int32_t* sched, void* stream) {
+  if (n <= 0 || total_tiles <= 0) return TOBF_OK;
+  if (!d_descs) return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: null descriptors");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (prec == TOBF_PREC_TF32X3) {
+    if (block_n == 128) return launch_conv<128, 0>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 0>(d_descs, n, total_tiles, sched, st);
+  } else if (prec == TOBF_PREC_BF16) {
+    if (block_n == 128) return launch_conv<128, 1>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 1>(d_descs, n, total_tiles, sched, st);
+  } else {
+    return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: unknown precision %d", prec);
+  }
+  return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: block_n must be 64 or 128");
 }
 
 extern "C" int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n,
                                  void* stream) {
-  if (n <= 0 || total_tiles <= 0) return TOBF_OK;
-  if (!d_descs) return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: null descriptors");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (block_n == 128) return launch_conv<128>(d_descs, n, total_tiles, st);
-  if (block_n == 64) return launch_conv<64>(d_descs, n, total_tiles, st);
-  return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: block_n must be 64 or 128");
+  return tobf_conv_grouped_ex(d_descs, n, total_tiles, block_n, TOBF_PREC_TF32X3, nullptr, stream);
 }
 
 #ifdef TOBF_CONV_PROF

@@ -27,7 +27,9 @@ import numpy as np
 import torch
 
 from .engine import cat_records, device
-from .executor import PlanTables, PopulationRun, compare_outputs, lower, plan_forward, trial_inputs
+from .refcompat import to_engine
+from .executor import (DEFAULT_TOL, PlanTables, PopulationRun, compare_outputs, lower, plan_forward, precision_code,
+                       trial_inputs)
 from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, decode, edit_distances, encode_labels, reward
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
@@ -100,11 +102,22 @@ class PopulationEvaluator:
     """
 
     def __init__(self, vanilla: Graph, evaluator: Evaluator | None = None, budget: float = 0.02, trials: int = 8,
-                 seed: int = 0, tol: float = 1e-5, eps: float = EPSILON, memo: dict | None = None, exchange=None):
+                 seed: int = 0, tol: float | None = None, eps: float = EPSILON, memo: dict | None = None,
+                 exchange=None, precision="fp32"):
+        """``precision``: conv arithmetic of the forward — 'fp32' (3xTF32, the
+        reference's 1e-5 verdict tolerance by default) or 'bf16' (BASELINE's
+        bf16 mode: verdicts at 2e-2 by default, SURVEY cfg4)."""
         self.ctx = device()
+        # the reference's own objects are welcome (refcompat.py)
+        vanilla = to_engine(vanilla)
+        self.prec = precision_code(precision)
+        tol = DEFAULT_TOL[self.prec] if tol is None else tol
         self.exchange = exchange  # dist.exchange_signatures when the population is sharded
         self.vanilla = vanilla
         self.ev = evaluator or Evaluator()
+        if not isinstance(self.ev.profile, DeviceProfile):  # a reference DeviceProfile / LeakageCase
+            self.ev = Evaluator(self.ev.predictors, to_engine(self.ev.case), self.ev.dim_regressors,
+                                to_engine(self.ev.profile))
         self.budget, self.trials, self.seed, self.tol, self.eps = budget, trials, seed, tol, eps
         self.memo = _SCHEDULE_CACHE if memo is None else memo
         self.truth = encode_labels(label_sequence(vanilla))
@@ -131,8 +144,8 @@ class PopulationEvaluator:
         if self.pool is None:
             from .hostpipe import HostPool, ParentRefs
             self.prefs = ParentRefs(self.vanilla)
-            self.vanilla_plan = plan_forward(self.lowered_vanilla, self.trials, self.prefs)
-            self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers)
+            self.vanilla_plan = plan_forward(self.lowered_vanilla, self.trials, self.prefs, self.prec)
+            self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers, self.prec)
 
     def receive(self, result: tuple, tables: PlanTables | None = None) -> None:
         """Parent side of one worker result, as soon as it arrives: fold in its
@@ -212,13 +225,14 @@ class PopulationEvaluator:
         ``first_seen``/``extra`` per micro-batch. ``base``: global index of
         ``plans[0]`` (default: contiguous shards in rank order)."""
         memo = self.memo if memo is None else memo
+        plans = to_engine(list(plans))
         t0 = time.perf_counter()
         if cands is None:
             cands = build_candidates(self.vanilla, plans, self.vanilla_analysis)
         t1 = time.perf_counter()
         feas = [i for i, c in enumerate(cands) if c.graph is not None]
         run = PopulationRun(self.ctx, [self.lowered_vanilla] + [lower(cands[i].graph, cands[i].analysis) for i in feas],
-                            reps=self.trials)
+                            reps=self.trials, prec=self.prec)
         t2 = time.perf_counter()
         if shard and self.exchange is not None:
             _candidate_traces(cands, self.ev.profile.name)
@@ -400,6 +414,7 @@ class PopulationEvaluator:
         then waits for the whole shard's host records."""
         memo = self.memo if memo is None else memo
         t_call = time.perf_counter()
+        plans = to_engine(list(plans))
         sharded = self.exchange is not None
         if not plans:
             self.last_host_ms = {}

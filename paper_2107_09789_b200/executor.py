@@ -352,7 +352,7 @@ class ForwardPlan:
     conv_k: np.ndarray
     ew: np.ndarray
     ew_level: np.ndarray
-    wimg: list      # (weight ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn)
+    wimg: list      # (weight ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec)
     affine: list    # BatchNorm weight ref
     const: list     # (constant ref, b0, channels, h, w, cp)
     arena_bytes: int
@@ -362,6 +362,7 @@ class ForwardPlan:
     flops_per_image: int
     gemm_act_bytes_per_image: int = 0   # conv/linear input + output activations, fp32, once each
     gemm_weight_bytes: int = 0          # conv/linear weights, fp32, once
+    prec: int = N.PREC_TF32X3           # conv arithmetic (N.PRECISIONS)
 
 
 def _plan_getstate(self) -> dict:
@@ -392,8 +393,9 @@ def _gemm_geom(lw: Lowered, op: Op, s_in: TensorShape):
     return s_in.height, s_in.width, _rup4(s_in.channels), j
 
 
-def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
-    """Descriptor rows of one lowered graph for ``reps`` stacked trials."""
+def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF32X3) -> ForwardPlan:
+    """Descriptor rows of one lowered graph for ``reps`` stacked trials, its
+    convs in precision ``prec`` (N.PREC_TF32X3 / N.PREC_BF16)."""
     graph, shapes, nodes = lw.graph, lw.shapes, lw.graph.nodes
     ishape = graph.input_shape
     batch = ishape.batch * reps
@@ -457,7 +459,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
             w_bytes += 4 * k1 * k2 * s_in.channels * j
             w = n.weights if op.w is None else op.w
             wi = index("wimg", (refs.ref(w), n.kind is K.Conv2D, s_in.height, s_in.width, s_in.channels,
-                                k1, k2, cp, j, bn))
+                                k1, k2, cp, j, bn, prec))
             epi = epi_rows(op.steps)
             conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
                               s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
@@ -497,7 +499,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs) -> ForwardPlan:
         ew_level=np.array(ew_lv, np.int32),
         wimg=tables["wimg"][1], affine=tables["affine"][1], const=tables["const"][1],
         arena_bytes=used, out_off=offs[lw.out_node], out_shape=shapes[lw.out_node], input_shape=ishape,
-        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes)
+        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes, prec=prec)
 
 
 def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, tables: dict) -> np.ndarray:
@@ -521,6 +523,17 @@ def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, 
 
 
 SPLITK_MAX = 16  # work units per tile at most
+
+
+def conv_sched(ctx: DeviceContext) -> torch.Tensor:
+    """The context's launch-wide conv tile-claim counters (2 x int32, zero
+    between launches: each launch's last CTA re-zeroes them). Every conv
+    launch of a context is ordered on its engine stream, so one pair serves
+    them all."""
+    t = ctx.__dict__.get("conv_sched")
+    if t is None:
+        t = ctx.conv_sched = torch.zeros(2, dtype=torch.int32, device=ctx.device)
+    return t
 
 
 def splitk_workspace(ctx: DeviceContext, floats: int, counters: int):
@@ -597,33 +610,33 @@ class PlanTables:
 
     def _wimg_ptr(self, entry: tuple) -> int:
         ctx, lib = self.ctx, self.ctx.lib
-        ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn = entry
+        ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec = entry
         w = self.refs.resolve(ref)
         if isinstance(w, DerivedWeight):
-            return self._derived_wimg_ptr(w, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn)
+            return self._derived_wimg_ptr(w, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec)
         wptr, st = ctx.cached_view(w)
         if is_conv:
             su, sv, sc, sn = st
         else:
             r, cstride = st
             su, sv, sc, sn = in_w * r, r, in_h * in_w * r, cstride
-        key = (wptr, su, sv, sc, sn, k1, k2, in_c, cp, j, bn)
+        key = (wptr, su, sv, sc, sn, k1, k2, in_c, cp, j, bn, prec)
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
             self.keep.append(hit)
             return hit.data_ptr()
-        nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
+        nbytes = lib.tobf_wimg_bytes_ex(k1, k2, cp, j, bn, prec)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
         ctx.wimg_bytes += nbytes
-        ctx.check(lib.tobf_pack_weights(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn, bn,
-                                        C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
+        ctx.check(lib.tobf_pack_weights_ex(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn, None, None, bn,
+                                           prec, C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack weights")
         ctx.launches += 1
         cache[key] = img
         self.keep.append(img)
         return img.data_ptr()
 
-    def _derived_wimg_ptr(self, w: DerivedWeight, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn) -> int:
+    def _derived_wimg_ptr(self, w: DerivedWeight, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec) -> int:
         """Weight image of a knob-derived weight, packed on the device straight
         from the resident vanilla array through the gather maps (derived.py);
         only the maps (a few KB) cross PCIe."""
@@ -635,7 +648,7 @@ class PlanTables:
             r, cstride = st
             H, W = w.hw
             su, sv, sc, sn = W * r, r, H * W * r, cstride
-        key = ("D", wptr, su, sv, sc, sn, w.key(), k1, k2, in_c, cp, j, bn)
+        key = ("D", wptr, su, sv, sc, sn, w.key(), k1, k2, in_c, cp, j, bn, prec)
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
@@ -649,12 +662,12 @@ class PlanTables:
         imaps = np.concatenate([mu, mv, mc, mn]).astype(np.int32)
         blob = ctx.upload_array(np.concatenate([imaps, np.concatenate([s_c, s_n]).astype(np.float32).view(np.int32)]))
         maps, scales = blob, blob[len(imaps):]
-        nbytes = lib.tobf_wimg_bytes(k1, k2, cp, j, bn)
+        nbytes = lib.tobf_wimg_bytes_ex(k1, k2, cp, j, bn, prec)
         img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
         ctx.wimg_bytes += nbytes
-        ctx.check(lib.tobf_pack_weights_gather(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn,
-                                               C.c_void_p(maps.data_ptr()), C.c_void_p(scales.data_ptr()), bn,
-                                               C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack derived weights")
+        ctx.check(lib.tobf_pack_weights_ex(C.c_void_p(wptr), k1, k2, in_c, cp, j, su, sv, sc, sn,
+                                           C.c_void_p(maps.data_ptr()), C.c_void_p(scales.data_ptr()), bn, prec,
+                                           C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack derived weights")
         ctx.launches += 1
         cache[key] = (img, maps, scales)  # maps stay alive until the (async) pack has run
         self.keep.append(img)
@@ -735,15 +748,20 @@ class PopulationRun:
 
     def __init__(self, ctx: DeviceContext, lowered: list[Lowered] | None, reps: int,
                  plans: list[ForwardPlan] | None = None, refs: ArrayRefs | None = None,
-                 tables: "PlanTables | None" = None):
+                 tables: "PlanTables | None" = None, prec: int = N.PREC_TF32X3):
         """``tables``: the plans' requirement tables already resolved (built
         incrementally while the plans arrive from host workers); resolved
-        here otherwise."""
+        here otherwise. ``prec``: conv arithmetic of plans built here (given
+        plans carry their own, and must agree)."""
         self.ctx = ctx
         self.reps = reps
         if plans is None:
             refs = ArrayRefs()
-            plans = [plan_forward(lw, reps, refs) for lw in lowered]
+            plans = [plan_forward(lw, reps, refs, prec) for lw in lowered]
+        precs = {p.prec for p in plans}
+        if len(precs) != 1:
+            raise ValueError(f"one run computes in one precision, got {sorted(precs)}")
+        self.prec = precs.pop()
         self.plans, self.refs = plans, refs
         ishape = plans[0].input_shape
         for p in plans:
@@ -809,9 +827,9 @@ class PopulationRun:
             bn = int(ckey[lo, 1])
             # split-K for groups too small to fill the SMs; workspace offsets
             # now, one workspace shared by every (stream-ordered) conv launch
-            ctx.check(lib.tobf_conv_prepare_split(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
-                                                  ctx.sms, SPLITK_MAX, None, None, C.byref(tot), C.byref(wsf),
-                                                  C.byref(cnts)), "conv prepare")
+            ctx.check(lib.tobf_conv_prepare_split_ex(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
+                                                     self.prec, ctx.sms, SPLITK_MAX, None, None, C.byref(tot),
+                                                     C.byref(wsf), C.byref(cnts)), "conv prepare")
             ws_need, cnt_need = max(ws_need, wsf.value), max(cnt_need, cnts.value)
             launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, bn))
         if ws_need:
@@ -853,12 +871,13 @@ class PopulationRun:
     def run(self) -> None:
         lib, sp = self.ctx.lib, C.c_void_p(self.ctx.sp)
         evs = self.conv_events
+        sched = C.c_void_p(conv_sched(self.ctx).data_ptr())
         for kind, dptr, n, tot, bn in self.launches:
             if kind == "conv":
                 if evs is not None:
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record()
-                rc = lib.tobf_conv_grouped(C.c_void_p(dptr), n, tot, bn, sp)
+                rc = lib.tobf_conv_grouped_ex(C.c_void_p(dptr), n, tot, bn, self.prec, sched, sp)
                 if evs is not None:
                     b.record()
                     evs.append((a, b))
@@ -904,13 +923,29 @@ def trial_inputs(shape: TensorShape, trials: int, seed: int) -> np.ndarray:
     return np.concatenate(xs, axis=0)
 
 
-def execute(graph: Graph, x: np.ndarray) -> np.ndarray:
+def precision_code(precision) -> int:
+    """'fp32' (3xTF32, the default) | 'bf16' -> N.PREC_*."""
+    if isinstance(precision, (int, np.integer)) and int(precision) in N.PRECISIONS.values():
+        return int(precision)
+    try:
+        return N.PRECISIONS[precision]
+    except KeyError:
+        raise ValueError(f"precision must be one of {sorted(N.PRECISIONS)}, got {precision!r}") from None
+
+
+#: equivalence tolerance of each precision when the caller gives none: the
+#: reference's tol (interpreter.py:93) in fp32, BASELINE's 2e-2 in bf16 mode
+DEFAULT_TOL = {N.PREC_TF32X3: 1e-5, N.PREC_BF16: 2e-2}
+
+
+def execute(graph: Graph, x: np.ndarray, *, precision="fp32") -> np.ndarray:
     """Run ``graph`` on ``x`` (NCHW float32) on the GPU; returns the output node's
-    tensor as a numpy array (interpreter.py:75-90)."""
+    tensor as a numpy array (interpreter.py:75-90). ``precision='bf16'``:
+    convs in the bf16 mode (tolerance 2e-2 against the fp32 reference)."""
     if tuple(x.shape) != graph.input_shape.as_tuple():
         raise ShapeMismatch(-1, f"input shape {x.shape} != {graph.input_shape.as_tuple()}")
     ctx = device()
-    run = PopulationRun(ctx, [lower(graph)], reps=1)
+    run = PopulationRun(ctx, [lower(graph)], reps=1, prec=precision_code(precision))
     xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(ctx.device)
     run.set_input(xd)
     run.run()
@@ -920,7 +955,7 @@ def execute(graph: Graph, x: np.ndarray) -> np.ndarray:
 
 
 def equivalence_check(g1: Graph, g2: Graph, trials: int = 8, seed: int = 0,
-                      tol: float = 1e-5) -> tuple[bool, float]:
+                      tol: float | None = None, *, precision="fp32") -> tuple[bool, float]:
     """Seeded random-input functional comparison (interpreter.py:93-118): both
     graphs run all ``trials`` inputs stacked in one batch; verdict and worst
     relative difference use the reference's float32 formulas bit for bit."""
@@ -930,7 +965,7 @@ def equivalence_check(g1: Graph, g2: Graph, trials: int = 8, seed: int = 0,
     out2 = shape_map(g2)[g2.output_id]
     if out1 != out2:
         raise ShapeMismatch(-1, f"output shapes differ: {out1} vs {out2}")
-    res = evaluate_equivalence(g1, [g2], trials=trials, seed=seed, tol=tol)
+    res = evaluate_equivalence(g1, [g2], trials=trials, seed=seed, tol=tol, precision=precision)
     return bool(res[0][0]), float(res[1][0])
 
 
@@ -965,12 +1000,15 @@ def compare_outputs(ctx: DeviceContext, run: PopulationRun, ref_index: int, cand
 
 
 def evaluate_equivalence(reference: Graph, candidates: list[Graph], trials: int = 8, seed: int = 0,
-                         tol: float = 1e-5):
+                         tol: float | None = None, *, precision="fp32"):
     """Batched equivalence_check(reference, c) for every candidate c: one
     forward of the reference and of all candidates on the stacked trials.
-    Returns (ok[np.bool_], worst[np.float64]) per candidate."""
+    Returns (ok[np.bool_], worst[np.float64]) per candidate. ``tol`` defaults
+    to the precision's (DEFAULT_TOL)."""
     ctx = device()
-    run = PopulationRun(ctx, [lower(reference)] + [lower(g) for g in candidates], reps=trials)
+    prec = precision_code(precision)
+    tol = DEFAULT_TOL[prec] if tol is None else tol
+    run = PopulationRun(ctx, [lower(reference)] + [lower(g) for g in candidates], reps=trials, prec=prec)
     x = trial_inputs(reference.input_shape, trials, seed)
     run.set_input(torch.from_numpy(x).to(ctx.device))
     run.run()

@@ -110,8 +110,9 @@ class ParentRefs(ArrayRefs):
 _W: dict = {}
 
 
-def _worker_init(vanilla: Graph, reps: int, pname: str) -> None:
+def _worker_init(vanilla: Graph, reps: int, pname: str, prec: int = 0) -> None:
     _W["vanilla"] = vanilla
+    _W["prec"] = prec
     _W["analysis"] = analyze(vanilla)
     _W["reps"] = reps
     _W["pname"] = pname
@@ -126,14 +127,14 @@ LAZY_KNOBS = os.environ.get("TOBF_EAGER_KNOBS", "") != "1"
 
 
 def encode_candidate(cand: int, plan: ObfuscationPlan, vanilla: Graph, vanilla_analysis, reps: int, pname: str,
-                     roots: dict, sent_sigs: set | None = None):
+                     roots: dict, sent_sigs: set | None = None, prec: int = 0):
     """(cand, error, payload): payload = (ForwardPlan, CandidateTrace, new arrays)."""
     try:
         g, d, ana = apply_plan_analyzed(vanilla, plan, vanilla_analysis, lazy=LAZY_KNOBS)
     except TransformError as exc:
         return cand, str(exc), None
     refs = WorkerRefs(roots, cand)
-    fp = plan_forward(lower(g, ana), reps, refs)
+    fp = plan_forward(lower(g, ana), reps, refs, prec)
     ct, _, _ = trace_records(g, d.fusion_limits, d.schedule_strategies, pname, ana)
     if sent_sigs is not None:
         ct = ct.compact(sent_sigs)
@@ -155,14 +156,14 @@ def plan_unwire(w: tuple) -> ObfuscationPlan:
 
 def _worker_job(job: list[tuple[int, tuple]]) -> list:
     return [encode_candidate(c, plan_unwire(p), _W["vanilla"], _W["analysis"], _W["reps"], _W["pname"],
-                             _W["roots"], _W["sent_sigs"]) for c, p in job]
+                             _W["roots"], _W["sent_sigs"], _W["prec"]) for c, p in job]
 
 
 def _worker_main(rfd: int, wfd: int) -> None:
     rconn = Connection(rfd, writable=False)
     wconn = Connection(wfd, readable=False)
-    vanilla, reps, pname = rconn.recv()
-    _worker_init(vanilla, reps, pname)
+    vanilla, reps, pname, prec = rconn.recv()
+    _worker_init(vanilla, reps, pname, prec)
     while True:
         msg = rconn.recv()
         if msg is None:
@@ -181,7 +182,7 @@ class HostPool:
     jobs in order, so a result is received on the parent's thread exactly
     when it is needed."""
 
-    def __init__(self, vanilla: Graph, reps: int, pname: str, workers: int | None = None):
+    def __init__(self, vanilla: Graph, reps: int, pname: str, workers: int | None = None, prec: int = 0):
         n = workers if workers is not None else default_workers()
         self.workers = n
         self.procs, self.wconns, self.rconns = [], [], []
@@ -202,7 +203,7 @@ class HostPool:
             self.wconns.append(Connection(to_w, readable=False))
             self.rconns.append(Connection(from_r, writable=False))
         for c in self.wconns:
-            c.send((vanilla, reps, pname))
+            c.send((vanilla, reps, pname, prec))
         self._next = 0
         self._jid = 0
         self._done: dict[int, list] = {}

@@ -2,7 +2,7 @@
 
 The capture (run on the GPU box, one GPU):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      --clock-control none --print-units base -k regex:conv_tf32x3 --launch-skip S -c L --csv \
+      --clock-control none --print-units base -k regex:conv_tc_kernel --launch-skip S -c L --csv \
       --log-file gpurun_out/conv_traffic.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-sweeps
 where L = conv launches per step and S = L (skip the warm-up step).
 usage: python scripts/conv_traffic.py gpurun_out/conv_traffic.csv FLOPS_PER_STEP L

@@ -1,4 +1,4 @@
-"""Development aid: per-role warp-stall breakdown of a conv_tf32x3 ncu capture
+"""Development aid: per-role warp-stall breakdown of a conv_tc_kernel ncu capture
 (source page), roles delimited by the setmaxnreg / UTCHMMA landmarks."""
 import csv
 import subprocess

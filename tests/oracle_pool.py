@@ -39,6 +39,20 @@ def equiv_job(plan):
     return IR.equivalence_check(_S["vanilla"], og, trials=_S["trials"], seed=_S["seed"])
 
 
+def equiv64_job(plan):
+    """equivalence_check's `worst` in float64 arithmetic (the exact-arithmetic
+    yardstick) on the same float32 inputs."""
+    from oracle import interp_ref as IR
+    from paper_2107_09789_b200.knobs import apply_plan
+    og, _ = apply_plan(_S["vanilla"], plan)
+    worst = 0.0
+    for x in IR.trial_inputs(tuple(_S["vanilla"].input_shape.as_tuple()), _S["trials"], _S["seed"]):
+        a = IR.execute(_S["vanilla"], x, dtype=np.float64)
+        b = IR.execute(og, x, dtype=np.float64)
+        worst = max(worst, float((np.abs(a - b) / (1.0 + np.abs(b))).max()))
+    return worst
+
+
 def equiv_trial_job(args):
     """One (plan, trial index) of equivalence_check (interpreter.py:110-117):
     returns (worst, ok) of that trial so the parent folds them in trial order.

@@ -418,3 +418,81 @@ def test_weight_cache_eviction_is_exact(ctx):
     finally:
         ctx.weight_cache_limit = saved
         ctx.clear_cache()
+
+
+# ----------------------------------------------------------------- bf16 mode
+BF16_TOL = 2e-2  # BASELINE north_star: outputs within 2e-2 of the fp32 reference in bf16 mode
+
+
+def _bf16(a: np.ndarray) -> np.ndarray:
+    """Round to bf16 (nearest even), as float64."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_kernel_bf16(ctx, case):
+    """kind::f16 conv: (1) exactly bf16 weights times the activation pair
+    a_hi + a_lo, accumulated in fp32 (against fp64 arithmetic on those
+    operands, normalised by the magnitude of the products), (2) within 2e-2
+    of the fp32 oracle."""
+    b, c, h, w, j, k, s, p = case
+    rng = np.random.default_rng(hash(case) % 2**32 + 1)
+    x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+    wt = (rng.standard_normal((k, k, c, j)) * np.sqrt(2.0 / (k * k * c))).astype(np.float32)
+    from paper_2107_09789_b200.ir import Graph, Node, OperatorKind, TensorShape
+    g = Graph({0: Node(0, OperatorKind.Conv2D, {"k1": k, "k2": k, "c": c, "j": j, "stride": s, "padding": p}, wt, [])},
+              0, TensorShape(b, c, h, w))
+    got = executor.execute(g, x, precision="bf16").astype(np.float64)
+    xh = _bf16(x)
+    xpair = xh + _bf16(x - xh.astype(np.float32))  # the activation pair a_hi + a_lo the kernel multiplies
+    exact_bf = IR.conv2d(xpair, _bf16(wt), s, p)
+    mag = IR.conv2d(np.abs(xpair), np.abs(_bf16(wt)), s, p)
+    assert float(np.max(np.abs(got - exact_bf) / (1.0 + mag))) <= 1e-5
+    ref = IR.conv2d(x, wt, s, p).astype(np.float64)
+    assert _rel(got, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("name,mode,size", [("c1c2", "dimension", 24), ("resnet18", "sequence", 64),
+                                            ("vgg16", "dimension", 32)])
+def test_execute_bf16_matches_fp32_oracle(ctx, name, mode, size):
+    """Whole obfuscated graphs in bf16 mode: outputs within 2e-2 of the fp32
+    oracle; bf16-mode verdicts (tol 2e-2) equal the oracle's at 2e-2."""
+    kw = {"hidden": 256} if name == "vgg16" else {}
+    g = fixtures.FIXTURES[name](size=size, **kw)
+    x = np.random.default_rng(6).standard_normal(g.input_shape.as_tuple()).astype(np.float32)
+    plans = _plans(g, mode, 3, seed=13)
+    cands = [knobs.apply_plan(g, p)[0] for p in plans]
+    for og in cands:
+        got = executor.execute(og, x, precision="bf16")
+        assert _rel(got, IR.execute(og, x).astype(np.float64)) <= BF16_TOL
+    ok, worst = executor.evaluate_equivalence(g, cands, trials=2, seed=0, precision="bf16")
+    for i, og in enumerate(cands):
+        rok, rworst = IR.equivalence_check(g, og, trials=2, seed=0, tol=BF16_TOL)
+        assert bool(ok[i]) == rok and worst[i] <= BF16_TOL, (i, ok[i], worst[i], rok, rworst)
+
+
+def test_bf16_population_records(ctx):
+    """PopulationEvaluator(precision='bf16'): trace, T, LER and R are the
+    precision-independent oracle values; verdicts at the bf16 tolerance."""
+    g = fixtures.vgg16(size=32, hidden=256)
+    plans = _plans(g, "dimension", 4, seed=8)
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
+    pe = PopulationEvaluator(g, ev, budget=0.02, trials=2, seed=0, memo={}, precision="bf16")
+    try:
+        rec = pe.evaluate_records(plans, micro=2, memo={}, workers=2)
+    finally:
+        pe.close()
+    truth = fitness.encode_labels(label_sequence(g))
+    memo = CM.ScheduleMemo()
+    t_star = CM.profile_pipeline(g, "default", None, None, CM.ScheduleMemo())[3]
+    for i, p in enumerate(plans):
+        og, d = knobs.apply_plan(g, p)
+        _, _, rows, T = CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)
+        ok, _ = IR.equivalence_check(g, og, trials=2, seed=0, tol=BF16_TOL)
+        assert rec["latency"][i] == T and bool(rec["ok"][i]) == ok, i
+        feats = np.array([[r[f] for f in CM.FEATURES] for r in rows])
+        lers = [FR.ler(FR.lstm_ctc(feats, 9, pr.weights()), truth) for pr in ev.predictors]
+        R, mean = FR.eq10(lers, T, ok, t_star, 0.02)
+        assert rec["mean_ler"][i] == mean and rec["reward"][i] == R, i
