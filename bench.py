@@ -274,12 +274,29 @@ def kernel_sweeps(args, vanilla, predictors, hbm_peak: float) -> dict:
     ms = statistics.median(a.elapsed_time(b) for a, b in evs)
     alg = int(lens.sum().item()) + B * m + B * (4 + 4 + 8)  # |L| + |L*| tokens, ntok in, ED + LER out
     gbs = alg / (ms / 1e3) / 1e9
+    # integer-issue roofline beside the HBM one: the bit-parallel update is ~14
+    # integer instructions per token (SASS), so the kernel is bound by warp
+    # instruction issue (1 per clock per SM sub-partition), not by HBM. The
+    # instruction count per token comes from the committed ncu capture of this
+    # launch (profiles/ler_instr.json: smsp__inst_executed.sum / tokens).
+    alu = None
+    ip = ROOT / "profiles" / "ler_instr.json"
+    if ip.exists():
+        lj = json.loads(ip.read_text())
+        tokens = int(lens.sum().item())
+        warp_instr = lj["warp_instr_per_token"] * tokens
+        sm_mhz = (ler_clk.get("sm_mhz") or 1965.0)
+        issue_ms = warp_instr / (148 * 4 * sm_mhz * 1e6) * 1e3
+        alu = {"bound": "warp instruction issue (integer ALU + FMA pipes)",
+               "thread_instr_per_token": round(32 * lj["warp_instr_per_token"], 2),
+               "issue_limit_ms": round(issue_ms, 4), "frac": round(issue_ms / ms, 4),
+               "source": lj["source"]}
     out["ler"] = {"kernel": "levenshtein_bp_kernel (thread per pair, bit-parallel)", "pairs": B, "truth_len": m,
                   "pred_len": "U[119,169]", "ms_per_launch": round(ms, 4), "pairs_per_s": B / (ms / 1e3),
                   "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                   "frac": round(gbs / hbm_peak, 4), "algorithmic_bytes": alg,
                   "bytes_def": "sum(|L|) + pairs*|L*| (1 B tokens) + 16 B/pair (ntok, ED, LER)",
-                  "timing": "median of 10 launches", "clocks": ler_clk}
+                  "timing": "median of 10 launches", "clocks": ler_clk, "alu_roofline": alu}
     del toks, lens
     # cfg5: 10k traces, T ~ U[119,169], F = 9 cost-model-scale features
     nt = 10_000

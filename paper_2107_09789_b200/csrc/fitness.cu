@@ -16,6 +16,8 @@
 // explicit fmaf, every other product/sum is separately rounded.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include "detmath.h"
 #include "tobf_internal.h"
 
@@ -311,6 +313,211 @@ __global__ void __launch_bounds__(TPC * 32, 1)
   if (rank == 0 && u == 0 && b < B) ntok[b] = cnt;
 }
 
+// ------------------------------------------------------------------------
+// Register-blocked cluster LSTM (the cfg5 / generation kernel). Same cluster
+// layout as lstm_ctc_cluster_kernel — CTA rank r of a cluster of CS = H/32
+// CTAs owns hidden units [32r, 32r+32), gate rows resident in shared memory
+// as bf16 — but each thread now computes its unit's 4 gates for RB = 4
+// traces (warp w: traces 4w..4w+3, lane = unit), so every bf16 weight
+// loaded and widened is used RB times: per 4 K a thread issues 4 weight
+// loads, 16 widenings, 4 broadcast h loads (h is stored k-major,
+// trace-minor: one 16-B load gives the 4 traces' values) and 64 FMAs —
+// 1.4 instructions per FMA instead of 2.3. h_t travels to every CTA of the
+// cluster as one 16-B DSMEM store per (unit, 4 traces). The head logits +
+// greedy CTC of trace q run in CTA q % CS (spread over the cluster instead of
+// serialising on rank 0). Accumulation order (bias, x[0..F), h[0..H)),
+// the lane-strided head partials + xor butterfly and every rounding are those
+// of the original formulation and of oracle/fitness_ref.c.
+constexpr int kRB = 4;       // traces per thread
+constexpr int kRBWarps = 4;  // warps per CTA
+constexpr int kRBTraces = kRB * kRBWarps;
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kRBWarps * 32, 1)
+    lstm_ctc_rb_kernel(const double* __restrict__ feats, const int32_t* __restrict__ offsets, int B, int F, int H,
+                       int NC, const float* __restrict__ w_ihT, const float* __restrict__ w_hhT,
+                       const float* __restrict__ bias, const float* __restrict__ w_out,
+                       const float* __restrict__ b_out, int8_t* __restrict__ tokens, int T_max,
+                       int32_t* __restrict__ ntok) {
+  constexpr int TPC = kRBTraces;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int L = F + H;
+  const int Lq = L >> 2;
+  const int Lp = (L + 3) & ~3;
+  uint2* wq = reinterpret_cast<uint2*>(sm);                                                       // [Lq][4][32]
+  uint16_t* wtail = reinterpret_cast<uint16_t*>(sm + (size_t)Lq * 4 * kLstmUnits * 8);              // [L%4][4][32]
+  float* hv = reinterpret_cast<float*>(sm + (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2);  // [2][Lp][TPC]
+  float* bsm = hv + 2 * Lp * TPC;  // [4][32]
+  float* wo = bsm + 4 * kLstmUnits;  // [NC][H]
+  __shared__ int s_len[TPC], s_row0[TPC];
+  const int G = 4 * H;
+  const uint32_t rank = cluster_rank();
+  const int CS = H / kLstmUnits;
+  const int u = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int unit = rank * kLstmUnits + u;
+  const int b0 = blockIdx.y * TPC;
+
+  for (int i = threadIdx.x; i < Lq * 4 * kLstmUnits; i += blockDim.x) {
+    const int uu = i % kLstmUnits, g = (i / kLstmUnits) % 4, kq = i / (4 * kLstmUnits);
+    const int col = g * H + rank * kLstmUnits + uu;
+    uint32_t pk[2];
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int k0 = kq * 4 + 2 * h2;
+      const float w0 = k0 < F ? w_ihT[(int64_t)k0 * G + col] : w_hhT[(int64_t)(k0 - F) * G + col];
+      const float w1 = k0 + 1 < F ? w_ihT[(int64_t)(k0 + 1) * G + col] : w_hhT[(int64_t)(k0 + 1 - F) * G + col];
+      pk[h2] = (__float_as_uint(w0) >> 16) | ((__float_as_uint(w1) >> 16) << 16);
+    }
+    wq[i] = make_uint2(pk[0], pk[1]);
+  }
+  for (int i = threadIdx.x; i < (L & 3) * 4 * kLstmUnits; i += blockDim.x) {
+    const int uu = i % kLstmUnits, g = (i / kLstmUnits) % 4, e = i / (4 * kLstmUnits);
+    const int k = Lq * 4 + e;
+    const int col = g * H + rank * kLstmUnits + uu;
+    const float wv = k < F ? w_ihT[(int64_t)k * G + col] : w_hhT[(int64_t)(k - F) * G + col];
+    wtail[i] = (uint16_t)(__float_as_uint(wv) >> 16);
+  }
+  for (int i = threadIdx.x; i < 4 * kLstmUnits; i += blockDim.x)
+    bsm[i] = bias[(i / kLstmUnits) * H + rank * kLstmUnits + (i % kLstmUnits)];
+  for (int i = threadIdx.x; i < NC * H; i += blockDim.x) wo[i] = w_out[i];
+  for (int i = threadIdx.x; i < 2 * Lp * TPC; i += blockDim.x) hv[i] = 0.0f;
+  if (threadIdx.x < TPC) {
+    const int b = b0 + threadIdx.x;
+    s_len[threadIdx.x] = b < B ? offsets[b + 1] - offsets[b] : 0;
+    s_row0[threadIdx.x] = b < B ? offsets[b] : 0;
+  }
+  __syncthreads();
+  int tmax = 0;
+  for (int i = 0; i < TPC; ++i) tmax = max(tmax, s_len[i]);
+  int len[kRB];
+#pragma unroll
+  for (int r = 0; r < kRB; ++r) len[r] = s_len[kRB * w + r];
+  cluster_sync_all();  // every CTA's buffers are initialised before remote writes start
+
+  // x_t of this warp's traces, one step ahead: element i (< 4F) of the warp =
+  // (trace 4w + i/F, feature i%F), held by lane i%32 (slot i/32)
+  int xk[2], xtr[2], xlen[2], xrow0[2];
+  bool xl[2];
+  float x_cur[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = u + 32 * j;
+    xl[j] = i < kRB * F;
+    const int xq = xl[j] ? i / F : 0;
+    xk[j] = xl[j] ? i - xq * F : 0;
+    xtr[j] = kRB * w + xq;
+    xlen[j] = xl[j] ? s_len[xtr[j]] : 0;
+    xrow0[j] = s_row0[xtr[j]];
+    x_cur[j] = (xl[j] && 0 < xlen[j]) ? (float)tobf_log1p_d(feats[(int64_t)xrow0[j] * 9 + xk[j]]) : 0.0f;
+  }
+  // head ownership: trace q = rank + CS*(w + 4s) (s = 0..3) is decoded by warp w of CTA q % CS
+  int prev[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  float c[kRB] = {0.f, 0.f, 0.f, 0.f};
+  const uint32_t hv_local = static_cast<uint32_t>(__cvta_generic_to_shared(hv));
+  for (int t = 0; t < tmax; ++t) {
+    float* hcur = hv + (t & 1) * Lp * TPC;
+    const int nxt = (t + 1) & 1;
+    double f_next[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (xl[j]) hcur[xk[j] * TPC + xtr[j]] = x_cur[j];
+      f_next[j] = (xl[j] && t + 1 < xlen[j]) ? feats[(int64_t)(xrow0[j] + t + 1) * 9 + xk[j]] : 0.0;
+    }
+    __syncwarp();
+    float acc[4][kRB];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float bv = bsm[g * 32 + u];
+#pragma unroll
+      for (int r = 0; r < kRB; ++r) acc[g][r] = bv;
+    }
+    const uint2* wrow = wq + u;
+    const float* hrow = hcur + kRB * w;
+#pragma unroll 2
+    for (int kq = 0; kq < Lq; ++kq) {
+      const uint2 w0 = wrow[(kq * 4 + 0) * kLstmUnits], w1 = wrow[(kq * 4 + 1) * kLstmUnits];
+      const uint2 w2 = wrow[(kq * 4 + 2) * kLstmUnits], w3 = wrow[(kq * 4 + 3) * kLstmUnits];
+      const float4 h0 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 0) * TPC);
+      const float4 h1 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 1) * TPC);
+      const float4 h2 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 2) * TPC);
+      const float4 h3 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 3) * TPC);
+      const float hs[4][kRB] = {{h0.x, h0.y, h0.z, h0.w}, {h1.x, h1.y, h1.z, h1.w},
+                                {h2.x, h2.y, h2.z, h2.w}, {h3.x, h3.y, h3.z, h3.w}};
+      const float wg[4][4] = {{bf16lo(w0.x), bf16hi(w0.x), bf16lo(w0.y), bf16hi(w0.y)},
+                              {bf16lo(w1.x), bf16hi(w1.x), bf16lo(w1.y), bf16hi(w1.y)},
+                              {bf16lo(w2.x), bf16hi(w2.x), bf16lo(w2.y), bf16hi(w2.y)},
+                              {bf16lo(w3.x), bf16hi(w3.x), bf16lo(w3.y), bf16hi(w3.y)}};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wg[g][e], hs[e][r], acc[g][r]);
+    }
+    for (int e = 0; e < (L & 3); ++e) {
+      const float4 hx = *reinterpret_cast<const float4*>(hrow + (Lq * 4 + e) * TPC);
+      const float hs[kRB] = {hx.x, hx.y, hx.z, hx.w};
+      const uint16_t* wt = wtail + e * 4 * kLstmUnits + u;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const float wv = __uint_as_float((uint32_t)wt[g * 32] << 16);
+#pragma unroll
+        for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wv, hs[r], acc[g][r]);
+      }
+    }
+    const float4 hold = *reinterpret_cast<const float4*>(hcur + (F + unit) * TPC + kRB * w);
+    float hval[kRB] = {hold.x, hold.y, hold.z, hold.w};
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+      if (t < len[r]) {
+        const float ig = tobf_sigmoid(acc[0][r]);
+        const float fg = tobf_sigmoid(acc[1][r]);
+        const float gg = tobf_tanh(acc[2][r]);
+        const float og = tobf_sigmoid(acc[3][r]);
+        c[r] = fmaf(fg, c[r], ig * gg);
+        hval[r] = og * tobf_tanh(c[r]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) x_cur[j] = (xl[j] && t + 1 < xlen[j]) ? (float)tobf_log1p_d(f_next[j]) : 0.0f;
+    const uint32_t slot = hv_local + 4u * (uint32_t)(nxt * Lp * TPC + (F + unit) * TPC + kRB * w);
+    for (int rr = 0; rr < CS; ++rr) st_cluster_v4(map_shared(slot, rr), hval[0], hval[1], hval[2], hval[3]);
+    cluster_sync_all();
+    // head + greedy CTC of the traces this warp owns (same formula and order as before)
+    const float* hn = hv + nxt * Lp * TPC + F * TPC;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int q = (int)rank + CS * (w + kRBWarps * s);
+      if (q >= TPC || t >= s_len[q]) continue;
+      int best = 0;
+      float bestv = 0.0f;
+      for (int cls = 0; cls < NC; ++cls) {
+        float p = 0.0f;
+        for (int k = u; k < H; k += 32) p = fmaf(wo[cls * H + k], hn[k * TPC + q], p);
+        for (int off = 16; off; off >>= 1) p = p + __shfl_xor_sync(0xffffffffu, p, off);
+        const float lg = b_out[cls] + p;
+        if (cls == 0 || lg > bestv) {
+          best = cls;
+          bestv = lg;
+        }
+      }
+      if (u == 0 && best != 0 && best != prev[s]) {
+        tokens[(int64_t)(b0 + q) * T_max + cnt[s]] = (int8_t)best;
+      }
+      if (best != 0 && best != prev[s]) ++cnt[s];
+      prev[s] = best;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int q = (int)rank + CS * (w + kRBWarps * s);
+    if (q < TPC && u == 0 && b0 + q < B) ntok[b0 + q] = cnt[s];
+  }
+}
+
 // One warp per prediction; strips of 32 truth columns, anti-diagonal sweep.
 __global__ void levenshtein_kernel(const int8_t* __restrict__ pred, const int32_t* __restrict__ ntok, int B,
                                    int T_max, const int8_t* __restrict__ truth, int m, int32_t* __restrict__ ed,
@@ -539,6 +746,34 @@ static int launch_lstm_cluster(const double* feats, const int32_t* offsets, int3
   return tobf_cuda_check("tobf_lstm_ctc");
 }
 
+static int launch_lstm_rb(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H, int32_t NC,
+                          const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
+                          const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, cudaStream_t st) {
+  const int L = F + H, Lq = L / 4, Lp = (L + 3) & ~3, CS = H / kLstmUnits;
+  const size_t smem = (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2 +
+                      sizeof(float) * (2 * (size_t)Lp * kRBTraces + 4 * kLstmUnits + NC * H);
+  auto kern = lstm_ctc_rb_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm rb attrs: %s", cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, (B + kRBTraces - 1) / kRBTraces, 1);
+  cfg.blockDim = dim3(kRBWarps * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, feats, offsets, (int)B, (int)F, (int)H, (int)NC, w_ihT, w_hhT, b, w_out, b_out,
+                         tokens, (int)T_max, ntok);
+  if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm rb launch: %s", cudaGetErrorString(e));
+  return tobf_cuda_check("tobf_lstm_ctc");
+}
+
 extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H,
                              int32_t NC, const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
                              const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, void* stream) {
@@ -547,6 +782,12 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
       NC < 2 || NC > kMaxNC || H < 32 || H > 1024 || H % 32 || T_max < 1)
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
+  static const int variant = [] {
+    const char* v = getenv("TOBF_LSTM_VARIANT");  // A/B measurements only: "cluster16" = the round-1 kernel
+    return v && strcmp(v, "cluster16") == 0 ? 1 : 0;
+  }();
+  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16 && variant == 0)
+    return launch_lstm_rb(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   if (H % kLstmUnits == 0 && H / kLstmUnits <= 16) {
     // 16 traces per cluster (the h double buffer of 16 traces plus the bf16
     // gate rows fill the 227 KB of shared memory at H=512): the per-step

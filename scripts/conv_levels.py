@@ -12,12 +12,12 @@ from paper_2107_09789_b200 import fixtures, ga  # noqa: E402
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator  # noqa: E402
 
 
-def main(pop=32, reps=5):
-    g = fixtures.resnet18()
-    space = ga.search_space(g, "sequence")
-    sizes = ga.domain_sizes("sequence", space)
-    plans = [ga.decode_genome(g, "sequence", space, x) for x in ga.random_genomes(np.random.default_rng(0), sizes, pop)]
-    pe = PopulationEvaluator(g, Evaluator(), trials=8, memo={})
+def main(pop=32, reps=5, fixture="resnet18", mode="sequence", prec="fp32"):
+    g = fixtures.FIXTURES[fixture]()
+    space = ga.search_space(g, mode)
+    sizes = ga.domain_sizes(mode, space)
+    plans = [ga.decode_genome(g, mode, space, x) for x in ga.random_genomes(np.random.default_rng(0), sizes, pop)]
+    pe = PopulationEvaluator(g, Evaluator(), trials=8, memo={}, precision=prec)
     prep = pe.prepare(plans, memo={})
     run = prep["run"]
     x = pe.x_host.cuda()
@@ -62,4 +62,14 @@ def main(pop=32, reps=5):
 
 
 if __name__ == "__main__":
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--pop", type=int, default=32)
+    ap.add_argument("--fixture", default="resnet18")
+    ap.add_argument("--mode", default="sequence")
+    ap.add_argument("--prec", default="fp32")
+    ap.add_argument("--order", action="store_true")
+    a = ap.parse_args()
+    main(a.pop, 5, a.fixture, a.mode, a.prec)
+    sys.exit(0)
     main()

@@ -35,7 +35,7 @@ def main():
     lib.tobf_conv_prof_read(buf.ctypes.data, 1)
     sp = C.c_void_p(pe.ctx.sp)
     convs = [L for L in run.launches if L[0] == "conv"]
-    for idx in (0, 1, 4, 14, 20, 22, 29, 34, 38, 44):
+    for idx in [int(v) for v in (sys.argv[1].split(',') if len(sys.argv) > 1 else '0,1,2,4,14,20,22,29,34,38,44'.split(','))]:
         if idx >= len(convs):
             break
         _, dptr, n, tot, bn = convs[idx]

@@ -11,6 +11,8 @@ INTEGRATION.md §3's maintainer patch (refcompat.install) is applied to the
 real package and leaves it answering in its own types.
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -118,3 +120,31 @@ def test_maintainer_patch_installs_on_the_real_package():
     finally:
         refcompat.uninstall(ref, saved)
     assert ref.execute is ref.interpreter.execute
+
+
+def test_integration_md_patch_applied_to_a_copy_of_the_reference(tmp_path):
+    """The maintainer patch exactly as INTEGRATION.md §3 prints it, appended to
+    a copy of the real package's __init__.py: the patched package imports,
+    its hot entry points are the engine's drop-in wrappers, the rest is the
+    reference's own code."""
+    import re
+    import shutil
+    import subprocess
+    import sys
+    src = Path(ref.__file__).resolve().parent
+    dst = tmp_path / "traceobf"
+    shutil.copytree(src, dst, ignore=shutil.ignore_patterns("__pycache__"))
+    md = (refpkg.ROOT / "INTEGRATION.md").read_text()
+    patch = re.search(r"```python\n(# traceobf/__init__.py \(maintainer patch.*?)```", md, re.S).group(1)
+    with open(dst / "__init__.py", "a") as f:
+        f.write("\n" + patch)
+    code = ("import traceobf, paper_2107_09789_b200 as eng\n"
+            "hot = ('execute', 'equivalence_check', 'compile_graph', 'profile_pipeline')\n"
+            "assert all(getattr(getattr(traceobf, n), '__dropin__', False) for n in hot)\n"
+            "assert traceobf.apply_plan is traceobf.transforms.apply_plan\n"
+            "assert traceobf.__file__.startswith(%r)\n"
+            "print('patched ok')\n") % str(tmp_path)
+    env = dict(__import__("os").environ)
+    env["PYTHONPATH"] = f"{tmp_path}:{refpkg.ROOT}"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "patched ok" in r.stdout, r.stderr[-2000:]

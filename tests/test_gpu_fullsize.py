@@ -120,7 +120,6 @@ def test_cfg2_headline_population_matches_oracle(ctx):
         exact = dict(zip(split, pool.map(oracle_pool.equiv64_job, [plans[i] for i in split], chunksize=1)))
     finally:
         pool.close()
-    assert len(split) <= len(plans) // 8, split
     assert pe.t_star == t_star
     assert sum(o["feasible"] for o in want) == len(feas) >= 24
     for i, o in enumerate(want):
@@ -134,8 +133,13 @@ def test_cfg2_headline_population_matches_oracle(ctx):
         assert rec["latency"][i] == o["T"], i
         assert abs(float(rec["worst"][i]) - o["worst"]) <= FP32_TOL, (i, rec["worst"][i], o["worst"])
         if i in exact:
+            # measured at RN18 224x224: about half the candidates, e.g. the trial
+            # whose top softmax probability is 0.80 gives fp32-oracle worst 3.2e-5
+            # against an exact worst of ~1e-23 (function-preserving); the GPU's
+            # verdict is exact arithmetic's
             w64 = exact[i]
             assert abs(w64 - 1e-5) < abs(o["worst"] - w64), (i, rec["worst"][i], o["worst"], w64)
+            assert bool(rec["ok"][i]) == (w64 <= 1e-5), (i, rec["worst"][i], o["worst"], w64)
             o["ok"] = bool(rec["ok"][i])  # the rounding-decided verdict: Eq. 10 below follows the GPU's
             o["R"], o["mean"] = FR.eq10(o["lers"], o["T"], o["ok"], t_star, 0.02)
         assert bool(rec["ok"][i]) == o["ok"], i
@@ -147,10 +151,10 @@ def test_cfg2_headline_population_matches_oracle(ctx):
         assert rec["mean_ler"][i] == o["mean"] and rec["reward"][i] == o["R"], i
     # outputs of a few candidates on trial 0 against the oracle (softmax and logits)
     x0 = IR.trial_inputs(g.input_shape.as_tuple(), 1, 0)[0]
-    logits = g.nodes[g.output_id].inputs[0]
     from paper_2107_09789_b200.ir import Graph
     for i in feas[:3]:
         og, _ = knobs.apply_plan(g, plans[i])
+        logits = og.nodes[og.output_id].inputs[0]  # the SoftMax input (a branched Linear has a new id)
         _, vals = IR.execute(og, x0, keep=True)
         assert _rel(executor.execute(og, x0), vals[og.output_id].astype(np.float64)) <= FP32_TOL
         _, exact = IR.execute(og, x0, keep=True, dtype=np.float64)
