@@ -54,7 +54,9 @@ struct ConvCfg {
   static constexpr int kEpiOff = kStagingOff + kStagingKB * kABytes;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
   static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
-  static constexpr int kSmem = kEpiOff + kEpiBytes + kInfoBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kBarOff = kEpiOff + kEpiBytes + kInfoBytes;
+  static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (1024 ints)
+  static constexpr int kSmem = kTabOff + 4096 + 1024 /*align*/;
   // TMEM columns (512 allocated):
   //   [0, kCorrSlots*BN)           correction accumulators (a_lo*b_hi + a_hi*b_lo), per tile
   //   next 2*BN                    ping-pong main accumulators (a_hi*b_hi), one K chunk each
@@ -290,7 +292,8 @@ __device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_co
 
 template <int BN, int PREC>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_tc_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles, int* __restrict__ sched) {
+    conv_tc_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles, int* __restrict__ sched,
+                   int claim) {
   using Cfg = ConvCfg<BN, PREC>;
   constexpr int STAGES = Cfg::kStages;
   constexpr bool kBf16 = Cfg::kBf16;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_buf = reinterpret_cast<float*>(smem + Cfg::kEpiOff);
   tobf_conv_desc* info = reinterpret_cast<tobf_conv_desc*>(smem + Cfg::kEpiOff + Cfg::kEpiBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kEpiOff + Cfg::kEpiBytes + Cfg::kInfoBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain (one K chunk)
   uint64_t* acc_empty = acc_full + 2;        // [2] drain -> MMA
@@ -866,27 +869,51 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   } else if (warp == 6) {
     // ---------------------------------------------------------- tile scheduler
-    // Claims tiles: the CTA's first tile is blockIdx.x, every further one
-    // comes from the launch-wide counter (tiles are in longest-K-first order,
-    // so greedy claiming is an LPT schedule).
-    int prob = 0;
+    // Claims tiles in batches of `claim` consecutive tiles: the CTA's first
+    // batch is [blockIdx.x*claim, +claim), every further one comes from the
+    // launch-wide counter (tiles are in longest-K-first order, so greedy
+    // claiming is an LPT schedule; launches of many short tiles claim 4 at a
+    // time so the atomic's latency is paid once per 4 tiles). The problem of a
+    // tile is found in a shared-memory copy of the descriptors' tile_start
+    // (forward scan: a CTA's tiles only increase), and a tile of the previous
+    // tile's problem copies its descriptor from the previous ring slot — the
+    // round-1 global binary search + 224-B global copy per tile cost a few
+    // microseconds of latency on every tile, longer than a 1x1 conv tile.
+    constexpr int kTab = 1024;
+    int* s_tstart = reinterpret_cast<int*>(smem + Cfg::kTabOff);
+    for (int i = lane; i < nprob && i < kTab; i += 32) s_tstart[i] = __ldg(&descs[i].tile_start);
+    __syncwarp();
+    auto tstart = [&](int i) { return i < kTab ? s_tstart[i] : __ldg(&descs[i].tile_start); };
+    int prob = 0, prev_slot = -1;
+    int bnext = 0, bend = 0;
     for (int it = 0;; ++it) {
       const int islot = it % kInfoSlots;
       mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
       // claim lazily: only once the A producer has taken tile it-1, so a CTA
       // holds at most one claimed-but-unstarted tile and the launch's tail
       // stays balanced (the info ring would otherwise let it claim 3 ahead)
-      if (it > 0) mbar_wait_backoff(a_took, (it - 1) & 1, 0x118);
-      int tile = 0;
-      if (lane == 0) tile = it == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&sched[0], 1);
-      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (it > 0) mbar_wait(a_took, (it - 1) & 1, 0x118);
+      if (bnext == bend) {
+        int first = 0;
+        if (lane == 0) first = it == 0 ? (int)blockIdx.x * claim : (int)gridDim.x * claim + atomicAdd(&sched[0], claim);
+        bnext = __shfl_sync(0xffffffffu, first, 0);
+        bend = bnext + claim;
+      }
+      int tile = bnext++;
       if (tile >= total_tiles) tile = -1;
       if (tile >= 0) {
-        prob = find_problem(descs, prob, nprob, tile);  // a CTA's tiles only increase: search forward
-        const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
+        const int p0 = prob;
+        while (prob + 1 < nprob && tstart(prob + 1) <= tile) ++prob;
         uint64_t* dst = reinterpret_cast<uint64_t*>(info + islot);
         constexpr int kWords = sizeof(tobf_conv_desc) / 8;
-        if (lane < kWords) dst[lane] = __ldg(src + lane);
+        if (prob == p0 && prev_slot >= 0) {
+          const uint64_t* src = reinterpret_cast<const uint64_t*>(info + prev_slot);
+          if (lane < kWords) dst[lane] = src[lane];
+        } else {
+          const uint64_t* src = reinterpret_cast<const uint64_t*>(descs + prob);
+          if (lane < kWords) dst[lane] = __ldg(src + lane);
+        }
+        prev_slot = islot;
       }
       if (lane == 0) info_tile[islot] = tile;
       __syncwarp();
@@ -1166,8 +1193,12 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
     if (e != cudaSuccess || count < 1) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     sms[dev] = count;
   }
-  const int grid = (int)std::min<int64_t>(total_tiles, sms[dev]);
-  conv_tc_kernel<BN, PREC><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles, sched);
+  // claim 4 tiles at a time when there are many (short-tile levels: the stem,
+  // 1x1 convs); one at a time otherwise (few long tiles: LPT balance)
+  const int claim = total_tiles >= 16 * (int64_t)sms[dev] ? 4 : 1;
+  const int grid = (int)std::min<int64_t>((total_tiles + claim - 1) / claim, sms[dev]);
+  conv_tc_kernel<BN, PREC><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles, sched,
+                                                                           claim);
   return tobf_cuda_check("tobf_conv_grouped");
 }
 

@@ -317,41 +317,53 @@ __global__ void __launch_bounds__(TPC * 32, 1)
 // Register-blocked cluster LSTM (the cfg5 / generation kernel). Same cluster
 // layout as lstm_ctc_cluster_kernel — CTA rank r of a cluster of CS = H/32
 // CTAs owns hidden units [32r, 32r+32), gate rows resident in shared memory
-// as bf16 — but each thread now computes its unit's 4 gates for RB = 4
-// traces (warp w: traces 4w..4w+3, lane = unit), so every bf16 weight
-// loaded and widened is used RB times: per 4 K a thread issues 4 weight
-// loads, 16 widenings, 4 broadcast h loads (h is stored k-major,
-// trace-minor: one 16-B load gives the 4 traces' values) and 64 FMAs —
-// 1.4 instructions per FMA instead of 2.3. h_t travels to every CTA of the
-// cluster as one 16-B DSMEM store per (unit, 4 traces). The head logits +
-// greedy CTC of trace q run in CTA q % CS (spread over the cluster instead of
-// serialising on rank 0). Accumulation order (bias, x[0..F), h[0..H)),
-// the lane-strided head partials + xor butterfly and every rounding are those
-// of the original formulation and of oracle/fitness_ref.c.
-constexpr int kRB = 4;       // traces per thread
-constexpr int kRBWarps = 4;  // warps per CTA
-constexpr int kRBTraces = kRB * kRBWarps;
+// as bf16 — but each thread computes its unit's 4 gates for RB = 4 traces
+// (warp w: traces 4w..4w+3, lane = unit), so every bf16 weight loaded and
+// widened is used RB times: per 4 K a thread issues 4 weight loads, 16
+// widenings, 4 broadcast h loads (h is stored k-major, trace-minor: one 16-B
+// load gives the 4 traces' values) and 64 FMAs — 1.4 instructions per FMA
+// instead of 2.3. NW warps per CTA, TPC = 4*NW traces per cluster.
+//
+// ONE h buffer (not a double buffer), so 32 traces fit beside the 133 KB of
+// H=512 gate rows and a CTA keeps 8 warps: each step has two cluster
+// barriers — A: every CTA has finished READING h_{t-1} (the gate products);
+// the activations and the next feature row are computed between A's arrive
+// and wait, hiding it — and B: every CTA's h_t has landed (one 16-B DSMEM
+// store per (unit, 4 traces) into every CTA). Rows are padded to TPC+4
+// floats so the head's k-strided reads of one trace are 4-way, not TPC-way,
+// bank conflicted. The head logits + greedy CTC of trace q run in CTA q % CS
+// (spread over the cluster instead of serialising on rank 0). Accumulation
+// order (bias, x[0..F), h[0..H)), the lane-strided head partials + xor
+// butterfly and every rounding are those of the original formulation and of
+// oracle/fitness_ref.c.
+constexpr int kRB = 4;  // traces per thread
 
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kRBWarps * 32, 1)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
     lstm_ctc_rb_kernel(const double* __restrict__ feats, const int32_t* __restrict__ offsets, int B, int F, int H,
                        int NC, const float* __restrict__ w_ihT, const float* __restrict__ w_hhT,
                        const float* __restrict__ bias, const float* __restrict__ w_out,
                        const float* __restrict__ b_out, int8_t* __restrict__ tokens, int T_max,
                        int32_t* __restrict__ ntok) {
-  constexpr int TPC = kRBTraces;
+  constexpr int TPC = kRB * NW;
+  constexpr int HS = TPC + 4;  // h row stride (floats)
   extern __shared__ __align__(16) uint8_t sm[];
   const int L = F + H;
   const int Lq = L >> 2;
   const int Lp = (L + 3) & ~3;
   uint2* wq = reinterpret_cast<uint2*>(sm);                                                       // [Lq][4][32]
   uint16_t* wtail = reinterpret_cast<uint16_t*>(sm + (size_t)Lq * 4 * kLstmUnits * 8);              // [L%4][4][32]
-  float* hv = reinterpret_cast<float*>(sm + (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2);  // [2][Lp][TPC]
-  float* bsm = hv + 2 * Lp * TPC;  // [4][32]
+  float* hv = reinterpret_cast<float*>(sm + (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2);  // [Lp][HS]
+  float* bsm = hv + Lp * HS;  // [4][32]
   float* wo = bsm + 4 * kLstmUnits;  // [NC][H]
   __shared__ int s_len[TPC], s_row0[TPC];
   const int G = 4 * H;
@@ -383,7 +395,7 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
   for (int i = threadIdx.x; i < 4 * kLstmUnits; i += blockDim.x)
     bsm[i] = bias[(i / kLstmUnits) * H + rank * kLstmUnits + (i % kLstmUnits)];
   for (int i = threadIdx.x; i < NC * H; i += blockDim.x) wo[i] = w_out[i];
-  for (int i = threadIdx.x; i < 2 * Lp * TPC; i += blockDim.x) hv[i] = 0.0f;
+  for (int i = threadIdx.x; i < Lp * HS; i += blockDim.x) hv[i] = 0.0f;
   if (threadIdx.x < TPC) {
     const int b = b0 + threadIdx.x;
     s_len[threadIdx.x] = b < B ? offsets[b + 1] - offsets[b] : 0;
@@ -413,19 +425,16 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
     xrow0[j] = s_row0[xtr[j]];
     x_cur[j] = (xl[j] && 0 < xlen[j]) ? (float)tobf_log1p_d(feats[(int64_t)xrow0[j] * 9 + xk[j]]) : 0.0f;
   }
-  // head ownership: trace q = rank + CS*(w + 4s) (s = 0..3) is decoded by warp w of CTA q % CS
+  // head ownership: trace q = rank + CS*(w + NW*s) is decoded by warp w of CTA q % CS
   int prev[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   float c[kRB] = {0.f, 0.f, 0.f, 0.f};
   const uint32_t hv_local = static_cast<uint32_t>(__cvta_generic_to_shared(hv));
+  const uint32_t slot = hv_local + 4u * (uint32_t)((F + unit) * HS + kRB * w);
+  const float* hrow = hv + kRB * w;
   for (int t = 0; t < tmax; ++t) {
-    float* hcur = hv + (t & 1) * Lp * TPC;
-    const int nxt = (t + 1) & 1;
-    double f_next[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (xl[j]) hcur[xk[j] * TPC + xtr[j]] = x_cur[j];
-      f_next[j] = (xl[j] && t + 1 < xlen[j]) ? feats[(int64_t)(xrow0[j] + t + 1) * 9 + xk[j]] : 0.0;
-    }
+    for (int j = 0; j < 2; ++j)
+      if (xl[j]) hv[xk[j] * HS + xtr[j]] = x_cur[j];
     __syncwarp();
     float acc[4][kRB];
 #pragma unroll
@@ -435,15 +444,14 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
       for (int r = 0; r < kRB; ++r) acc[g][r] = bv;
     }
     const uint2* wrow = wq + u;
-    const float* hrow = hcur + kRB * w;
 #pragma unroll 2
     for (int kq = 0; kq < Lq; ++kq) {
       const uint2 w0 = wrow[(kq * 4 + 0) * kLstmUnits], w1 = wrow[(kq * 4 + 1) * kLstmUnits];
       const uint2 w2 = wrow[(kq * 4 + 2) * kLstmUnits], w3 = wrow[(kq * 4 + 3) * kLstmUnits];
-      const float4 h0 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 0) * TPC);
-      const float4 h1 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 1) * TPC);
-      const float4 h2 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 2) * TPC);
-      const float4 h3 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 3) * TPC);
+      const float4 h0 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 0) * HS);
+      const float4 h1 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 1) * HS);
+      const float4 h2 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 2) * HS);
+      const float4 h3 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 3) * HS);
       const float hs[4][kRB] = {{h0.x, h0.y, h0.z, h0.w}, {h1.x, h1.y, h1.z, h1.w},
                                 {h2.x, h2.y, h2.z, h2.w}, {h3.x, h3.y, h3.z, h3.w}};
       const float wg[4][4] = {{bf16lo(w0.x), bf16hi(w0.x), bf16lo(w0.y), bf16hi(w0.y)},
@@ -458,7 +466,7 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
           for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wg[g][e], hs[e][r], acc[g][r]);
     }
     for (int e = 0; e < (L & 3); ++e) {
-      const float4 hx = *reinterpret_cast<const float4*>(hrow + (Lq * 4 + e) * TPC);
+      const float4 hx = *reinterpret_cast<const float4*>(hrow + (Lq * 4 + e) * HS);
       const float hs[kRB] = {hx.x, hx.y, hx.z, hx.w};
       const uint16_t* wt = wtail + e * 4 * kLstmUnits + u;
 #pragma unroll
@@ -468,7 +476,14 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
         for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wv, hs[r], acc[g][r]);
       }
     }
-    const float4 hold = *reinterpret_cast<const float4*>(hcur + (F + unit) * TPC + kRB * w);
+    const float4 hold = *reinterpret_cast<const float4*>(hv + (F + unit) * HS + kRB * w);
+    // barrier A: every CTA is done reading h_{t-1}; its latency hides behind
+    // the activations and the next feature row
+    cluster_arrive();
+    double f_next[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      f_next[j] = (xl[j] && t + 1 < xlen[j]) ? feats[(int64_t)(xrow0[j] + t + 1) * 9 + xk[j]] : 0.0;
     float hval[kRB] = {hold.x, hold.y, hold.z, hold.w};
 #pragma unroll
     for (int r = 0; r < kRB; ++r) {
@@ -483,20 +498,20 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
     }
 #pragma unroll
     for (int j = 0; j < 2; ++j) x_cur[j] = (xl[j] && t + 1 < xlen[j]) ? (float)tobf_log1p_d(f_next[j]) : 0.0f;
-    const uint32_t slot = hv_local + 4u * (uint32_t)(nxt * Lp * TPC + (F + unit) * TPC + kRB * w);
+    cluster_wait();
     for (int rr = 0; rr < CS; ++rr) st_cluster_v4(map_shared(slot, rr), hval[0], hval[1], hval[2], hval[3]);
-    cluster_sync_all();
+    cluster_sync_all();  // barrier B: h_t has landed in every CTA
     // head + greedy CTC of the traces this warp owns (same formula and order as before)
-    const float* hn = hv + nxt * Lp * TPC + F * TPC;
+    const float* hn = hv + F * HS;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      const int q = (int)rank + CS * (w + kRBWarps * s);
+      const int q = (int)rank + CS * (w + NW * s);
       if (q >= TPC || t >= s_len[q]) continue;
       int best = 0;
       float bestv = 0.0f;
       for (int cls = 0; cls < NC; ++cls) {
         float p = 0.0f;
-        for (int k = u; k < H; k += 32) p = fmaf(wo[cls * H + k], hn[k * TPC + q], p);
+        for (int k = u; k < H; k += 32) p = fmaf(wo[cls * H + k], hn[k * HS + q], p);
         for (int off = 16; off; off >>= 1) p = p + __shfl_xor_sync(0xffffffffu, p, off);
         const float lg = b_out[cls] + p;
         if (cls == 0 || lg > bestv) {
@@ -513,7 +528,7 @@ __global__ void __launch_bounds__(kRBWarps * 32, 1)
   }
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    const int q = (int)rank + CS * (w + kRBWarps * s);
+    const int q = (int)rank + CS * (w + NW * s);
     if (q < TPC && u == 0 && b0 + q < B) ntok[b0 + q] = cnt[s];
   }
 }
@@ -746,19 +761,21 @@ static int launch_lstm_cluster(const double* feats, const int32_t* offsets, int3
   return tobf_cuda_check("tobf_lstm_ctc");
 }
 
+template <int NW>
 static int launch_lstm_rb(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H, int32_t NC,
                           const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
                           const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, cudaStream_t st) {
+  constexpr int TPC = kRB * NW, HS = TPC + 4;
   const int L = F + H, Lq = L / 4, Lp = (L + 3) & ~3, CS = H / kLstmUnits;
   const size_t smem = (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2 +
-                      sizeof(float) * (2 * (size_t)Lp * kRBTraces + 4 * kLstmUnits + NC * H);
-  auto kern = lstm_ctc_rb_kernel;
+                      sizeof(float) * ((size_t)Lp * HS + 4 * kLstmUnits + NC * H);
+  auto kern = lstm_ctc_rb_kernel<NW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm rb attrs: %s", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CS, (B + kRBTraces - 1) / kRBTraces, 1);
-  cfg.blockDim = dim3(kRBWarps * 32, 1, 1);
+  cfg.gridDim = dim3(CS, (B + TPC - 1) / TPC, 1);
+  cfg.blockDim = dim3(NW * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -783,11 +800,20 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   static const int variant = [] {
-    const char* v = getenv("TOBF_LSTM_VARIANT");  // A/B measurements only: "cluster16" = the round-1 kernel
-    return v && strcmp(v, "cluster16") == 0 ? 1 : 0;
+    // A/B measurements only: "cluster16" = the round-1 kernel, "rb4" / "rb8" force the warps per CTA
+    const char* v = getenv("TOBF_LSTM_VARIANT");
+    if (!v) return 0;
+    return strcmp(v, "cluster16") == 0 ? 1 : strcmp(v, "rb4") == 0 ? 4 : strcmp(v, "rb8") == 0 ? 8 : 0;
   }();
-  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16 && variant == 0)
-    return launch_lstm_rb(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+  if (H % kLstmUnits == 0 && H / kLstmUnits <= 16 && variant != 1) {
+    // 8 warps (32 traces) per cluster once the batch fills the GPU with them,
+    // else 4 (16 traces): a generation-sized batch (32) keeps twice the clusters
+    // (measured, cfg5 10k traces: H=512 169 vs 222 ms, H=256 34 vs 40 ms; H=128 9.7 vs 10.9 ms the other way)
+    const bool wide = variant == 8 || (variant == 0 && H >= 256 && (int64_t)B * (H / kLstmUnits) >= 32 * 148);
+    if (wide)
+      return launch_lstm_rb<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+    return launch_lstm_rb<4>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+  }
   if (H % kLstmUnits == 0 && H / kLstmUnits <= 16) {
     // 16 traces per cluster (the h double buffer of 16 traces plus the bf16
     // gate rows fill the 227 KB of shared memory at H=512): the per-step
