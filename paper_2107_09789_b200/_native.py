@@ -19,6 +19,7 @@ TOBF_MAX_EPI = 6
 EPI_NONE, EPI_AFFINE, EPI_RELU, EPI_ADD_TENSOR, EPI_ADD_CONST = 0, 1, 2, 3, 4
 OP_MAXPOOL, OP_EPI, OP_COPYCH, OP_SOFTMAX = 1, 2, 3, 4
 PREC_TF32X3, PREC_BF16 = 0, 1
+CONV_TMA = 0x100  # block_n flag of an all-TMA conv launch (include/tobf.h TOBF_CONV_TMA)
 PRECISIONS = {"fp32": PREC_TF32X3, "bf16": PREC_BF16}
 
 
@@ -44,6 +45,7 @@ class ConvDesc(C.Structure):
         ("tile_start", C.c_int32), ("nepi", C.c_int32), ("ldx", C.c_int32), ("ldy", C.c_int32),
         ("epi", EpiStep * TOBF_MAX_EPI),
         ("ws", C.c_void_p), ("cnt", C.c_void_p), ("ksplit", C.c_int32), ("kper", C.c_int32),
+        ("tmap", C.c_void_p), ("tma", C.c_int32), ("pad_", C.c_int32),
     ]
 
 
@@ -81,7 +83,7 @@ class DeviceProfileC(C.Structure):
     ]
 
 
-assert C.sizeof(ConvDesc) == 224, C.sizeof(ConvDesc)
+assert C.sizeof(ConvDesc) == 240, C.sizeof(ConvDesc)
 assert C.sizeof(EwDesc) == 176, C.sizeof(EwDesc)
 assert C.sizeof(KernDesc) == 136, C.sizeof(KernDesc)
 
@@ -104,6 +106,7 @@ SIGNATURES = {
     "tobf_pack_weights_ex": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32,
                                        _i32, _vp, _vp]),
     "tobf_conv_grouped_ex": (C.c_int, [_vp, C.c_int, _i64, C.c_int, C.c_int, _vp, _vp]),
+    "tobf_conv_tmaps": (C.c_int, [_vp, C.c_int, _vp, C.c_uint64, C.POINTER(C.c_int)]),
     "tobf_ew_prepare": (C.c_int, [_vp, C.c_int, C.POINTER(_i64)]),
     "tobf_ew_grouped": (C.c_int, [_vp, C.c_int, _i64, _vp]),
     "tobf_equiv_compare": (C.c_int, [_vp, _vp, C.c_int, _i64, _i32, _i32, _f32, _vp, _vp, _vp]),

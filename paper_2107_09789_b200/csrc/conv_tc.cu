@@ -23,6 +23,7 @@
 // hi/lo per row and written to tensor memory; B (weights) is a pre-packed,
 // pre-split, 128B-swizzled image bulk-copied into shared memory. Each K step
 // issues three tcgen05.mma kind::tf32 with A from TMEM and B from SMEM.
+#include <cuda.h>
 #include "ptx.cuh"
 #include "tobf_internal.h"
 
@@ -290,7 +291,7 @@ __device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_co
   }
 }
 
-template <int BN, int PREC>
+template <int BN, int PREC, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles, int* __restrict__ sched,
                    int claim) {
@@ -310,7 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
   uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
   uint64_t* a_took = info_empty + kInfoSlots;     // A producer took tile k's descriptor (phase k)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_took + 1);
+  uint64_t* stg_full = a_took + 1;                // [kStagingKB] TMA im2col -> A warps (TMA mode)
+  uint64_t* stg_empty = stg_full + Cfg::kStagingKB;  // [kStagingKB] A warps -> TMA issuer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + Cfg::kStagingKB);
   volatile int* info_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kInfoSlots], -1 = no more tiles
   volatile int* split_last = info_tile + kInfoSlots;  // drain: this unit completes its split-K tile
   // launch-wide tile counters: the caller's pair, else this variant's module pair
@@ -338,9 +341,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kInfoSlots; ++s) {
       mbar_init(&info_full[s], 1);
-      mbar_init(&info_empty[s], kInfoConsumers);
+      mbar_init(&info_empty[s], kInfoConsumers + (TMA ? 1 : 0));  // + the TMA issuer warp
     }
-    mbar_init(a_took, 4);
+    // the scheduler claims tile k+1 once tile k's descriptor is taken by the
+    // first role to need it: the A warps (cp.async mode) or the TMA issuer
+    mbar_init(a_took, TMA ? 1 : 4);
+    for (int s = 0; s < Cfg::kStagingKB; ++s) {
+      mbar_init(&stg_full[s], 1);
+      mbar_init(&stg_empty[s], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 4) tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -460,36 +469,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++ikb;
       ++issued;
     };
+    if constexpr (!TMA) {
 #pragma unroll 1
-    for (int q = 0; q < SD - 1; ++q) {
-      if (ensure()) issue();
-      cp_async_commit();
+      for (int q = 0; q < SD - 1; ++q) {
+        if (ensure()) issue();
+        cp_async_commit();
+      }
     }
     int stage = 0;
     uint32_t phase = 0;
-#pragma unroll 1
-    for (int g = 0;; ++g) {
-      __syncwarp();  // every lane is done reading the slot about to be refilled
-#ifdef TOBF_CONV_DIAG_NOA
-      // diagnostic build: no A gather/split (wrong results; isolates the MMA/B/drain side)
-      if (ensure()) { ++ikb; ++issued; }
-      cp_async_commit();
-      if (g >= issued) break;
-      if (g % Cfg::kStgPerKB == Cfg::kStgPerKB - 1) {
-        PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
-        mbar_arrive(&full_bar[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      continue;
-#endif
-      PROF_WAIT(4, if (ensure()) issue());
-      cp_async_commit();  // one group per block (empty past the end): group g holds block g
-      if (g >= issued) break;
-      PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
-      const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
-      float4 row[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+    // one staged block of this thread's row (32 fp32 of K, = TMEM lane t)
+    // -> its A stage in tensor memory (tf32 hi/lo split, or the bf16 pair)
+    auto to_tmem = [&](const float4 (&row)[8], int g) {
       if constexpr (kBf16) {
         // 32 fp32 -> 16 hi + 16 lo bf16x2 columns (round to nearest even),
         // element k in the low half of column k/2; two staging blocks fill
@@ -518,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&full_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        continue;
+        return;
       }
       // split hi/lo BEFORE waiting for the free TMEM stage: after the MMAs
       // release it only the four tcgen05.st are left on the critical path
@@ -546,13 +537,134 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&full_bar[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    };
+    if constexpr (TMA) {
+      // ---- TMA im2col mode: warp 7 loads each 32-channel K block of the
+      // tile's 128 output pixels with one cp.async.bulk.tensor.im2col into
+      // the staging ring (stg_full); these warps only read their rows,
+      // release the slot (stg_empty) and split into tensor memory.
+      int g = 0;
+#pragma unroll 1
+      for (int it = 0;; ++it) {
+        const int islot = it % kInfoSlots;
+        PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x110));
+        const int itile = info_tile[islot];
+        if (itile < 0) break;
+        const tobf_conv_desc& d = info[islot];
+        const int lt = itile - d.tile_start;
+        const int t2 = lt / d.ksplit;
+        const int kb0 = (lt - t2 * d.ksplit) * d.kper;
+        const int nsb = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);
+        const int sb0 = kb0 * Cfg::kStgPerKB, nvalid = d.K / kBK;  // staging blocks past K read zeros
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&info_empty[islot]);
+#pragma unroll 1
+        for (int j = 0; j < nsb; ++j, ++g) {
+          const int slot = g % SD;
+          PROF_WAIT(2, mbar_wait(&stg_full[slot], (g / SD) & 1, 0x11a));
+          float4 row[8];
+          if (sb0 + j < nvalid) {
+            const uint32_t src = stg_s + slot * kABytes + t * kRowBytes;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&stg_empty[slot]);
+          to_tmem(row, g);
+        }
+      }
+    } else {
+#pragma unroll 1
+    for (int g = 0;; ++g) {
+      __syncwarp();  // every lane is done reading the slot about to be refilled
+#ifdef TOBF_CONV_DIAG_NOA
+      // diagnostic build: no A gather/split (wrong results; isolates the MMA/B/drain side)
+      if (ensure()) { ++ikb; ++issued; }
+      cp_async_commit();
+      if (g >= issued) break;
+      if (g % Cfg::kStgPerKB == Cfg::kStgPerKB - 1) {
+        PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
+        mbar_arrive(&full_bar[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      continue;
+#endif
+      PROF_WAIT(4, if (ensure()) issue());
+      cp_async_commit();  // one group per block (empty past the end): group g holds block g
+      if (g >= issued) break;
+      PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
+      const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
+      float4 row[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      to_tmem(row, g);
     }
+    }  // TMA
     cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF
     if (t == 0) { PROF_FLUSH(0); PROF_ADD(7); }
 #endif
   } else if (warp < 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+  }
+  if (TMA && warp == 7) {
+    // ---------------------------------------------------------- TMA im2col issuer
+    // Per tile: the first output pixel (n, yo, xo) of the M tile gives the
+    // im2col base (xo*s - pad, yo*s - pad, n); each 32-channel K block is one
+    // filter tap (u, v) — the load's im2col offsets — and a channel offset c0.
+    // The tensor map's pixel box walks the tile's 128 output pixels (wrapping
+    // rows and images, zero-filling the padding) with the conv stride.
+    constexpr int SD = Cfg::kStagingKB;
+    const uint32_t stg_s = smem_u32(smem + Cfg::kStagingOff);
+    int g = 0;
+    for (int it = 0;; ++it) {
+      const int islot = it % kInfoSlots;
+      mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x119);
+      const int tile = info_tile[islot];
+      if (tile < 0) break;
+      const tobf_conv_desc& d = info[islot];
+      const int lt = tile - d.tile_start;
+      const int t2 = lt / d.ksplit;
+      const int kb0 = (lt - t2 * d.ksplit) * d.kper;
+      const int nsb = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);
+      const int sb0 = kb0 * Cfg::kStgPerKB, nvalid = d.K / kBK;
+      const int m0 = (t2 / d.ntiles) * kBM;
+      const int HWo = d.Ho * d.Wo;
+      const int n0 = m0 / HWo;
+      const int rem = m0 - n0 * HWo;
+      const int yo = rem / d.Wo;
+      const int xo = rem - yo * d.Wo;
+      const int w0 = xo * d.stride - d.pad, h0 = yo * d.stride - d.pad;
+      const int Cp = d.Cp, k2 = d.k2;
+      const void* tmap = d.tmap;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&info_empty[islot]);
+        mbar_arrive(a_took);
+      }
+      for (int j = 0; j < nsb; ++j, ++g) {
+        const int slot = g % SD;
+        mbar_wait(&stg_empty[slot], ((g / SD) & 1) ^ 1, 0x11b);
+        if (lane == 0) {
+          const int sb = sb0 + j;
+          if (sb < nvalid) {
+            const int kk = sb * kBK;
+            const int tap = kk / Cp;
+            const int c0 = kk - tap * Cp;
+            const int u = tap / k2, v = tap - (tap / k2) * k2;
+            mbar_arrive_expect_tx(&stg_full[slot], kABytes);
+            tma_im2col_4d(stg_s + slot * kABytes, tmap, c0, w0, h0, n0, (uint16_t)v, (uint16_t)u,
+                          &stg_full[slot]);
+          } else {
+            mbar_arrive(&stg_full[slot]);  // past K (bf16 tail): the A warps use zeros
+          }
+        }
+        __syncwarp();
+      }
+    }
   }
   if (warp == 4) {
     // ---------------------------------------------------------- B producer
@@ -1175,9 +1287,62 @@ extern "C" int tobf_pack_weights_gather(const float* w, int32_t k1, int32_t k2, 
                               wimg, stream);
 }
 
+// ------------------------------------------------------------ TMA im2col maps
+// cuTensorMapEncodeIm2col through the runtime's driver entry point (no link
+// dependency on libcuda).
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeIm2colFn>(p);
+  }();
+  return fn;
+}
+
+extern "C" int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, uint64_t tmap_dev, int* n_tma) {
+  if (n < 0 || (n > 0 && (!descs || !tmap_host)) || (tmap_dev & 127) || !n_tma)
+    return tobf_fail(TOBF_E_INVALID, "tobf_conv_tmaps: bad arguments");
+  const EncodeIm2colFn enc = encode_im2col_fn();
+  int count = 0;
+  for (int i = 0; i < n; ++i) {
+    tobf_conv_desc& d = descs[i];
+    d.tma = 0;
+    d.tmap = nullptr;
+    const bool ok = enc && d.Cp % kBK == 0 && d.k1 <= 256 && d.k2 <= 256 && d.stride >= 1 && d.stride <= 8 &&
+                    d.pad <= 127 && d.pad - (d.k1 - 1) >= -128 && d.pad - (d.k2 - 1) >= -128 &&
+                    (reinterpret_cast<uintptr_t>(d.x) & 15) == 0 && d.ldx % 4 == 0;
+    if (!ok) continue;
+    CUtensorMap* map = reinterpret_cast<CUtensorMap*>(static_cast<uint8_t*>(tmap_host) + 128 * (size_t)i);
+    const cuuint64_t dims[4] = {(cuuint64_t)d.Cp, (cuuint64_t)d.W, (cuuint64_t)d.H, (cuuint64_t)d.batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)d.ldx * 4, (cuuint64_t)d.ldx * 4 * d.W,
+                                   (cuuint64_t)d.ldx * 4 * d.W * d.H};
+    const int lower[2] = {-d.pad, -d.pad};                              // (w, h)
+    const int upper[2] = {d.pad - (d.k2 - 1), d.pad - (d.k1 - 1)};      // (w, h)
+    const cuuint32_t estr[4] = {1, (cuuint32_t)d.stride, (cuuint32_t)d.stride, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(d.x), dims, strides, lower,
+                           upper, kBK /*channels per pixel*/, kBM /*pixels per column*/, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) continue;
+    d.tmap = reinterpret_cast<const void*>(tmap_dev + 128 * (uint64_t)i);
+    d.tma = 1;
+    ++count;
+  }
+  *n_tma = count;
+  return TOBF_OK;
+}
+
 // Per-device launch state of one kernel variant: SM count and the one-time
 // dynamic shared-memory opt-in (a context may drive several devices).
-template <int BN, int PREC>
+template <int BN, int PREC, bool TMA>
 static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int32_t* sched, cudaStream_t st) {
   constexpr int kMaxDev = 64;
   static int sms[kMaxDev] = {0};
@@ -1188,7 +1353,7 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
   if (sms[dev] == 0) {
     int count = 0;
     cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaFuncSetAttribute(conv_tc_kernel<BN, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(conv_tc_kernel<BN, PREC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ConvCfg<BN, PREC>::kSmem);
     if (e != cudaSuccess || count < 1) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     sms[dev] = count;
@@ -1197,9 +1362,22 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
   // 1x1 convs); one at a time otherwise (few long tiles: LPT balance)
   const int claim = total_tiles >= 16 * (int64_t)sms[dev] ? 4 : 1;
   const int grid = (int)std::min<int64_t>((total_tiles + claim - 1) / claim, sms[dev]);
-  conv_tc_kernel<BN, PREC><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles, sched,
-                                                                           claim);
+  conv_tc_kernel<BN, PREC, TMA><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles,
+                                                                                sched, claim);
   return tobf_cuda_check("tobf_conv_grouped");
+}
+
+template <bool TMA>
+static int launch_variant(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, int prec,
+                          int32_t* sched, cudaStream_t st) {
+  if (prec == TOBF_PREC_TF32X3) {
+    if (block_n == 128) return launch_conv<128, 0, TMA>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 0, TMA>(d_descs, n, total_tiles, sched, st);
+  } else if (prec == TOBF_PREC_BF16) {
+    if (block_n == 128) return launch_conv<128, 1, TMA>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 1, TMA>(d_descs, n, total_tiles, sched, st);
+  }
+  return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: block_n must be 64 or 128, prec 0 or 1");
 }
 
 extern "C" int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n,
@@ -1207,12 +1385,13 @@ extern "C" int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_
   if (n <= 0 || total_tiles <= 0) return TOBF_OK;
   if (!d_descs) return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: null descriptors");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (prec == TOBF_PREC_TF32X3) {
-    if (block_n == 128) return launch_conv<128, 0>(d_descs, n, total_tiles, sched, st);
-    if (block_n == 64) return launch_conv<64, 0>(d_descs, n, total_tiles, sched, st);
-  } else if (prec == TOBF_PREC_BF16) {
-    if (block_n == 128) return launch_conv<128, 1>(d_descs, n, total_tiles, sched, st);
-    if (block_n == 64) return launch_conv<64, 1>(d_descs, n, total_tiles, sched, st);
+  // the A-operand mode of a launch is that of its problems (tobf_conv_tmaps);
+  // block_n | 0x100 marks an all-TMA launch
+  const bool tma = (block_n & 0x100) != 0;
+  block_n &= 0xFF;
+  if (prec == TOBF_PREC_TF32X3 || prec == TOBF_PREC_BF16) {
+    return tma ? launch_variant<true>(d_descs, n, total_tiles, block_n, prec, sched, st)
+               : launch_variant<false>(d_descs, n, total_tiles, block_n, prec, sched, st);
   } else {
     return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: unknown precision %d", prec);
   }

@@ -80,7 +80,7 @@ class DeviceContext:
     # -- host arrays -> device ----------------------------------------------
     RING_BYTES = 64 << 20
 
-    def _staged(self, raw: np.ndarray) -> torch.Tensor:
+    def _staged(self, raw: np.ndarray, dst: torch.Tensor | None = None) -> torch.Tensor:
         """Stream-ordered H2D of ``raw`` (uint8) through a pinned staging ring
         allocated once: no per-upload page pinning (a cudaHostAlloc can stall
         the host behind queued device work) and no pageable copy. A ring
@@ -88,7 +88,11 @@ class DeviceContext:
         n = raw.nbytes
         self.h2d_bytes += n
         if n > self.RING_BYTES // 4:
-            return torch.from_numpy(raw.copy()).pin_memory().to(self.device, non_blocking=True)
+            src = torch.from_numpy(raw.copy()).pin_memory()
+            if dst is not None:
+                dst.copy_(src, non_blocking=True)
+                return dst
+            return src.to(self.device, non_blocking=True)
         ring = self.__dict__.get("_ring")
         if ring is None:
             ring = self._ring = torch.empty(self.RING_BYTES, dtype=torch.uint8, pin_memory=True)
@@ -102,7 +106,7 @@ class DeviceContext:
             if blo < hi and lo < bhi:
                 ev.synchronize()
         self._ring_np[lo:hi] = raw
-        dev = torch.empty(n, dtype=torch.uint8, device=self.device)
+        dev = torch.empty(n, dtype=torch.uint8, device=self.device) if dst is None else dst
         dev.copy_(ring[lo:hi], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))  # the stream the copy was issued on

@@ -463,7 +463,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
             epi = epi_rows(op.steps)
             conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
                               s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
-                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0))
+                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
             conv_lv.append(op.level)
             conv_bn.append(bn)
             conv_k.append(k1 * k2 * cp)
@@ -523,6 +523,8 @@ def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, 
 
 
 SPLITK_MAX = 16  # work units per tile at most
+#: A operand by TMA im2col where eligible (TOBF_CONV_TMA=0: cp.async gather everywhere, A/B measurements)
+TMA_A = __import__("os").environ.get("TOBF_CONV_TMA", "1") != "0"
 
 
 def conv_sched(ctx: DeviceContext) -> torch.Tensor:
@@ -811,10 +813,25 @@ class PopulationRun:
         conv_bn = np.concatenate([p.conv_bn for p in plans])
         conv_k = np.concatenate([p.conv_k for p in plans])
         ew_level = np.concatenate([p.ew_level for p in plans])
-        # one launch per (level, BN), long K first; one ew launch per level
-        order = np.lexsort((-conv_k, -conv_bn, conv_level))
+        # TMA im2col for every conv whose 32-channel K blocks stay within one
+        # filter tap (Cp % 32 == 0): one 128-B tensor map per problem, encoded
+        # on the host now that the input pointers are final
+        conv_tma = np.zeros(len(conv), np.int64)
+        if len(conv) and TMA_A:
+            self._tmaps = torch.empty(128 * len(conv) + 128, dtype=torch.uint8, device=ctx.device)
+            tbase = (self._tmaps.data_ptr() + 127) & ~127
+            host_maps = np.zeros(128 * len(conv), np.uint8)
+            ntma = C.c_int()
+            ctx.check(lib.tobf_conv_tmaps(C.c_void_p(conv.ctypes.data), len(conv), C.c_void_p(host_maps.ctypes.data),
+                                          tbase, C.byref(ntma)), "conv tensor maps")
+            if ntma.value:
+                ctx._staged(host_maps, self._tmaps[tbase - self._tmaps.data_ptr():][:len(host_maps)])
+            conv_tma = conv["tma"].astype(np.int64)
+        # one launch per (level, BN, A mode), long K first; one ew launch per level
+        order = np.lexsort((-conv_k, -conv_tma, -conv_bn, conv_level))
         conv = conv[order]
-        ckey = np.stack([conv_level[order], conv_bn[order]], 1) if len(conv) else np.zeros((0, 2), np.int64)
+        ckey = np.stack([conv_level[order], conv_bn[order], conv_tma[order]], 1) if len(conv) else \
+            np.zeros((0, 3), np.int64)
         eorder = np.argsort(ew_level, kind="stable")
         ew = ew[eorder]
         ekey = ew_level[eorder]
@@ -825,13 +842,14 @@ class PopulationRun:
         conv_ptr = conv.ctypes.data
         for lo, hi in _runs(ckey):
             bn = int(ckey[lo, 1])
+            tma_flag = N.CONV_TMA if ckey[lo, 2] else 0
             # split-K for groups too small to fill the SMs; workspace offsets
             # now, one workspace shared by every (stream-ordered) conv launch
             ctx.check(lib.tobf_conv_prepare_split_ex(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
                                                      self.prec, ctx.sms, SPLITK_MAX, None, None, C.byref(tot),
                                                      C.byref(wsf), C.byref(cnts)), "conv prepare")
             ws_need, cnt_need = max(ws_need, wsf.value), max(cnt_need, cnts.value)
-            launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, bn))
+            launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, bn | tma_flag))
         if ws_need:
             ws, cnt = splitk_workspace(ctx, ws_need, cnt_need)
             split = conv["ksplit"] > 1

@@ -48,7 +48,7 @@ def main(pop=32, reps=5, fixture="resnet18", mode="sequence", prec="fp32"):
         kmax = max(d.kblocks for d in arr)
         kavg = sum(d.kblocks * d.mtiles * d.ntiles for d in arr) / max(tot, 1)
         geo = sorted({(d.k1, d.Cp, d.j, d.Ho) for d in arr})
-        rows.append((times[ci], n, tot, bn, fl, kmax, arr[0].Ho, arr[0].j, ci, kavg, geo))
+        rows.append((times[ci], n, tot, bn & 0xFF, fl, kmax, arr[0].Ho, arr[0].j, ci, kavg, geo))
         ci += 1
     tot_t = sum(r[0] for r in rows)
     tot_f = sum(r[4] for r in rows)
