@@ -73,8 +73,8 @@ typedef struct tobf_conv_desc {
   int32_t ksplit, kper;
   /* A operand by TMA im2col (filled by tobf_conv_tmaps): `tmap` = DEVICE
    * address of this problem's 128-B CUtensorMap (im2col mode, NHWC fp32,
-   * 32 channels x 128 output pixels per load, 128B swizzle), tma = 1. tma = 0:
-   * the A operand is gathered with cp.async (any Cp % 4 == 0). */
+   * 32 channels x 128 output pixels per load, 128B swizzle), tma = 32.
+   * tma = 0: the A operand is gathered with cp.async. */
   const void* tmap;
   int32_t tma, pad_;
 } tobf_conv_desc;
@@ -142,15 +142,15 @@ int tobf_pack_weights_ex(const float* w, int32_t k1, int32_t k2, int32_t c_real,
  * descriptors live in DEVICE memory (prepared with tobf_conv_prepare). */
 int tobf_conv_grouped(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, void* stream);
 
-/* TMA im2col eligibility + tensor maps: for every descriptor (host memory,
- * pointers already final) whose input view has Cp % 32 == 0 (a 32-channel K
- * block never straddles two filter taps), k1, k2 <= 256, stride <= 8 and
- * pad <= 127, encode its CUtensorMap into tmap_host + 128*i and set
- * descs[i].tmap = tmap_dev + 128*i, tma = 1; every other descriptor gets
- * tma = 0. tmap_host / tmap_dev must hold 128*n bytes, tmap_dev 128-B
- * aligned; the caller copies tmap_host to tmap_dev before the launch. A
- * launch (tobf_conv_grouped_ex) must contain only tma = 1 or only tma = 0
- * problems. *n_tma returns the count of tma = 1 descriptors. */
+/* TMA im2col tensor maps: for every descriptor (host memory, pointers
+ * already final) with Cp % 32 == 0 (a 32-channel K block never straddles
+ * two filter taps), k1, k2 <= 256, stride <= 8 and pad <= 127, encode its
+ * CUtensorMap into tmap_host + 128*i and set descs[i].tmap = tmap_dev +
+ * 128*i, tma = 32; every other descriptor gets tma = 0 (its A operand is
+ * gathered with cp.async, also inside a TMA-capable launch). tmap_host /
+ * tmap_dev must hold 128*n bytes, tmap_dev 128-B aligned; the caller copies
+ * tmap_host to tmap_dev before the launch. *n_tma returns the count of
+ * tma != 0 descriptors. */
 int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, uint64_t tmap_dev, int* n_tma);
 
 /* Either precision. `sched`: two int32 of DEVICE memory, zero before the
@@ -160,9 +160,11 @@ int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, uint64_t tmap
  * one variant must then be stream-ordered). */
 int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, int prec,
                          int32_t* sched, void* stream);
-/* block_n | TOBF_CONV_TMA: every problem of the launch has tma = 1 (A operand
- * loaded by TMA im2col: cp.async.bulk.tensor.4d...im2col, one load per
- * 32-channel K block of 128 output pixels, issued by a dedicated warp). */
+/* block_n | TOBF_CONV_TMA: a TMA-capable launch — problems with tma != 0
+ * get their A operand by TMA im2col (cp.async.bulk.tensor.4d...im2col, one
+ * load per 32-channel K block of 128 output pixels, issued by a dedicated
+ * warp), the others by the cp.async gather. Without the flag every problem
+ * uses cp.async (tma ignored). */
 #define TOBF_CONV_TMA 0x100
 
 /* Generic fused element-wise / pooling / copy ops (one op per descriptor). */

@@ -29,6 +29,15 @@
 
 namespace tobf {
 
+// 1 (default): tf32 correction products in their own per-tile TMEM
+// accumulator. 0 (measured, reverted): into the chunk's main accumulator —
+// 3 tf32 accumulates per K step into one buffer lose enough (the obfuscated
+// RN18 logits' error reached 1.4e-4 against the fp32 oracle's 4.5e-5) to
+// break the 1e-4 contract, for a 1.5 % faster conv.
+#ifndef TOBF_CONV_SPLIT_CORR
+#define TOBF_CONV_SPLIT_CORR 1
+#endif
+
 constexpr int kBM = 128;
 constexpr int kBK = 32;           // fp32 elements per K block = one 128-B swizzle row
 constexpr int kRowBytes = 128;
@@ -59,17 +68,21 @@ struct ConvCfg {
   static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (1024 ints)
   static constexpr int kSmem = kTabOff + 4096 + 1024 /*align*/;
   // TMEM columns (512 allocated):
-  //   [0, kCorrSlots*BN)           correction accumulators (a_lo*b_hi + a_hi*b_lo), per tile
-  //   next 2*BN                    ping-pong main accumulators (a_hi*b_hi), one K chunk each
+  //   [0, kCorrSlots*BN)           (TOBF_CONV_SPLIT_CORR=1 only) correction accumulators
+  //                                (a_lo*b_hi + a_hi*b_lo), one per tile slot
+  //   next kMainBufs*BN            main accumulators, one K chunk each, round robin
   //   kTmemACol + 64*s             A stage s: 32 hi + 32 lo columns
-  // BN=128 has room for one correction slot only: a tile's first MMA waits
-  // until the drain has read the previous tile's correction.
-  // bf16: no correction terms; the tile accumulates in one TMEM buffer (no
-  // chunked drain: bf16 rounding dominates the accumulation error), two
-  // buffers so tile i+1's MMAs overlap tile i's drain.
-  static constexpr int kCorrSlots = kBf16 ? 0 : (BN >= 128 ? 1 : 2);
+  // With TOBF_CONV_SPLIT_CORR=0 the two tf32 correction products would go
+  // into the chunk's main accumulator and the freed columns give 3 (BN=128) /
+  // 4 (BN=64) chunk buffers (too lossy: see the macro). bf16: the tile
+  // accumulates in one buffer (no chunked drain: bf16 rounding dominates),
+  // two buffers so tile i+1's MMAs overlap tile i's drain.
+  static constexpr bool kSplitCorr = !kBf16 && TOBF_CONV_SPLIT_CORR;
+  static constexpr int kCorrSlots = kSplitCorr ? (BN >= 128 ? 1 : 2) : 0;
+  static constexpr int kMainBufsRaw = (512 - 64 * kStages) / BN;
+  static constexpr int kMainBufs = (kSplitCorr || kBf16) ? 2 : (kMainBufsRaw > 4 ? 4 : kMainBufsRaw);
   static constexpr int kTmemMainCol = kCorrSlots * BN;
-  static constexpr int kTmemACol = kTmemMainCol + 2 * BN;
+  static constexpr int kTmemACol = kTmemMainCol + kMainBufs * BN;
   static constexpr int kAStageCols = 64;  // tf32: 32 hi + 32 lo; bf16: 64 K as 32 hi + 32 lo bf16x2 columns
   static constexpr int kTmemCols = 512;
   static_assert(kTmemACol + kAStageCols * kStages <= 512, "TMEM budget");
@@ -305,9 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tobf_conv_desc* info = reinterpret_cast<tobf_conv_desc*>(smem + Cfg::kEpiOff + Cfg::kEpiBytes);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
   uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* acc_full = empty_bar + STAGES;   // [2] MMA -> drain (one K chunk)
-  uint64_t* acc_empty = acc_full + 2;        // [2] drain -> MMA
-  uint64_t* small_empty = acc_empty + 2;     // [2] drain -> MMA (tile-slot correction accumulator)
+  constexpr int NB = Cfg::kMainBufs;
+  uint64_t* acc_full = empty_bar + STAGES;   // [NB <= 4] MMA -> drain (one K chunk)
+  uint64_t* acc_empty = acc_full + 4;        // [NB] drain -> MMA
+  uint64_t* small_empty = acc_empty + 4;     // [2] drain -> MMA (tile-slot correction accumulator)
   uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
   uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
   uint64_t* a_took = info_empty + kInfoSlots;     // A producer took tile k's descriptor (phase k)
@@ -334,18 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full_bar[s], 128 + 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NB; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
-      mbar_init(&small_empty[s], 128);
     }
+    for (int s = 0; s < 2; ++s) mbar_init(&small_empty[s], 128);
     for (int s = 0; s < kInfoSlots; ++s) {
       mbar_init(&info_full[s], 1);
       mbar_init(&info_empty[s], kInfoConsumers + (TMA ? 1 : 0));  // + the TMA issuer warp
     }
-    // the scheduler claims tile k+1 once tile k's descriptor is taken by the
-    // first role to need it: the A warps (cp.async mode) or the TMA issuer
-    mbar_init(a_took, TMA ? 1 : 4);
+    // the scheduler claims tile k+1 once the A warps' issue cursor took tile k
+    mbar_init(a_took, 4);
     for (int s = 0; s < Cfg::kStagingKB; ++s) {
       mbar_init(&stg_full[s], 1);
       mbar_init(&stg_empty[s], 4);
@@ -383,6 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float* rowp[8];
     int yb[8], xb[8];
     int Cp = 32, k1 = 1, k2 = 1, H = 1, W = 1, ldx = 0;
+    bool itma = false;                 // issue cursor's tile: A by TMA
+    int isb0 = 0, insb = 0;            // its first staging block, the problem's staging blocks within K
+    uint32_t tma_bits = 0, zero_bits = 0;  // per staging slot (TMA launches)
     int u = 0, v = 0, c0 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) { rowp[i] = nullptr; yb[i] = xb[i] = -(1 << 28); }
@@ -406,8 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ikblocks = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);  // staging blocks
         Cp = d.Cp; k1 = d.k1; k2 = d.k2; H = d.H; W = d.W; ldx = d.ldx;
         x = d.x;
+        itma = TMA && d.tma != 0;             // this tile's A blocks come by TMA (warp 7)
+        isb0 = kb0 * Cfg::kStgPerKB;
+        insb = d.K / kBK;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 8 && !itma; ++i) {
           const int m = m0 + 4 * i;
           if (m < M) {
             const int n = m / HWo;
@@ -422,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             rowp[i] = x;
           }
         }
-        {  // cursor at K element kb0*kBKe + chunk*4 = ((u*k2 + v)*Cp + c0)
+        if (!itma) {  // cursor at K element kb0*kBKe + chunk*4 = ((u*k2 + v)*Cp + c0)
           const int k0 = kb0 * Cfg::kBKe + chunk * 4;
           const int tap = k0 / Cp;
           c0 = k0 - tap * Cp;
@@ -441,6 +460,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     int issued = 0;
     auto issue = [&]() {
+      if (TMA) {
+        // per slot: block mode (TMA or cp.async) and "wholly past K" (zeros)
+        const uint32_t bit = 1u << (issued % SD);
+        tma_bits = itma ? (tma_bits | bit) : (tma_bits & ~bit);
+        zero_bits = (itma && isb0 + ikb >= insb) ? (zero_bits | bit) : (zero_bits & ~bit);
+        if (itma) {  // warp 7 loads this block
+          ++ikb;
+          ++issued;
+          return;
+        }
+      }
       const uint32_t slot = stg_s + (issued % SD) * kABytes;
       const int uq = u < k1 ? u : (1 << 28);  // K tail beyond k1*k2*Cp reads zeros
       const int toff = (u * W + v) * ldx + c0;
@@ -469,12 +499,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++ikb;
       ++issued;
     };
-    if constexpr (!TMA) {
 #pragma unroll 1
-      for (int q = 0; q < SD - 1; ++q) {
-        if (ensure()) issue();
-        cp_async_commit();
-      }
+    for (int q = 0; q < SD - 1; ++q) {
+      if (ensure()) issue();
+      cp_async_commit();
     }
     int stage = 0;
     uint32_t phase = 0;
@@ -538,45 +566,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&full_bar[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     };
-    if constexpr (TMA) {
-      // ---- TMA im2col mode: warp 7 loads each 32-channel K block of the
-      // tile's 128 output pixels with one cp.async.bulk.tensor.im2col into
-      // the staging ring (stg_full); these warps only read their rows,
-      // release the slot (stg_empty) and split into tensor memory.
-      int g = 0;
-#pragma unroll 1
-      for (int it = 0;; ++it) {
-        const int islot = it % kInfoSlots;
-        PROF_WAIT(0, mbar_wait(&info_full[islot], (it / kInfoSlots) & 1, 0x110));
-        const int itile = info_tile[islot];
-        if (itile < 0) break;
-        const tobf_conv_desc& d = info[islot];
-        const int lt = itile - d.tile_start;
-        const int t2 = lt / d.ksplit;
-        const int kb0 = (lt - t2 * d.ksplit) * d.kper;
-        const int nsb = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);
-        const int sb0 = kb0 * Cfg::kStgPerKB, nvalid = d.K / kBK;  // staging blocks past K read zeros
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&info_empty[islot]);
-#pragma unroll 1
-        for (int j = 0; j < nsb; ++j, ++g) {
-          const int slot = g % SD;
-          PROF_WAIT(2, mbar_wait(&stg_full[slot], (g / SD) & 1, 0x11a));
-          float4 row[8];
-          if (sb0 + j < nvalid) {
-            const uint32_t src = stg_s + slot * kABytes + t * kRowBytes;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&stg_empty[slot]);
-          to_tmem(row, g);
-        }
-      }
-    } else {
 #pragma unroll 1
     for (int g = 0;; ++g) {
       __syncwarp();  // every lane is done reading the slot about to be refilled
@@ -595,14 +584,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_WAIT(4, if (ensure()) issue());
       cp_async_commit();  // one group per block (empty past the end): group g holds block g
       if (g >= issued) break;
-      PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
+      const uint32_t sbit = 1u << (g % SD);
+      const bool blk_tma = TMA && (tma_bits & sbit);
+      if (blk_tma) {  // warp 7's TMA im2col load of this block (same 128B-swizzled layout)
+        PROF_WAIT(2, mbar_wait(&stg_full[g % SD], (g / SD) & 1, 0x11a));
+      } else {
+        PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
+      }
       const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
       float4 row[8];
+      if (TMA && (zero_bits & sbit)) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+        for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      }
+      if (TMA) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stg_empty[g % SD]);  // every block: keeps warp 7's phases
+      }
       to_tmem(row, g);
     }
-    }  // TMA
     cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF
     if (t == 0) { PROF_FLUSH(0); PROF_ADD(7); }
@@ -630,7 +633,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t2 = lt / d.ksplit;
       const int kb0 = (lt - t2 * d.ksplit) * d.kper;
       const int nsb = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);
-      const int sb0 = kb0 * Cfg::kStgPerKB, nvalid = d.K / kBK;
+      const int sb0 = kb0 * Cfg::kStgPerKB, K = d.K;
+      const bool tile_tma = d.tma != 0;
       const int m0 = (t2 / d.ntiles) * kBM;
       const int HWo = d.Ho * d.Wo;
       const int n0 = m0 / HWo;
@@ -641,17 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int Cp = d.Cp, k2 = d.k2;
       const void* tmap = d.tmap;
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&info_empty[islot]);
-        mbar_arrive(a_took);
-      }
+      if (lane == 0) mbar_arrive(&info_empty[islot]);
       for (int j = 0; j < nsb; ++j, ++g) {
         const int slot = g % SD;
         mbar_wait(&stg_empty[slot], ((g / SD) & 1) ^ 1, 0x11b);
         if (lane == 0) {
-          const int sb = sb0 + j;
-          if (sb < nvalid) {
-            const int kk = sb * kBK;
+          const int kk = (sb0 + j) * kBK;
+          if (tile_tma && kk < K) {
             const int tap = kk / Cp;
             const int c0 = kk - tap * Cp;
             const int u = tap / k2, v = tap - (tap / k2) * k2;
@@ -659,7 +659,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_im2col_4d(stg_s + slot * kABytes, tmap, c0, w0, h0, n0, (uint16_t)v, (uint16_t)u,
                           &stg_full[slot]);
           } else {
-            mbar_arrive(&stg_full[slot]);  // past K (bf16 tail): the A warps use zeros
+            // a cp.async tile's block (the A warps load it), or wholly past K
+            // (zeros): keep every slot's phase in step
+            mbar_arrive(&stg_full[slot]);
           }
         }
         __syncwarp();
@@ -733,16 +735,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_empty[islot]);
-      const int slot = kBf16 ? 0 : it % Cfg::kCorrSlots;
+      const int slot = Cfg::kSplitCorr ? it % (Cfg::kSplitCorr ? Cfg::kCorrSlots : 1) : 0;
       const uint32_t acc_small = tb + slot * BN;
-      if constexpr (!kBf16) {
+      if constexpr (Cfg::kSplitCorr) {
         PROF_WAIT(1, mbar_wait(&small_empty[slot], ((it / Cfg::kCorrSlots) & 1) ^ 1, 0x107));
         tc_fence_after();
       }
       for (int kb0 = 0; kb0 < kblocks; kb0 += kChunk, ++gc) {
-        const int buf = gc & 1;
+        const int buf = gc % NB;
         const uint32_t acc = tb + Cfg::kTmemMainCol + buf * BN;
-        PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc >> 1) & 1) ^ 1, 0x106));
+        PROF_WAIT(2, mbar_wait(&acc_empty[buf], ((gc / NB) & 1) ^ 1, 0x106));
         tc_fence_after();
         const int kend = kblocks - kb0 > kChunk ? kb0 + kChunk : kblocks;
         for (int kb = kb0; kb < kend; ++kb) {
@@ -766,9 +768,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < kBK / 8; ++kk) {
               const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
               const uint64_t dbh = sdesc_k128(b_hi + koff), dbl = sdesc_k128(b_lo + koff);
-              mma_tf32_ts(acc_small, ta + 32 + kk * 8, dbh, idesc, (kb | kk) != 0);
-              mma_tf32_ts(acc_small, ta + kk * 8, dbl, idesc, 1u);
-              mma_tf32_ts(acc, ta + kk * 8, dbh, idesc, (kb - kb0 | kk) != 0);
+              if constexpr (Cfg::kSplitCorr) {
+                mma_tf32_ts(acc_small, ta + 32 + kk * 8, dbh, idesc, (kb | kk) != 0);
+                mma_tf32_ts(acc_small, ta + kk * 8, dbl, idesc, 1u);
+                mma_tf32_ts(acc, ta + kk * 8, dbh, idesc, (kb - kb0 | kk) != 0);
+              } else {
+                mma_tf32_ts(acc, ta + kk * 8, dbh, idesc, (kb - kb0 | kk) != 0);  // a_hi * b_hi
+                mma_tf32_ts(acc, ta + kk * 8, dbl, idesc, 1u);                    // a_hi * b_lo
+                mma_tf32_ts(acc, ta + 32 + kk * 8, dbh, idesc, 1u);               // a_lo * b_hi
+              }
             }
             mma_commit(&empty_bar[stage]);
           }
@@ -808,13 +816,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int HWo = d.Ho * d.Wo;
       const int M = d.batch * HWo;
       const int kblocks = min(d.kper, d.kblocks - ks * d.kper);
-      const int slot = kBf16 ? 0 : it % Cfg::kCorrSlots;
+      const int slot = Cfg::kSplitCorr ? it % (Cfg::kSplitCorr ? Cfg::kCorrSlots : 1) : 0;
       float sum[BN];
 #pragma unroll
       for (int i = 0; i < BN; ++i) sum[i] = 0.0f;
       for (int kb0 = 0; kb0 < kblocks; kb0 += kChunk, ++gc) {
-        const int buf = gc & 1;
-        if (ew == 0) PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc >> 1) & 1, 0x103));
+        const int buf = gc % NB;
+        if (ew == 0) PROF_WAIT(1, mbar_wait(&acc_full[buf], (gc / NB) & 1, 0x103));
         asm volatile("bar.sync 2, 128;" ::: "memory");
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + Cfg::kTmemMainCol + buf * BN;
@@ -830,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
       }
-      if constexpr (!kBf16) {
+      if constexpr (Cfg::kSplitCorr) {
         // the tile's last acc_full commit covered every MMA of the tile, so the
         // correction accumulator of this slot is complete as well
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + slot * BN;
@@ -1316,7 +1324,14 @@ extern "C" int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, ui
     tobf_conv_desc& d = descs[i];
     d.tma = 0;
     d.tmap = nullptr;
-    const bool ok = enc && d.Cp % kBK == 0 && d.k1 <= 256 && d.k2 <= 256 && d.stride >= 1 && d.stride <= 8 &&
+    // one load = 32 channels of one filter tap x 128 pixels (128-B rows,
+    // 128B swizzle: the cp.async staging layout), so Cp % 32 == 0 only. A
+    // variant loading 16/8/4-channel pieces for the other Cp was measured
+    // slower than the cp.async gather for them (RN18 step conv 11.5 vs
+    // 10.1 ms: the stem's 8 loads of 16-B rows per K block), so those
+    // problems keep cp.async, in the SAME launch (per-tile A mode).
+    const int cpp = 32;
+    const bool ok = enc && d.Cp % cpp == 0 && d.k1 <= 256 && d.k2 <= 256 && d.stride >= 1 && d.stride <= 8 &&
                     d.pad <= 127 && d.pad - (d.k1 - 1) >= -128 && d.pad - (d.k2 - 1) >= -128 &&
                     (reinterpret_cast<uintptr_t>(d.x) & 15) == 0 && d.ldx % 4 == 0;
     if (!ok) continue;
@@ -1328,12 +1343,14 @@ extern "C" int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, ui
     const int upper[2] = {d.pad - (d.k2 - 1), d.pad - (d.k1 - 1)};      // (w, h)
     const cuuint32_t estr[4] = {1, (cuuint32_t)d.stride, (cuuint32_t)d.stride, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(d.x), dims, strides, lower,
-                           upper, kBK /*channels per pixel*/, kBM /*pixels per column*/, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           upper, (cuuint32_t)cpp /*channels per pixel*/, kBM /*pixels per column*/, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           cpp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : cpp == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : cpp == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) continue;
     d.tmap = reinterpret_cast<const void*>(tmap_dev + 128 * (uint64_t)i);
-    d.tma = 1;
+    d.tma = cpp;
     ++count;
   }
   *n_tma = count;

@@ -813,9 +813,8 @@ class PopulationRun:
         conv_bn = np.concatenate([p.conv_bn for p in plans])
         conv_k = np.concatenate([p.conv_k for p in plans])
         ew_level = np.concatenate([p.ew_level for p in plans])
-        # TMA im2col for every conv whose 32-channel K blocks stay within one
-        # filter tap (Cp % 32 == 0): one 128-B tensor map per problem, encoded
-        # on the host now that the input pointers are final
+        # TMA im2col for the A operand of every conv: one 128-B tensor map per
+        # problem, encoded on the host now that the input pointers are final
         conv_tma = np.zeros(len(conv), np.int64)
         if len(conv) and TMA_A:
             self._tmaps = torch.empty(128 * len(conv) + 128, dtype=torch.uint8, device=ctx.device)
@@ -826,12 +825,13 @@ class PopulationRun:
                                           tbase, C.byref(ntma)), "conv tensor maps")
             if ntma.value:
                 ctx._staged(host_maps, self._tmaps[tbase - self._tmaps.data_ptr():][:len(host_maps)])
-            conv_tma = conv["tma"].astype(np.int64)
-        # one launch per (level, BN, A mode), long K first; one ew launch per level
-        order = np.lexsort((-conv_k, -conv_tma, -conv_bn, conv_level))
+            conv_tma = (conv["tma"] > 0).astype(np.int64)
+        # one launch per (level, BN), long K first (TMA-capable when any of its
+        # problems is: the A mode is per tile); one ew launch per level
+        order = np.lexsort((-conv_k, -conv_bn, conv_level))
         conv = conv[order]
-        ckey = np.stack([conv_level[order], conv_bn[order], conv_tma[order]], 1) if len(conv) else \
-            np.zeros((0, 3), np.int64)
+        conv_tma = conv_tma[order]
+        ckey = np.stack([conv_level[order], conv_bn[order]], 1) if len(conv) else np.zeros((0, 2), np.int64)
         eorder = np.argsort(ew_level, kind="stable")
         ew = ew[eorder]
         ekey = ew_level[eorder]
@@ -842,7 +842,7 @@ class PopulationRun:
         conv_ptr = conv.ctypes.data
         for lo, hi in _runs(ckey):
             bn = int(ckey[lo, 1])
-            tma_flag = N.CONV_TMA if ckey[lo, 2] else 0
+            tma_flag = N.CONV_TMA if conv_tma[lo:hi].any() else 0
             # split-K for groups too small to fill the SMs; workspace offsets
             # now, one workspace shared by every (stream-ordered) conv launch
             ctx.check(lib.tobf_conv_prepare_split_ex(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
