@@ -257,8 +257,107 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
   }
 }
 
-// Any other chain (several affines / operands, dummy-add constants): a
-// per-element interpreter of the descriptor's steps.
+// Chains with dummy-add constants, 3-4 tensor / constant operands or two
+// folded BatchNorms (dimension-mode candidates: a layer with n dummies is
+// Conv -> Add(const) x n -> BN -> ReLU, fused): like epi_rows, U rows per
+// batch with EVERY step's operands loaded (16-B vectors) before the chain
+// runs in step order, so a batch pays one memory latency, not one per step.
+// Round 1 ran these through the per-element interpreter below: scalar loads,
+// one latency per step per row — the VGG-16 stem level with dummies took
+// 8.9 ms of a 54 ms bf16 population forward.
+#ifndef TOBF_EPI_OPS
+#define TOBF_EPI_OPS 1
+#endif
+struct EpiOps {
+  const float* ptr[4];
+  int aux[4];        // tensor: channel stride; const: batch period
+  int is_const[4];
+  float4 sc[2], sh[2];
+  int HWo, Cpo;
+};
+
+template <int BN, int U>
+__device__ __forceinline__ void epi_rows_ops(const EpiArgs ea, const EpiOps& eo, uint32_t prog, int nsteps, int ew,
+                                             int lane) {
+  constexpr int kLanesPerRow = BN / 4;
+  constexpr int kRowsPerIter = 32 / kLanesPerRow;
+  constexpr int kRowStep = 4 * kRowsPerIter;
+  const int sub = lane / kLanesPerRow;
+  const int g = lane % kLanesPerRow;
+  const int c = ea.c;
+  if (!ea.cvalid) return;
+  const bool cfull = c + 3 < ea.j;
+#pragma unroll 1
+  for (int r0 = ew * kRowsPerIter + sub; r0 < kBM; r0 += kRowStep * U) {
+    float4 o[U], opnd[4][U];
+    int mrow[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int row = r0 + q * kRowStep;
+      mrow[q] = ea.m0 + row;
+      const bool ok = row < kBM && mrow[q] < ea.M;
+      o[q] = ok ? lds_tile(ea.epi_s, row, g, BN) : make_float4(0.f, 0.f, 0.f, 0.f);
+      int pix = 0, img = 0;
+      if (ok) {
+        img = mrow[q] / eo.HWo;
+        pix = mrow[q] - img * eo.HWo;
+      } else {
+        mrow[q] = -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        opnd[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok && eo.ptr[k] != nullptr) {
+          const int64_t base = eo.is_const[k] ? ((int64_t)(img % eo.aux[k]) * eo.HWo + pix) * eo.Cpo
+                                              : (int64_t)mrow[q] * eo.aux[k];
+          opnd[k][q] = ldg_nc4(eo.ptr[k] + base + c);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int s = 0; s < nsteps; ++s) {
+      const uint32_t f = (prog >> (5 * s)) & 31u;
+      const uint32_t op = f & 7u, slot = f >> 3;
+      if (op == TOBF_EPI_AFFINE) {
+        const float4 a = slot ? eo.sc[1] : eo.sc[0], b = slot ? eo.sh[1] : eo.sh[0];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          o[q].x = o[q].x * a.x + b.x; o[q].y = o[q].y * a.y + b.y;
+          o[q].z = o[q].z * a.z + b.z; o[q].w = o[q].w * a.w + b.w;
+        }
+      } else if (op == TOBF_EPI_RELU) {
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          o[q].x = fmaxf(o[q].x, 0.0f); o[q].y = fmaxf(o[q].y, 0.0f);
+          o[q].z = fmaxf(o[q].z, 0.0f); o[q].w = fmaxf(o[q].w, 0.0f);
+        }
+      } else {  // ADD_TENSOR / ADD_CONST: operand `slot`
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k != (int)slot) continue;
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            o[q].x += opnd[k][q].x; o[q].y += opnd[k][q].y; o[q].z += opnd[k][q].z; o[q].w += opnd[k][q].w;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (mrow[q] < 0) continue;
+      if (!cfull) {
+        if (c + 0 >= ea.j) o[q].x = 0.0f;
+        if (c + 1 >= ea.j) o[q].y = 0.0f;
+        if (c + 2 >= ea.j) o[q].z = 0.0f;
+        if (c + 3 >= ea.j) o[q].w = 0.0f;
+      }
+      stg128(ea.y + (int64_t)mrow[q] * ea.ldy + c, o[q]);
+    }
+  }
+}
+
+// Anything else (more than 4 operands or 2 BatchNorms): a per-element
+// interpreter of the descriptor's steps.
 template <int BN>
 __device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_conv_desc& d, int ew, int lane,
                                               int HWo) {
@@ -586,11 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (g >= issued) break;
       const uint32_t sbit = 1u << (g % SD);
       const bool blk_tma = TMA && (tma_bits & sbit);
-      if (blk_tma) {  // warp 7's TMA im2col load of this block (same 128B-swizzled layout)
-        PROF_WAIT(2, mbar_wait(&stg_full[g % SD], (g / SD) & 1, 0x11a));
-      } else {
-        PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
-      }
+      // TMA launches: EVERY block passes stg_full (warp 7 arrives for
+      // cp.async blocks too), so the A warps can never run SD blocks ahead of
+      // warp 7 and complete two phases of a slot's stg_empty before it waits
+      // on the first (a mixed cp.async / TMA launch hung or faulted that way)
+      if (TMA) PROF_WAIT(2, mbar_wait(&stg_full[g % SD], (g / SD) & 1, 0x11a));
+      if (!blk_tma) PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
       const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
       float4 row[8];
       if (TMA && (zero_bits & sbit)) {
@@ -964,9 +1064,48 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       // Simple chains (<= 1 folded BN, <= 2 tensor operands, no dummy
       // constant) cover > 95% of the output volume the lowering emits for
-      // RN18 sequence candidates; anything else runs the per-element interpreter.
+      // RN18 sequence candidates; chains with constants / up to 4 operands /
+      // 2 BNs take epi_rows_ops; anything else the per-element interpreter.
       if (naff <= 1 && nld <= 2 && nconst == 0) {
         epi_rows<BN>(ea, prog, nepi, nld, ew, lane);
+      } else if (TOBF_EPI_OPS && naff <= 2 && nld + nconst <= 4) {
+        EpiOps eo;
+        uint32_t prog5 = 0;
+        int na = 0, nk = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          eo.ptr[k] = nullptr;
+          eo.aux[k] = 1;
+          eo.is_const[k] = 0;
+        }
+        eo.sc[0] = eo.sc[1] = eo.sh[0] = eo.sh[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        eo.HWo = HWo;
+        eo.Cpo = d.Cpo;
+#pragma unroll
+        for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+          uint32_t slot = 0;
+          if (eop[s] == TOBF_EPI_AFFINE) {
+            slot = na;
+            if (ea.cvalid) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(eptr[s] + ea.c));
+              const float4 b = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + ea.c));
+              if (na == 0) { eo.sc[0] = a; eo.sh[0] = b; } else { eo.sc[1] = a; eo.sh[1] = b; }
+            }
+            ++na;
+          } else if (eop[s] == TOBF_EPI_ADD_TENSOR || eop[s] == TOBF_EPI_ADD_CONST) {
+            slot = nk;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k == nk) {
+                eo.ptr[k] = eptr[s];
+                eo.aux[k] = max(eaux[s], 1);
+                eo.is_const[k] = eop[s] == TOBF_EPI_ADD_CONST;
+              }
+            ++nk;
+          }
+          prog5 |= (uint32_t)((eop[s] & 7) | (slot << 3)) << (5 * s);
+        }
+        epi_rows_ops<BN, 4>(ea, eo, prog5, nepi, ew, lane);
       } else {
         epi_rows_generic<BN>(ea, d, ew, lane, HWo);
       }
