@@ -342,8 +342,12 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, f
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+// Barrier A only orders this CTA's earlier shared-memory READS of h_{t-1}
+// (their values are already consumed by the gate FMAs) before the other
+// CTAs' remote writes of h_t: no release fence needed (barrier B, which
+// publishes the DSMEM writes, keeps release/acquire).
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const float4 hold = *reinterpret_cast<const float4*>(hv + (F + unit) * HS + kRB * w);
     // barrier A: every CTA is done reading h_{t-1}; its latency hides behind
     // the activations and the next feature row
-    cluster_arrive();
+    cluster_arrive_relaxed();
     double f_next[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
