@@ -338,6 +338,21 @@ __global__ void __launch_bounds__(TPC * 32, 1)
 // oracle/fitness_ref.c.
 constexpr int kRB = 4;  // traces per thread
 
+// fp32 pairs for FFMA2 (fma.rn.f32x2): element 0 in the low word
+__device__ __forceinline__ uint64_t f2pack(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -440,24 +455,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int j = 0; j < 2; ++j)
       if (xl[j]) hv[xk[j] * HS + xtr[j]] = x_cur[j];
     __syncwarp();
-    float acc[4][kRB];
+    // accumulators as fp32 PAIRS (traces 0-1, 2-3) updated with FFMA2
+    // (fma.rn.f32x2: two independent correctly rounded fmaf — the same
+    // per-accumulator sequence bias, x[0..F), h[0..H) as fmaf); the weight
+    // is the scalar operand broadcast to both lanes, the h pair comes straight
+    // from the 16-B k-major row. 8 FFMA2 per K instead of 16 FFMA.
+    uint64_t acc2[4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const float bv = bsm[g * 32 + u];
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) acc[g][r] = bv;
+      acc2[g][0] = acc2[g][1] = f2pack(bv, bv);
     }
     const uint2* wrow = wq + u;
 #pragma unroll 2
     for (int kq = 0; kq < Lq; ++kq) {
       const uint2 w0 = wrow[(kq * 4 + 0) * kLstmUnits], w1 = wrow[(kq * 4 + 1) * kLstmUnits];
       const uint2 w2 = wrow[(kq * 4 + 2) * kLstmUnits], w3 = wrow[(kq * 4 + 3) * kLstmUnits];
-      const float4 h0 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 0) * HS);
-      const float4 h1 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 1) * HS);
-      const float4 h2 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 2) * HS);
-      const float4 h3 = *reinterpret_cast<const float4*>(hrow + (kq * 4 + 3) * HS);
-      const float hs[4][kRB] = {{h0.x, h0.y, h0.z, h0.w}, {h1.x, h1.y, h1.z, h1.w},
-                                {h2.x, h2.y, h2.z, h2.w}, {h3.x, h3.y, h3.z, h3.w}};
+      ulonglong2 hq[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hq[e] = *reinterpret_cast<const ulonglong2*>(hrow + (kq * 4 + e) * HS);
       const float wg[4][4] = {{bf16lo(w0.x), bf16hi(w0.x), bf16lo(w0.y), bf16hi(w0.y)},
                               {bf16lo(w1.x), bf16hi(w1.x), bf16lo(w1.y), bf16hi(w1.y)},
                               {bf16lo(w2.x), bf16hi(w2.x), bf16lo(w2.y), bf16hi(w2.y)},
@@ -465,20 +481,28 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
       for (int e = 0; e < 4; ++e)
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-          for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wg[g][e], hs[e][r], acc[g][r]);
+        for (int g = 0; g < 4; ++g) {
+          const uint64_t wb = f2pack(wg[g][e], wg[g][e]);
+          acc2[g][0] = ffma2(wb, hq[e].x, acc2[g][0]);
+          acc2[g][1] = ffma2(wb, hq[e].y, acc2[g][1]);
+        }
     }
     for (int e = 0; e < (L & 3); ++e) {
-      const float4 hx = *reinterpret_cast<const float4*>(hrow + (Lq * 4 + e) * HS);
-      const float hs[kRB] = {hx.x, hx.y, hx.z, hx.w};
+      const ulonglong2 hx = *reinterpret_cast<const ulonglong2*>(hrow + (Lq * 4 + e) * HS);
       const uint16_t* wt = wtail + e * 4 * kLstmUnits + u;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const float wv = __uint_as_float((uint32_t)wt[g * 32] << 16);
-#pragma unroll
-        for (int r = 0; r < kRB; ++r) acc[g][r] = fmaf(wv, hs[r], acc[g][r]);
+        const uint64_t wb = f2pack(wv, wv);
+        acc2[g][0] = ffma2(wb, hx.x, acc2[g][0]);
+        acc2[g][1] = ffma2(wb, hx.y, acc2[g][1]);
       }
+    }
+    float acc[4][kRB];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      f2unpack(acc2[g][0], acc[g][0], acc[g][1]);
+      f2unpack(acc2[g][1], acc[g][2], acc[g][3]);
     }
     const float4 hold = *reinterpret_cast<const float4*>(hv + (F + unit) * HS + kRB * w);
     // barrier A: every CTA is done reading h_{t-1}; its latency hides behind
