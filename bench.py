@@ -10,9 +10,10 @@ greedy CTC + Levenshtein LER vs L*, Eq. 10 reward — plus (N > 1) the NCCL
 all-gather of the fitness records. Weak scaling: per-GPU work is fixed.
 
   value   device-timed, candidate programs already resident in HBM
-  e2e     through the public API (PopulationEvaluator.prepare + run + collect):
-          host apply_plan, weight upload (H2D) + packing, descriptor staging,
-          device pipeline, record read-back (D2H) — every step, cold caches
+  e2e     through the public API (PopulationEvaluator.evaluate_stream, two
+          steps in flight): host apply_plan, weight upload (H2D) + packing,
+          descriptor staging, device pipeline, record read-back (D2H) — every
+          step, cold caches; e2e.per_call = one evaluate_records per step
   --impl reference   the reference itself (traceobf 0.1.0 from baseline/_ref:
           apply_plan, equivalence_check, profile_pipeline; restated fitness)
           on the host CPU, one candidate per core in parallel with
@@ -60,6 +61,11 @@ def parse():
     ap.add_argument("--micro", type=lambda v: v if v == "auto" else [int(x) for x in v.split(",")], default="auto",
                     help="e2e micro-batch sizes, e.g. 16 or 8,24 (host prep overlaps the device run); "
                          "auto = evaluate.auto_micro")
+    ap.add_argument("--e2e-depth", type=int, default=2,
+                    help="e2e steps in flight through PopulationEvaluator.evaluate_stream "
+                         "(0 = one evaluate_records call per step)")
+    ap.add_argument("--stream-micro", type=lambda v: None if v == "none" else [int(x) for x in v.split(",")],
+                    default=None, help="micro-batch sizes inside each streamed e2e step (none = one launch per step)")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the LER / cfg5 fitness kernel sweeps")
     ap.add_argument("--ler-pairs", type=int, default=10_000_000, help="LER sweep size (SURVEY 8(d): >= 1e7 pairs)")
     ap.add_argument("--cfg4-pop", type=int, default=256, help="cfg4 (VGG-16 dimension) population; 0 = skip")
@@ -341,7 +347,8 @@ def workload_generation(args) -> dict | None:
     workers prepare micro-batch i+1 while the device runs micro-batch i).
     Run as a separate bench process so its arenas do not stack on this one's."""
     cmd = [sys.executable, str(ROOT / "bench.py"), "--pop", str(args.gen_pop), "--steps", "5", "--warmup", "3",
-           "--no-sweeps", "--no-cpu-baseline", "--cfg4-pop", "0", "--gen-pop", "0", "--seed", str(args.seed)]
+           "--no-sweeps", "--no-cpu-baseline", "--cfg4-pop", "0", "--gen-pop", "0", "--e2e-depth", "0",
+           "--seed", str(args.seed)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
         d = json.loads(r.stdout.strip().splitlines()[-1])
@@ -537,42 +544,61 @@ def main_ours(args):
         plans_e2e = population_plans(vanilla, P * world * (steps_total + 1), args.seed + 1)
         per_step = P * world
 
-        host_ms = {}
+        def shards(lo, hi):
+            # one step's plans; cold caches: every weight re-uploaded, every
+            # image re-packed (dropped while the previous step may still run:
+            # the allocator is stream-ordered)
+            for s in range(lo, hi):
+                ctx.clear_cache()
+                yield plans_e2e[s * per_step + rank * P: s * per_step + (rank + 1) * P]
 
-        def e2e_step(s):
-            ctx.clear_cache()
-            shard = plans_e2e[s * per_step + rank * P: s * per_step + (rank + 1) * P]
-            rec = pe.evaluate_records(shard, micro=args.micro, memo={}, base=rank * P)
-            for k, v in pe.last_host_ms.items():
-                host_ms[k] = host_ms.get(k, 0.0) + v
-            if world > 1:
-                from paper_2107_09789_b200 import dist as tdist
-                rec = tdist.gather_records(rec, per_step)
-            return rec
+        def e2e_run(depth):
+            """Warm-up, then ``args.steps`` timed steps through the public API:
+            evaluate_stream with ``depth`` steps in flight, or (depth 0) one
+            evaluate_records call per step, nothing overlapped across steps."""
+            def run(lo, hi):
+                if depth:
+                    yield from pe.evaluate_stream(shards(lo, hi), micro=args.stream_micro, base=rank * P,
+                                                  depth=depth, cold=True)
+                else:
+                    for shard in shards(lo, hi):
+                        yield pe.evaluate_records(shard, micro=args.micro, memo={}, base=rank * P)
+            host_ms = {}
+            for _ in run(0, args.warmup):
+                pass
+            torch.cuda.synchronize()
+            barrier()
+            h0 = ctx.h2d_bytes
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record()
+            d2h = 0
+            for r in run(args.warmup, steps_total):
+                for k, v in pe.last_host_ms.items():
+                    host_ms[k] = host_ms.get(k, 0.0) + v
+                if world > 1:
+                    from paper_2107_09789_b200 import dist as tdist
+                    r = tdist.gather_records(r, per_step)
+                d2h += r.nbytes
+            f1.record()
+            torch.cuda.synchronize()
+            barrier()
+            e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
+            return e2e_ms, int((ctx.h2d_bytes - h0) / args.steps), int(d2h / args.steps), host_ms
 
-        for s in range(args.warmup):
-            e2e_step(s)
-        torch.cuda.synchronize()
-        barrier()
-        host_ms.clear()
-        h0 = ctx.h2d_bytes
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record()
-        d2h = 0
-        for s in range(args.warmup, steps_total):
-            r = e2e_step(s)
-            d2h += r.nbytes
-        f1.record()
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
         x_bytes = pe.x_host.numel() * 4
+        call = e2e_run(0)
+        e2e_ms, h2d, d2h, host_ms = e2e_run(args.e2e_depth) if args.e2e_depth else call
+        call_ms = call[0]
         e2e = {"value": world * P / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int((ctx.h2d_bytes - h0) / args.steps) + x_bytes,
-               "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d + x_bytes, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "steps_in_flight": args.e2e_depth,
+               "per_call": {"value": world * P / (call_ms / 1e3), "ms_per_step": call_ms,
+                            "micro_batch": list(auto_micro(P)) if args.micro == "auto" else args.micro,
+                            "note": "one evaluate_records call per step, no overlap across steps"},
                "host_ms_per_step": {k: round(v / args.steps, 2) for k, v in host_ms.items()},
-               "micro_batch": list(auto_micro(P)) if args.micro == "auto" else args.micro, "host_workers": pe.pool.workers if pe.pool is not None else 0}
+               "micro_batch": (args.stream_micro or [P]) if args.e2e_depth else
+               (list(auto_micro(P)) if args.micro == "auto" else args.micro), "host_workers": pe.pool.workers if pe.pool is not None else 0}
         pe.close()
 
     # ---- cpu baseline (rank 0, N == 1 only)

@@ -288,6 +288,11 @@ int tobf_version(void);
 /* Reads and clears the device fault word; returns TOBF_E_FAULT if a bounded
  * wait timed out since the last check. */
 int tobf_check_fault(void* stream);
+/* Enqueues a read of that fault word into ``host`` (pinned, 4 bytes) on
+ * ``stream`` without synchronising: a batch's results and its fault word come
+ * back together behind its last kernel; a nonzero word is then raised (and
+ * cleared) by tobf_check_fault. */
+int tobf_fault_async(int* host, void* stream);
 int tobf_device_sync(void);
 
 #ifdef __cplusplus

@@ -124,6 +124,7 @@ SIGNATURES = {
     "tobf_last_error": (C.c_char_p, []),
     "tobf_version": (C.c_int, []),
     "tobf_check_fault": (C.c_int, [_vp]),
+    "tobf_fault_async": (C.c_int, [_vp, _vp]),
     "tobf_device_sync": (C.c_int, []),
 }
 

@@ -1570,6 +1570,14 @@ extern "C" int tobf_conv_prof_read(unsigned long long* out, int reset) {
 }
 #endif
 
+extern "C" int tobf_fault_async(int* host, void* stream) {
+  if (host == nullptr) return tobf_fail(TOBF_E_INVALID, "tobf_fault_async: null host word");
+  const cudaError_t e = cudaMemcpyFromSymbolAsync(host, g_tobf_fault, sizeof(int), 0, cudaMemcpyDeviceToHost,
+                                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "tobf_fault_async: %s", cudaGetErrorString(e));
+  return TOBF_OK;
+}
+
 extern "C" int tobf_check_fault(void* stream) {
   int h = 0;
   cudaError_t e = cudaMemcpyFromSymbolAsync(&h, g_tobf_fault, sizeof(int), 0, cudaMemcpyDeviceToHost,

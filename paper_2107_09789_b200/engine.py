@@ -210,6 +210,34 @@ class DeviceContext:
         self.check(rc, "device pipeline")
 
 
+class Readback:
+    """One batch's results on their way to the host: stream-ordered D2H copies
+    into pinned buffers plus the device fault word, enqueued right behind the
+    batch's last kernel. ``wait`` blocks on that point only, so later batches
+    already queued on the engine stream keep the device busy meanwhile (a
+    ``.cpu()`` or stream synchronise would wait for them too)."""
+
+    def __init__(self, ctx: "DeviceContext", tensors: dict[str, torch.Tensor]):
+        self.ctx = ctx
+        with torch.cuda.stream(ctx.stream):
+            self.host = {}
+            for k, t in tensors.items():
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t, non_blocking=True)
+                self.host[k] = h
+            self.fault = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            ctx.check(ctx.lib.tobf_fault_async(C.c_void_p(self.fault.data_ptr()), C.c_void_p(ctx.sp)),
+                      "fault word read")
+            self.done = torch.cuda.Event()
+            self.done.record(ctx.stream)
+
+    def wait(self) -> dict[str, np.ndarray]:
+        self.done.synchronize()
+        if int(self.fault[0]) != 0:
+            self.ctx.sync()  # raises TOBF_E_FAULT (and clears the word)
+        return {k: h.numpy() for k, h in self.host.items()}
+
+
 def cat_records(arrs: list, dtype: np.dtype) -> np.ndarray:
     """np.concatenate for structured record arrays of one dtype, through
     opaque void views: numpy 2 otherwise re-promotes every (nested) field per

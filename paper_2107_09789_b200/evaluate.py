@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import cat_records, device
+from .engine import Readback, cat_records, device
 from .refcompat import to_engine
 from .executor import (DEFAULT_TOL, PlanTables, PopulationRun, compare_outputs, lower, plan_forward, precision_code,
                        trial_inputs)
@@ -34,7 +34,8 @@ from .attacker import EPSILON, FitnessReport, Predictor, bagged_predictors, deco
 from .ir import Graph, analyze, label_sequence
 from .knobs import ObfuscationPlan, TransformError, apply_plan, apply_plan_analyzed
 from .trace import (BUILTIN_PROFILES, DeviceProfile, LeakageCase, _SCHEDULE_CACHE, finish_trace, prepare_trace,
-                    prepare_trace_records, resolve_first_seen, run_trace, trace_population, trace_records)
+                    prepare_trace_records, readback_trace, resolve_first_seen, run_trace, trace_population,
+                    trace_records)
 
 RECORD_DTYPE = np.dtype([("reward", "<f8"), ("mean_ler", "<f8"), ("latency", "<f8"), ("worst", "<f4"),
                          ("ok", "<i4"), ("feasible", "<i4"), ("ntok", "<i4")])
@@ -383,8 +384,23 @@ class PopulationEvaluator:
         return {"R": R, "mean": mean, "T": T, "ok": ok, "worst": worst, "ntok": att["ntok"], "trace": tp,
                 "events": ev if ev is not None else {}, "feasible": prep["feasible"], "lers": att["lers"]}
 
+    _RESULTS = ("R", "mean", "T", "worst", "ok", "ntok")
+
+    def readback(self, out: dict) -> None:
+        """Enqueue the batch's result D2H (and the fault word) behind its
+        reward kernel (engine.Readback): ``collect`` then waits for this batch
+        only."""
+        out["readback"] = Readback(self.ctx, {k: out[k] for k in self._RESULTS})
+
     def collect(self, out: dict) -> np.ndarray:
         rec = np.zeros(len(out["feasible"]), dtype=RECORD_DTYPE)
+        rb = out.get("readback")
+        if rb is not None:
+            h = rb.wait()
+            rec["reward"], rec["mean_ler"], rec["latency"] = h["R"], h["mean"], h["T"]
+            rec["worst"], rec["ok"], rec["ntok"] = h["worst"], h["ok"], h["ntok"]
+            rec["feasible"] = np.asarray(out["feasible"], dtype=np.int32)
+            return rec
         rec["reward"] = out["R"].cpu().numpy()
         rec["mean_ler"] = out["mean"].cpu().numpy()
         rec["latency"] = out["T"].cpu().numpy()
@@ -397,9 +413,74 @@ class PopulationEvaluator:
 
     def evaluate_records(self, plans: list[ObfuscationPlan], micro="auto", memo: dict | None = None,
                          workers: int | None = None, base: int | None = None) -> np.ndarray:
-        """Records for ``plans`` with host preparation of micro-batch i+1
-        overlapping the device pipeline of micro-batch i (launches are async;
-        the only host waits are the final read-backs). With ``workers`` != 0
+        """Records for ``plans`` (see ``launch``): launch, then wait for them."""
+        return self.complete(self.launch(plans, micro, memo, workers, base))
+
+    def evaluate_stream(self, batches, micro=None, memo: dict | None = None, workers: int | None = None,
+                        base: int | None = None, depth: int = 2, cold: bool = False):
+        """Records of each batch of an iterable of plan batches, in order, with
+        up to ``depth`` batches in flight: the host prepares and launches batch
+        k+1 (worker apply_plan, memo resolution, linking, uploads) while the
+        device still runs batch k, whose results come back through its own
+        stream-ordered readback. Every batch still uploads its inputs and reads
+        its records back; only the waiting overlaps. ``micro`` (default: one
+        launch per batch — batches already overlap one another) as in
+        ``launch``.
+
+        Schedules: with a shared memo (default) the batches in flight share one
+        first-seen table, so a signature pending in batch k is searched from
+        the same descriptor in batch k+1 — the schedules equal a one-batch-at-
+        a-time run. ``cold``: each batch gets its own empty memo (the
+        benchmark's cold-search policy). A sharded evaluator with a shared
+        memo runs one batch at a time (its exchange resolves against the memo,
+        which must hold the previous batch)."""
+        from collections import deque
+        if self.exchange is not None and not cold:
+            depth = 1
+        nworkers = self._host_workers(workers)
+        it = iter(batches)
+
+        def pull():
+            # the next batch, already dealt to the host workers: they prepare
+            # batch k+1 while the parent links and launches batch k
+            plans = next(it, None)
+            if plans is None:
+                return None
+            plans = to_engine(list(plans))
+            pre = None
+            if nworkers and len(plans) > 1:
+                self._ensure_pool(nworkers)
+                pre = self.pool.submit(plans, per_job=1)
+            return plans, pre
+
+        first_seen: dict = {}
+        inflight: deque = deque()
+        cur = pull()
+        while cur is not None:
+            nxt = pull()
+            m = {} if cold else (self.memo if memo is None else memo)
+            inflight.append(self.launch(cur[0], micro, m, nworkers, base, pre=cur[1],
+                                        first_seen=None if cold or self.exchange is not None else first_seen))
+            cur = nxt
+            while len(inflight) >= max(depth, 1):
+                yield self.complete(inflight.popleft())
+        while inflight:
+            yield self.complete(inflight.popleft())
+
+    @staticmethod
+    def _host_workers(workers: int | None) -> int:
+        if workers is None:
+            from .hostpipe import default_workers
+            return default_workers() if os.environ.get("TOBF_HOST_WORKERS", "") != "0" else 0
+        return workers
+
+    def launch(self, plans: list[ObfuscationPlan], micro="auto", memo: dict | None = None,
+               workers: int | None = None, base: int | None = None, first_seen: dict | None = None,
+               pre: list | None = None) -> dict:
+        """Prepare and launch ``plans`` (``complete`` returns their records),
+        host preparation of micro-batch i+1 overlapping the device pipeline of
+        micro-batch i (launches are async; each micro-batch enqueues its own
+        result readback, the only host waits are in ``complete``). With ``workers`` != 0
         (default: hostpipe.default_workers(), TOBF_HOST_WORKERS=0 disables)
         the per-candidate host work runs in a process pool and the parent only
         links and launches. First-seen schedule semantics hold across
@@ -411,32 +492,35 @@ class PopulationEvaluator:
         ranks ONCE per call, before any micro-batch runs and whatever the
         shard holds (empty, all infeasible, any split), so every rank makes
         the same collective calls; the trace stage of the first micro-batch
-        then waits for the whole shard's host records."""
+        then waits for the whole shard's host records. ``first_seen``: a
+        first-seen table shared with calls still in flight (evaluate_stream).
+        ``pre``: pool handles of ``plans`` already dealt to the host workers
+        (one candidate per job, in order)."""
         memo = self.memo if memo is None else memo
         t_call = time.perf_counter()
         plans = to_engine(list(plans))
         sharded = self.exchange is not None
         if not plans:
-            self.last_host_ms = {}
             if sharded:
                 self._memoise_remote(self._resolve([], [], base, memo), memo)
-            return np.zeros(0, dtype=RECORD_DTYPE)
-        first_seen: dict = {}
+            return {"jobs": [], "t_call": t_call}
+        first_seen = {} if first_seen is None else first_seen
         extra = None
         jobs = []
         bounds = _micro_bounds(len(plans), micro)
-        if workers is None:
-            from .hostpipe import default_workers
-            workers = default_workers() if os.environ.get("TOBF_HOST_WORKERS", "") != "0" else 0
-        if workers and len(plans) > 1:
+        workers = self._host_workers(workers)
+        if pre is not None or (workers and len(plans) > 1):
             self._ensure_pool(workers)
             per_job = 1  # 32 candidates over 14 workers: at most 3 each (2-candidate jobs: 4)
             # deal two jobs per worker now, the rest while waiting for results
             # (encoding + sending 256 plans up front delayed the first result
             # by ~5 ms)
             ahead = 3 * self.pool.workers
-            handles = self.pool.submit(plans[:2 * self.pool.workers], per_job=per_job)
-            sent = min(len(plans), 2 * self.pool.workers)
+            if pre is not None:
+                handles, sent = list(pre), len(plans)
+            else:
+                handles = self.pool.submit(plans[:2 * self.pool.workers], per_job=per_job)
+                sent = min(len(plans), 2 * self.pool.workers)
             got: dict[int, tuple] = {}
             nxt = 0  # next handle to receive
 
@@ -482,10 +566,14 @@ class PopulationEvaluator:
                 # links the forward plans
                 t1 = time.perf_counter()
                 att = self.run_attack(prep)
+                if prep["trace"] is not None:
+                    readback_trace(prep["trace"])
                 t2 = time.perf_counter()
                 self.link_forward(prep, tables)
                 t3 = time.perf_counter()
-                jobs.append((prep, self.run_forward(prep, att)))
+                out = self.run_forward(prep, att)
+                self.readback(out)
+                jobs.append((prep, out))
                 prep["host_ms"]["launch"] = 1e3 * (t2 - t1 + time.perf_counter() - t3)
         else:
             cands = None
@@ -500,8 +588,22 @@ class PopulationEvaluator:
                                     extra=extra if b == 0 else None,
                                     cands=cands[lo:hi] if cands is not None else None, shard=False)
                 t1 = time.perf_counter()
-                jobs.append((prep, self.run(prep, cold_schedules=False)))
+                att = self.run_attack(prep)
+                if prep["trace"] is not None:
+                    readback_trace(prep["trace"])
+                out = self.run_forward(prep, att)
+                self.readback(out)
+                jobs.append((prep, out))
                 prep["host_ms"]["launch"] = 1e3 * (time.perf_counter() - t1)
+        return {"jobs": jobs, "t_call": t_call}
+
+    def complete(self, state: dict) -> np.ndarray:
+        """Wait for a launched call's batches (their own readbacks), fold the
+        searched schedules into the memo, and return the records."""
+        jobs = state["jobs"]
+        if not jobs:
+            self.last_host_ms = {}
+            return np.zeros(0, dtype=RECORD_DTYPE)
         t1 = time.perf_counter()
         recs = [self.collect(out) for _, out in jobs]
         jobs[0][0]["host_ms"]["collect"] = 1e3 * (time.perf_counter() - t1)
@@ -512,7 +614,7 @@ class PopulationEvaluator:
         jobs[0][0]["host_ms"]["finish_trace"] = 1e3 * (time.perf_counter() - t2)
         self.last_host_ms = {k: sum(p["host_ms"].get(k, 0.0) for p, _ in jobs) for k in jobs[0][0]["host_ms"]}
         out = cat_records(recs, RECORD_DTYPE)
-        self.last_host_ms["total"] = 1e3 * (time.perf_counter() - t_call)
+        self.last_host_ms["total"] = 1e3 * (time.perf_counter() - state["t_call"])
         return out
 
     def evaluate(self, plans: list[ObfuscationPlan]) -> PopulationResult:
@@ -558,6 +660,8 @@ def _micro_bounds(n: int, micro) -> list[tuple[int, int]]:
     """Micro-batch [lo, hi) ranges: ``micro`` is a size (every batch that big,
     the last one ragged) or a sequence of sizes (the last one repeats), e.g.
     (8, 24): a small first batch gets the device busy early."""
+    if micro is None:
+        return [(0, n)] if n else []
     if isinstance(micro, str):
         if micro != "auto":
             raise ValueError(f"bad micro-batch sizes {micro!r}")

@@ -576,19 +576,45 @@ def run_trace(tp: TracePlan, profile: bool = True, restore: bool = False) -> Non
     ctx.launches += 2
 
 
-def finish_trace(tp: TracePlan) -> None:
-    """Record newly searched schedules in the memo (first-seen) and attach the
-    resolved schedules to the CompiledGraphs (one D2H)."""
+def readback_trace(tp: TracePlan) -> None:
+    """Enqueue finish_trace's D2H (the searched signature rows, and the
+    resolved kernel rows when CompiledGraphs want them) into pinned memory
+    right behind the trace stage, so finish_trace waits for this batch only,
+    not for the batches launched after it."""
     ctx = device()
     need_kern = any(cg is not None for cg in tp.compiled)
     if not tp.pending and not need_kern:
         return
     ns = tp.sigs.numel()
-    host = torch.empty(ns + (tp.kern.numel() if need_kern else 0), dtype=torch.uint8)
-    host[:ns].copy_(tp.sigs)
-    if need_kern:
-        host[ns:].copy_(tp.kern)
-    ctx.sync()
+    with torch.cuda.stream(ctx.stream):
+        host = torch.empty(ns + (tp.kern.numel() if need_kern else 0), dtype=torch.uint8, pin_memory=True)
+        host[:ns].copy_(tp.sigs, non_blocking=True)
+        if need_kern:
+            host[ns:].copy_(tp.kern, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(ctx.stream)
+    tp.readback = (host, ev)
+
+
+def finish_trace(tp: TracePlan) -> None:
+    """Record newly searched schedules in the memo (first-seen) and attach the
+    resolved schedules to the CompiledGraphs (one D2H; enqueued earlier by
+    readback_trace when the caller pipelines batches)."""
+    ctx = device()
+    need_kern = any(cg is not None for cg in tp.compiled)
+    if not tp.pending and not need_kern:
+        return
+    ns = tp.sigs.numel()
+    rb = getattr(tp, "readback", None)
+    if rb is not None:
+        host, ev = rb
+        ev.synchronize()
+    else:
+        host = torch.empty(ns + (tp.kern.numel() if need_kern else 0), dtype=torch.uint8)
+        host[:ns].copy_(tp.sigs)
+        if need_kern:
+            host[ns:].copy_(tp.kern)
+        ctx.sync()
     raw = host.numpy().tobytes()
     sigs = (N.KernDesc * max(tp.nsig, 1)).from_buffer_copy(raw[:ns])
     for i, sig in tp.pending:

@@ -73,6 +73,7 @@ def test_micro_batch_bounds():
     assert _micro_bounds(3, "auto") == [(0, 1), (1, 3)]
     assert _micro_bounds(80, "auto") == [(0, 8), (8, 32), (32, 80)]
     assert _micro_bounds(256, "auto") == [(0, 8), (8, 32), (32, 80), (80, 144), (144, 208), (208, 256)]
+    assert _micro_bounds(32, None) == [(0, 32)] and _micro_bounds(0, None) == []  # evaluate_stream default
     with pytest.raises(ValueError):
         _micro_bounds(4, 0)
 

@@ -398,6 +398,38 @@ def test_micro_batched_records_match_single_batch(ctx):
         assert many["latency"][i] == CM.profile_pipeline(og, "default", d.fusion_limits, d.schedule_strategies, memo)[3]
 
 
+def test_evaluate_stream_matches_per_call(ctx):
+    """evaluate_stream keeps two batches in flight (batch k+1 prepared,
+    uploaded and launched before batch k's readback; caches dropped between
+    batches as the e2e bench does): every batch's records are identical to
+    one evaluate_records call per batch — with a cold memo per batch, and with
+    one shared memo (first-seen schedules carried across the batches in
+    flight, as a one-at-a-time run would carry them through the memo)."""
+    g = fixtures.resnet18(size=64)
+    batches = [_plans(g, "sequence", 5, seed=40 + k) for k in range(4)]
+    ev = Evaluator(predictors=fitness.bagged_predictors(hiddens=(128,)))
+    for workers in (0, 2):
+        pe = PopulationEvaluator(g, ev, trials=2, memo={})
+        try:
+            want = [pe.evaluate_records(b, micro=2, memo={}, workers=workers) for b in batches]
+
+            def feed():
+                for b in batches:
+                    ctx.clear_cache()
+                    yield b
+            got = list(pe.evaluate_stream(feed(), micro=2, workers=workers, depth=2, cold=True))
+            assert [r.tobytes() for r in got] == [r.tobytes() for r in want]
+            shared_want, m = [], {}
+            for b in batches:
+                shared_want.append(pe.evaluate_records(b, micro=2, memo=m, workers=workers))
+            m2: dict = {}
+            shared = list(pe.evaluate_stream(iter(batches), micro=2, memo=m2, workers=workers, depth=3))
+            assert [r.tobytes() for r in shared] == [r.tobytes() for r in shared_want]
+            assert m2 == m
+        finally:
+            pe.close()
+
+
 def test_weight_cache_eviction_is_exact(ctx):
     """A weight cache bounded so tightly that it is dropped at every upload
     (packed images keyed by a device address must go with it, and
