@@ -38,6 +38,24 @@ namespace tobf {
 #define TOBF_CONV_SPLIT_CORR 1
 #endif
 
+// A staging ring depth (K blocks the cp.async gather / TMA im2col loads run
+// ahead of the split into TMEM), per BN.
+#ifndef TOBF_CONV_SD64
+#define TOBF_CONV_SD64 4
+#endif
+#ifndef TOBF_CONV_SD128
+#define TOBF_CONV_SD128 4
+#endif
+
+// problems whose tile_start the scheduler keeps in shared memory (the rest
+// are read from the descriptors)
+#ifndef TOBF_CONV_TAB
+#define TOBF_CONV_TAB 1024
+#endif
+#ifndef TOBF_CONV_ST64
+#define TOBF_CONV_ST64 4
+#endif
+
 constexpr int kBM = 128;
 constexpr int kBK = 32;           // fp32 elements per K block = one 128-B swizzle row
 constexpr int kRowBytes = 128;
@@ -56,17 +74,17 @@ struct ConvCfg {
   // three MMA reads per K step are what the tensor pipe pulls from it.
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kBf16 ? kBBytes : 2 * kBBytes;  // B (tf32: hi, lo)
-  static constexpr int kStages = kBf16 ? 4 : (BN >= 128 ? 2 : 4);
+  static constexpr int kStages = kBf16 ? 4 : (BN >= 128 ? 2 : TOBF_CONV_ST64);
   // fp32 A blocks land here by cp.async (coalesced, zero-filled padding)
   // kStagingKB blocks ahead of the split into TMEM
-  static constexpr int kStagingKB = 4;
+  static constexpr int kStagingKB = BN >= 128 ? TOBF_CONV_SD128 : TOBF_CONV_SD64;
   static constexpr int kStagingOff = kStages * kStageBytes;
   static constexpr int kEpiOff = kStagingOff + kStagingKB * kABytes;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
   static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
   static constexpr int kBarOff = kEpiOff + kEpiBytes + kInfoBytes;
-  static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (1024 ints)
-  static constexpr int kSmem = kTabOff + 4096 + 1024 /*align*/;
+  static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (kSchedTab ints)
+  static constexpr int kSmem = kTabOff + 4 * TOBF_CONV_TAB + 1024 /*align*/;
   // TMEM columns (512 allocated):
   //   [0, kCorrSlots*BN)           (TOBF_CONV_SPLIT_CORR=1 only) correction accumulators
   //                                (a_lo*b_hi + a_hi*b_lo), one per tile slot
@@ -1138,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tile's problem copies its descriptor from the previous ring slot — the
     // round-1 global binary search + 224-B global copy per tile cost a few
     // microseconds of latency on every tile, longer than a 1x1 conv tile.
-    constexpr int kTab = 1024;
+    constexpr int kTab = TOBF_CONV_TAB;
     int* s_tstart = reinterpret_cast<int*>(smem + Cfg::kTabOff);
     for (int i = lane; i < nprob && i < kTab; i += 32) s_tstart[i] = __ldg(&descs[i].tile_start);
     __syncwarp();
