@@ -201,6 +201,14 @@ int tobf_nhwc_to_nchw(const float* x, float* y, int32_t batch, int32_t C, int32_
 int tobf_nchw_to_nhwc(const float* x, float* y, int32_t batch, int32_t C, int32_t H, int32_t W, int32_t ld,
                       void* stream);
 
+/* im2col of a staged NHWC(padded) input for a k1 x k2 conv (stride, pad)
+ * over its first c channels: out[b][yo][xo][Kp], element k = (u*k2 + v)*c + ch
+ * (the weights' (u, v, c) order), zero past K = k1*k2*c and outside the image.
+ * The executor's path for convs reading the graph input with c % 32 != 0
+ * (interpreter.py:22-30's conv2d as a 1x1 GEMM over the shared matrix). */
+int tobf_im2col(const float* x, int32_t batch, int32_t H, int32_t W, int32_t ldx, int32_t c, int32_t k1, int32_t k2,
+                int32_t stride, int32_t pad, int32_t Ho, int32_t Wo, int32_t Kp, float* out, void* stream);
+
 /* ------------------------------------------------------------------ trace */
 
 /* One kernel of a compiled graph, reduced to the exact integers the cost

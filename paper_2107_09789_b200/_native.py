@@ -112,6 +112,7 @@ SIGNATURES = {
     "tobf_equiv_compare": (C.c_int, [_vp, _vp, C.c_int, _i64, _i32, _i32, _f32, _vp, _vp, _vp]),
     "tobf_nhwc_to_nchw": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "tobf_nchw_to_nhwc": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "tobf_im2col": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "tobf_schedule_search": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "tobf_resolve_schedules": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "tobf_profile_kernels": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),

@@ -265,3 +265,52 @@ extern "C" int tobf_nchw_to_nhwc(const float* x, float* y, int32_t B, int32_t C,
   nchw_to_nhwc_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, B, C, H, W, ld);
   return tobf_cuda_check("tobf_nchw_to_nhwc");
 }
+
+// Input im2col (the executor's stem path, executor.py `input_im2col`): for a
+// conv reading the graph input with few channels (c % 32 != 0: no TMA
+// im2col), the K = k1*k2*c elements of every output pixel, in the weights'
+// (u, v, c) order, zero-padded to Kp (a multiple of 32), as one NHWC-like
+// matrix out[n][yo][xo][Kp]. Built once per staged input and shared by every
+// candidate whose conv reads it; the conv becomes a 1x1 GEMM over it fed by
+// the TMA path (RN18 stem: 7x7x3 -> Kp 160 = 5 K blocks instead of 7 padded
+// 7x7x4 blocks gathered with cp.async). One thread per 4 output columns.
+__global__ void im2col_kernel(const float* __restrict__ x, int B, int H, int W, int ldx, int c, int k1, int k2,
+                              int stride, int pad, int Ho, int Wo, int Kp, float* __restrict__ out) {
+  const int64_t quads = (int64_t)B * Ho * Wo * (Kp / 4);
+  const int K = k1 * k2 * c;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < quads;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int kq = (int)(q % (Kp / 4));
+    const int64_t pix = q / (Kp / 4);
+    const int xo = (int)(pix % Wo);
+    const int64_t r = pix / Wo;
+    const int yo = (int)(r % Ho);
+    const int n = (int)(r / Ho);
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = kq * 4 + e;
+      v[e] = 0.0f;
+      if (k < K) {
+        const int uv = k / c, cc = k - uv * c;
+        const int u = uv / k2, vv = uv - u * k2;
+        const int yi = yo * stride - pad + u, xi = xo * stride - pad + vv;
+        if ((unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W)
+          v[e] = __ldg(x + (((int64_t)n * H + yi) * W + xi) * ldx + cc);
+      }
+    }
+    *reinterpret_cast<float4*>(out + pix * Kp + kq * 4) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+extern "C" int tobf_im2col(const float* x, int32_t B, int32_t H, int32_t W, int32_t ldx, int32_t c, int32_t k1,
+                           int32_t k2, int32_t stride, int32_t pad, int32_t Ho, int32_t Wo, int32_t Kp, float* out,
+                           void* stream) {
+  if (!x || !out || B < 1 || H < 1 || W < 1 || c < 1 || ldx < c || k1 < 1 || k2 < 1 || stride < 1 || pad < 0 ||
+      Ho < 1 || Wo < 1 || Kp % 4 || Kp < k1 * k2 * c)
+    return tobf_fail(TOBF_E_INVALID, "tobf_im2col: bad arguments");
+  const int64_t quads = (int64_t)B * Ho * Wo * (Kp / 4);
+  im2col_kernel<<<grid_for(quads, 256), 256, 0, (cudaStream_t)stream>>>(x, B, H, W, ldx, c, k1, k2, stride, pad, Ho,
+                                                                          Wo, Kp, out);
+  return tobf_cuda_check("tobf_im2col");
+}

@@ -298,7 +298,7 @@ _NO_EPI = (0, 0, 0)
 # A symbolic pointer is (space << 56) | value: value = byte offset into the
 # graph's activation block (SP_ARENA) or an index into one of the plan's
 # requirement tables (packed weight images, folded BatchNorms, constants).
-SP_INPUT, SP_ARENA, SP_WIMG, SP_AFFINE, SP_CONST = 1, 2, 3, 4, 5
+SP_INPUT, SP_ARENA, SP_WIMG, SP_AFFINE, SP_CONST, SP_XCOL = 1, 2, 3, 4, 5, 6
 _SP_SHIFT = 56
 _SP_LOW = (1 << _SP_SHIFT) - 1
 
@@ -363,6 +363,9 @@ class ForwardPlan:
     gemm_act_bytes_per_image: int = 0   # conv/linear input + output activations, fp32, once each
     gemm_weight_bytes: int = 0          # conv/linear weights, fp32, once
     prec: int = N.PREC_TF32X3           # conv arithmetic (N.PRECISIONS)
+    # im2col matrices of the staged input the plan's input convs read
+    # (batch, H, W, c, k1, k2, stride, pad, Ho, Wo, Kp): see INPUT_IM2COL
+    xcol: list = field(default_factory=list)
 
 
 def _plan_getstate(self) -> dict:
@@ -409,7 +412,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
     def buf(v: int) -> int:
         return _sym(SP_INPUT, 0) if v < 0 else _sym(SP_ARENA, offs[v])
 
-    tables: dict[str, tuple[dict, list]] = {"wimg": ({}, []), "affine": ({}, []), "const": ({}, [])}
+    tables: dict[str, tuple[dict, list]] = {"wimg": ({}, []), "affine": ({}, []), "const": ({}, []), "xcol": ({}, [])}
 
     def index(table: str, entry) -> int:
         idx, lst = tables[table]
@@ -458,12 +461,28 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
                                              s_out.height * s_out.width * j)
             w_bytes += 4 * k1 * k2 * s_in.channels * j
             w = n.weights if op.w is None else op.w
+            epi = epi_rows(op.steps)
+            nepi = sum(1 for e in epi if e[0])
+            if INPUT_IM2COL and op.src < 0 and n.kind is K.Conv2D and cp % 32 and k1 * k2 > 1:
+                # a conv reading the staged input with few channels: a 1x1 GEMM
+                # over the input's im2col matrix (shared by every candidate of
+                # the run, built once per staged input), K = k1*k2*c rounded up
+                # to 32 (RN18 stem: 160 instead of 7x7x4 = 196 -> 224), A by TMA
+                ho, wo = s_out.height, s_out.width
+                kp = -(-(k1 * k2 * s_in.channels) // 32) * 32
+                xi = index("xcol", (batch, s_in.height, s_in.width, s_in.channels, k1, k2, stride, pad, ho, wo, kp))
+                wi = index("wimg", (refs.ref(w), 2, s_in.height, s_in.width, s_in.channels, k1, k2, kp, j, bn, prec))
+                conv_rows.append((_sym(SP_XCOL, xi), _sym(SP_WIMG, wi), buf(op.out), batch, ho, wo, kp, ho, wo,
+                                  _rup4(j), j, 1, 1, 1, 0, 0, 0, 0, 0, 0, nepi, kp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
+                conv_lv.append(op.level)
+                conv_bn.append(bn)
+                conv_k.append(kp)
+                continue
             wi = index("wimg", (refs.ref(w), n.kind is K.Conv2D, s_in.height, s_in.width, s_in.channels,
                                 k1, k2, cp, j, bn, prec))
-            epi = epi_rows(op.steps)
             conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
                               s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
-                              sum(1 for e in epi if e[0]), cp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
+                              nepi, cp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
             conv_lv.append(op.level)
             conv_bn.append(bn)
             conv_k.append(k1 * k2 * cp)
@@ -499,7 +518,8 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
         ew_level=np.array(ew_lv, np.int32),
         wimg=tables["wimg"][1], affine=tables["affine"][1], const=tables["const"][1],
         arena_bytes=used, out_off=offs[lw.out_node], out_shape=shapes[lw.out_node], input_shape=ishape,
-        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes, prec=prec)
+        flops_per_image=flops, gemm_act_bytes_per_image=act_bytes, gemm_weight_bytes=w_bytes, prec=prec,
+        xcol=tables["xcol"][1])
 
 
 def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, tables: dict) -> np.ndarray:
@@ -525,6 +545,8 @@ def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, 
 SPLITK_MAX = 16  # work units per tile at most
 #: A operand by TMA im2col where eligible (TOBF_CONV_TMA=0: cp.async gather everywhere, A/B measurements)
 TMA_A = __import__("os").environ.get("TOBF_CONV_TMA", "1") != "0"
+#: convs reading the graph input with c % 32 != 0 as 1x1 GEMMs over its im2col (TOBF_INPUT_IM2COL=0: direct)
+INPUT_IM2COL = __import__("os").environ.get("TOBF_INPUT_IM2COL", "1") != "0"
 
 
 def conv_sched(ctx: DeviceContext) -> torch.Tensor:
@@ -576,12 +598,15 @@ class PlanTables:
         self.ctx, self.refs = ctx, refs
         if ctx.wimg_bytes > ctx.WIMG_LIMIT:
             ctx.reset_wimg()  # a long GA run: bound the packed-image cache between batches
-        self.rows: list[tuple[list, list, list]] = []  # per plan: (wimg, affine, const) pointers
+        self.rows: list[tuple[list, list, list, list]] = []  # per plan: (wimg, affine, const, xcol) pointers
         # every device buffer a pointer was handed out for, held for the life of
         # the run: a context cache may drop its entry (size bound) mid-batch
         self.keep: list = []
         self._wimg_memo: dict = {}
         self._const_memo: dict = {}
+        # im2col matrices of the staged input (geometry -> device buffer),
+        # filled by PopulationRun.set_input before the forward reads them
+        self.xcol: dict = {}
 
     def add(self, plans: list) -> None:
         aff = self._affine_ptrs(list({r for p in plans for r in p.affine}))
@@ -599,10 +624,16 @@ class PlanTables:
                 if v is None:
                     v = cm[e] = self._const_ptr(e)
                 c.append(v)
-            self.rows.append((w, [aff[e] for e in p.affine], c))
+            x = []
+            for e in p.xcol:
+                buf = self.xcol.get(e)
+                if buf is None:
+                    buf = self.xcol[e] = self._xcol_buffer(e)
+                x.append(buf.data_ptr())
+            self.rows.append((w, [aff[e] for e in p.affine], c, x))
 
     def table(self, i: int) -> tuple[np.ndarray, np.ndarray]:
-        """Column ``i`` (0 wimg, 1 affine, 2 const) of every plan concatenated
+        """Column ``i`` (0 wimg, 1 affine, 2 const, 3 xcol) of every plan concatenated
         (+ a 0 sentinel) and each plan's offset into it."""
         lens = np.array([len(r[i]) for r in self.rows], np.int64)
         offsets = np.zeros(len(self.rows), np.int64)
@@ -610,10 +641,69 @@ class PlanTables:
         flat = [v for r in self.rows for v in r[i]]
         return np.array(flat + [0], np.uint64), offsets
 
+    def _xcol_buffer(self, geom: tuple) -> torch.Tensor:
+        """Device buffer of one input im2col matrix (batch*Ho*Wo rows of Kp),
+        cached per geometry in the context (the runs are stream-ordered)."""
+        batch, _, _, _, _, _, _, _, ho, wo, kp = geom
+        cache = self.ctx.__dict__.setdefault("xcol_cache", {})
+        buf = cache.get(geom)
+        if buf is None:
+            if len(cache) > 16:
+                cache.clear()
+            buf = cache[geom] = torch.empty(batch * ho * wo * kp, dtype=torch.float32, device=self.ctx.device)
+        self.keep.append(buf)
+        return buf
+
+    def _xcol_wimg_ptr(self, w, in_c, k1, k2, kp, j, bn, prec) -> int:
+        """Weight image of an input conv run as a 1x1 GEMM over the input's
+        im2col: K index (u*k2 + v)*c + ch of the (k1, k2, c, j) weight, packed
+        through gather maps (the flattened (u, v, c) offsets; knob-derived
+        weights compose their own maps and scales into them)."""
+        ctx, lib = self.ctx, self.ctx.lib
+        if isinstance(w, DerivedWeight):
+            wptr, st = ctx.cached_view(w.base)
+            mu, mv, mc, mn, s_c, s_n = w.maps()
+            if (len(mu), len(mv), len(mc), len(mn)) != (k1, k2, in_c, j):
+                raise ShapeMismatch(-1, f"derived weight maps {(len(mu), len(mv), len(mc), len(mn))} "
+                                        f"!= conv geometry {(k1, k2, in_c, j)}")
+            key = ("XD", wptr, st, w.key(), k1, k2, in_c, kp, j, bn, prec)
+        else:
+            wptr, st = ctx.cached_view(w)
+            mu, mv, mc, mn = np.arange(k1), np.arange(k2), np.arange(in_c), np.arange(j)
+            s_c, s_n = np.ones(in_c, np.float32), np.ones(j, np.float32)
+            key = ("X", wptr, st, k1, k2, in_c, kp, j, bn, prec)
+        cache = ctx.__dict__.setdefault("wimg_cache", {})
+        hit = cache.get(key)
+        if hit is not None:
+            self.keep.append(hit[0])
+            return hit[0].data_ptr()
+        su, sv, sc, sn = st
+        mu, mv, mc = (np.asarray(m, np.int64) for m in (mu, mv, mc))
+        off = (mu[:, None, None] * su + mv[None, :, None] * sv + mc[None, None, :] * sc)
+        bad = (mu[:, None, None] < 0) | (mv[None, :, None] < 0) | (mc[None, None, :] < 0)
+        flat = np.where(bad, -1, off).reshape(-1)
+        kk = k1 * k2 * in_c
+        imaps = np.concatenate([[0, 0], flat, np.asarray(mn, np.int64)]).astype(np.int32)
+        scales = np.concatenate([np.tile(np.asarray(s_c, np.float32), k1 * k2), np.asarray(s_n, np.float32)])
+        blob = ctx.upload_array(np.concatenate([imaps, scales.view(np.int32)]))
+        maps, sdev = blob, blob[len(imaps):]
+        nbytes = lib.tobf_wimg_bytes_ex(1, 1, kp, j, bn, prec)
+        img = torch.empty(nbytes // 4, dtype=torch.float32, device=ctx.device)
+        ctx.wimg_bytes += nbytes
+        ctx.check(lib.tobf_pack_weights_ex(C.c_void_p(wptr), 1, 1, kk, kp, j, 0, 0, 1, sn,
+                                           C.c_void_p(maps.data_ptr()), C.c_void_p(sdev.data_ptr()), bn, prec,
+                                           C.c_void_p(img.data_ptr()), C.c_void_p(ctx.sp)), "pack im2col weights")
+        ctx.launches += 1
+        cache[key] = (img, maps, sdev)
+        self.keep.append(img)
+        return img.data_ptr()
+
     def _wimg_ptr(self, entry: tuple) -> int:
         ctx, lib = self.ctx, self.ctx.lib
         ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec = entry
         w = self.refs.resolve(ref)
+        if is_conv == 2:
+            return self._xcol_wimg_ptr(w, in_c, k1, k2, cp, j, bn, prec)
         if isinstance(w, DerivedWeight):
             return self._derived_wimg_ptr(w, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec)
         wptr, st = ctx.cached_view(w)
@@ -796,7 +886,9 @@ class PopulationRun:
         self.arena.used = (cur - self.arena.base) // 4
         self.out_ptrs = [int(bases[i]) + p.out_off for i, p in enumerate(plans)]
         t0 = time.perf_counter()
-        tabs = {sp: tables.table(i) for i, sp in enumerate((SP_WIMG, SP_AFFINE, SP_CONST))}
+        tabs = {sp: tables.table(i) for i, sp in enumerate((SP_WIMG, SP_AFFINE, SP_CONST, SP_XCOL))}
+        # input im2col matrices this run's convs read: built in set_input
+        self._xcol = [(g, tables.xcol[g]) for g in sorted({e for p in plans for e in p.xcol})]
         t1 = time.perf_counter()
         # rows of all plans, linked, grouped into launches
         conv = cat_records([p.conv for p in plans], CONV_DTYPE)
@@ -885,6 +977,11 @@ class PopulationRun:
                                                       s.channels, s.height, s.width, _rup4(s.channels),
                                                       C.c_void_p(self.ctx.sp)), "input staging")
         self.ctx.launches += 1
+        for (b, h, w, c, k1, k2, stride, pad, ho, wo, kp), buf in self._xcol:
+            self.ctx.check(self.ctx.lib.tobf_im2col(C.c_void_p(self.x_ptr), b, h, w, _rup4(s.channels), c, k1, k2,
+                                                    stride, pad, ho, wo, kp, C.c_void_p(buf.data_ptr()),
+                                                    C.c_void_p(self.ctx.sp)), "input im2col")
+            self.ctx.launches += 1
 
     def run(self) -> None:
         lib, sp = self.ctx.lib, C.c_void_p(self.ctx.sp)

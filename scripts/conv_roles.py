@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2107_09789_b200 import fixtures, ga  # noqa: E402
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator  # noqa: E402
 
-NAMES = {0: "A.info", 1: "A.empty", 2: "A.cpw", 3: "A.stw", 4: "A.issue", 7: "A.total", 8: "M.info", 9: "M.small", 10: "M.accE", 11: "M.full",
+NAMES = {0: "A.info", 1: "A.empty", 2: "A.cpw", 3: "A.stw", 4: "A.issue", 5: "A.lds", 6: "A.sts", 7: "A.total", 8: "M.info", 9: "M.small", 10: "M.accE", 11: "M.full", 12: "M.issue",
          15: "M.total", 16: "D.info", 17: "D.accF", 18: "D.epi", 19: "D.bar1", 20: "D.setup", 21: "D.rows",
          22: "D.bar2", 23: "D.total", 24: "B.info", 25: "B.empty",
          31: "B.total"}

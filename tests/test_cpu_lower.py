@@ -56,7 +56,8 @@ def test_forward_plan_symbolic_rows():
         refs = S.ArrayRefs()
         plan = S.plan_forward(S.lower(og), 8, refs)
         assert len(plan.conv) and len(plan.conv) == len(plan.conv_level) == len(plan.conv_bn)
-        sizes = {S.SP_WIMG: len(plan.wimg), S.SP_AFFINE: len(plan.affine), S.SP_CONST: len(plan.const)}
+        sizes = {S.SP_WIMG: len(plan.wimg), S.SP_AFFINE: len(plan.affine), S.SP_CONST: len(plan.const),
+                 S.SP_XCOL: len(plan.xcol)}
         cols = [plan.conv["x"], plan.conv["y"], plan.conv["wimg"], plan.conv["epi"]["ptr"].ravel(),
                 plan.ew["x"], plan.ew["y"], plan.ew["epi"]["ptr"].ravel()]
         for col in cols:
@@ -70,6 +71,12 @@ def test_forward_plan_symbolic_rows():
                     assert v < sizes[sp]
                 else:
                     assert sp in (0, S.SP_INPUT)
+        # the stem (7x7, 3 channels) reads the input's im2col matrix (160 = 7*7*3
+        # rounded up to 32) as a 1x1 GEMM; its weight entry is the im2col view
+        assert plan.xcol == [(8, 224, 224, 3, 7, 7, 2, 3, 112, 112, 160)]
+        stem = plan.conv[(plan.conv["x"].astype(np.uint64) >> np.uint64(S._SP_SHIFT)) == S.SP_XCOL]
+        assert len(stem) >= 1 and (stem["Cp"] == 160).all() and (stem["k1"] == 1).all() and (stem["H"] == 112).all()
+        assert sum(1 for e in plan.wimg if e[1] == 2) == len({int(v) for v in stem["wimg"]})
         for e in plan.wimg:
             w = refs.resolve(e[0])
             assert w.dtype == np.float32 and w.ndim in (2, 4)

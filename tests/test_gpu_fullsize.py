@@ -27,6 +27,7 @@ import torch
 from oracle import costmodel_ref as CM
 from oracle import fitness_ref as FR
 from oracle import interp_ref as IR
+from paper_2107_09789_b200 import _native as N
 from paper_2107_09789_b200 import attacker, executor, fixtures, ga, knobs
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator
 from paper_2107_09789_b200.ir import label_sequence
@@ -101,11 +102,21 @@ def test_cfg2_headline_population_matches_oracle(ctx):
         pe.close()
     # identical records, except `worst` (a float32 max of |a-b|/(1+|b|)): the
     # micro-batch split changes which few-tile conv groups run split-K, i.e.
-    # the fp32 summation order of both graphs' outputs, within tolerance
-    for f in rec.dtype.names:
-        if f != "worst":
-            assert rec_e2e[f].tobytes() == rec[f].tobytes(), f
+    # the fp32 summation order of both graphs' outputs, within tolerance — and
+    # so the verdict (and the reward built on it) of a candidate whose two
+    # `worst` values straddle the 1e-5 equivalence tolerance itself
+    tol = executor.DEFAULT_TOL[N.PREC_TF32X3]
+    straddle = (rec["worst"] <= tol) != (rec_e2e["worst"] <= tol)
     assert np.max(np.abs(rec_e2e["worst"] - rec["worst"])) <= FP32_TOL
+    assert np.all(np.abs(rec_e2e["worst"][straddle] - rec["worst"][straddle]) <= 2 * tol)
+    for f in rec.dtype.names:
+        if f == "worst":
+            continue
+        if f in ("ok", "reward"):
+            assert rec_e2e[f][~straddle].tobytes() == rec[f][~straddle].tobytes(), f
+        else:
+            assert rec_e2e[f].tobytes() == rec[f].tobytes(), f
+    assert np.array_equal(rec_e2e["ok"][straddle] != 0, rec_e2e["worst"][straddle] <= tol)
 
     pool = oracle_pool.pool(g, trials=8, seed=0)
     try:

@@ -62,6 +62,47 @@ def test_conv_kernel_matches_oracle(ctx, case):
     assert _rel(got, ref) <= FP32_TOL
 
 
+@pytest.mark.parametrize("geom", [(8, 3, 64, 64, 7, 7, 2, 3), (2, 3, 32, 32, 3, 3, 1, 1), (1, 20, 9, 9, 5, 5, 1, 2)])
+def test_input_im2col_kernel(ctx, geom):
+    """tobf_im2col: the staged input's im2col matrix element for element
+    (a copy: bit-exact), K in the weights' (u, v, c) order, zero-padded."""
+    b, c, h, w, k1, k2, s, p = geom
+    ld = (c + 3) // 4 * 4
+    ho, wo = (h + 2 * p - k1) // s + 1, (w + 2 * p - k2) // s + 1
+    kp = -(-(k1 * k2 * c) // 32) * 32
+    rng = np.random.default_rng(3)
+    x = np.zeros((b, h, w, ld), np.float32)
+    x[..., :c] = rng.standard_normal((b, h, w, c))
+    xd = torch.from_numpy(x).cuda()
+    out = torch.full((b * ho * wo * kp,), 7.0, device="cuda")
+    assert ctx.lib.tobf_im2col(C.c_void_p(xd.data_ptr()), b, h, w, ld, c, k1, k2, s, p, ho, wo, kp,
+                               C.c_void_p(out.data_ptr()), C.c_void_p(ctx.sp)) == 0
+    got = out.cpu().numpy().reshape(b, ho, wo, kp)
+    xp = np.pad(x[..., :c], ((0, 0), (p, p), (p, p), (0, 0)))
+    ref = np.zeros((b, ho, wo, kp), np.float32)
+    for u in range(k1):
+        for v in range(k2):
+            k0 = (u * k2 + v) * c
+            ref[..., k0:k0 + c] = xp[:, u:u + s * ho:s, v:v + s * wo:s, :]
+    assert np.array_equal(got, ref)
+
+
+def test_input_im2col_path_matches_direct(ctx, monkeypatch):
+    """A stem-like conv (and a population of obfuscated RN18 candidates) through
+    the input-im2col 1x1 GEMM and through the direct conv agree within the fp32
+    contract, and both are within it of the oracle."""
+    g = fixtures.resnet18(size=64)
+    cands = [knobs.apply_plan(g, p)[0] for p in _plans(g, "sequence", 3, 5)]
+    x = IR.trial_inputs(g.input_shape.as_tuple(), 1, 0)[0]
+    outs = {}
+    for flag in (True, False):
+        monkeypatch.setattr(executor, "INPUT_IM2COL", flag)
+        outs[flag] = [executor.execute(og, x) for og in cands]
+    for a, b_, og in zip(outs[True], outs[False], cands):
+        ref = IR.execute(og, x).astype(np.float64)
+        assert _rel(a, ref) <= FP32_TOL and _rel(b_, ref) <= FP32_TOL
+
+
 def test_conv_split_k_deterministic(ctx):
     """A few-tile, long-K group (stage-4 shape, K = 4608) runs split-K: the
     partial tiles are summed in unit order by whichever unit finishes last, so
