@@ -317,12 +317,13 @@ __global__ void __launch_bounds__(TPC * 32, 1)
 // Register-blocked cluster LSTM (the cfg5 / generation kernel). Same cluster
 // layout as lstm_ctc_cluster_kernel — CTA rank r of a cluster of CS = H/32
 // CTAs owns hidden units [32r, 32r+32), gate rows resident in shared memory
-// as bf16 — but each thread computes its unit's 4 gates for RB = 4 traces
-// (warp w: traces 4w..4w+3, lane = unit), so every bf16 weight loaded and
-// widened is used RB times: per 4 K a thread issues 4 weight loads, 16
-// widenings, 4 broadcast h loads (h is stored k-major, trace-minor: one 16-B
-// load gives the 4 traces' values) and 64 FMAs — 1.4 instructions per FMA
-// instead of 2.3. NW warps per CTA, TPC = 4*NW traces per cluster.
+// as bf16 — but each thread computes its unit's 4 gates for RB = 4 or 8
+// traces (warp w: traces RB*w.., lane = unit), so every bf16 weight loaded
+// and widened is used RB times: per 4 K a thread issues 4 weight loads, 16
+// widenings, RB broadcast h loads (h is stored k-major, trace-minor: one 16-B
+// load gives 4 traces' values) and 16*RB FMAs (8*RB FFMA2) — RB = 4: 1.4
+// instructions per FMA instead of 2.3. NW warps per CTA, TPC = RB*NW traces
+// per cluster.
 //
 // ONE h buffer (not a double buffer), so 32 traces fit beside the 133 KB of
 // H=512 gate rows and a CTA keeps 8 warps: each step has two cluster
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(TPC * 32, 1)
 // order (bias, x[0..F), h[0..H)), the lane-strided head partials + xor
 // butterfly and every rounding are those of the original formulation and of
 // oracle/fitness_ref.c.
-constexpr int kRB = 4;  // traces per thread
+// traces per thread: the kernel's RB template parameter (4 or 8)
 
 // fp32 pairs for FFMA2 (fma.rn.f32x2): element 0 in the low word
 __device__ __forceinline__ uint64_t f2pack(float x, float y) {
@@ -366,14 +367,17 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
-template <int NW>
+template <int NW, int RB>
 __global__ void __launch_bounds__(NW * 32, 1)
     lstm_ctc_rb_kernel(const double* __restrict__ feats, const int32_t* __restrict__ offsets, int B, int F, int H,
                        int NC, const float* __restrict__ w_ihT, const float* __restrict__ w_hhT,
                        const float* __restrict__ bias, const float* __restrict__ w_out,
                        const float* __restrict__ b_out, int8_t* __restrict__ tokens, int T_max,
                        int32_t* __restrict__ ntok) {
-  constexpr int TPC = kRB * NW;
+  static_assert(RB % 4 == 0, "traces per thread: a multiple of 4");
+  constexpr int TPC = RB * NW;
+  constexpr int XS = (RB * 9 + 31) / 32;  // feature slots per lane (F <= 9)
+  constexpr int NS = RB;                   // head slots per warp (covers CS >= 1)
   constexpr int HS = TPC + 4;  // h row stride (floats)
   extern __shared__ __align__(16) uint8_t sm[];
   const int L = F + H;
@@ -423,36 +427,40 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __syncthreads();
   int tmax = 0;
   for (int i = 0; i < TPC; ++i) tmax = max(tmax, s_len[i]);
-  int len[kRB];
+  int len[RB];
 #pragma unroll
-  for (int r = 0; r < kRB; ++r) len[r] = s_len[kRB * w + r];
+  for (int r = 0; r < RB; ++r) len[r] = s_len[RB * w + r];
   cluster_sync_all();  // every CTA's buffers are initialised before remote writes start
 
   // x_t of this warp's traces, one step ahead: element i (< 4F) of the warp =
   // (trace 4w + i/F, feature i%F), held by lane i%32 (slot i/32)
-  int xk[2], xtr[2], xlen[2], xrow0[2];
-  bool xl[2];
-  float x_cur[2];
+  int xk[XS], xtr[XS], xlen[XS], xrow0[XS];
+  bool xl[XS];
+  float x_cur[XS];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < XS; ++j) {
     const int i = u + 32 * j;
-    xl[j] = i < kRB * F;
+    xl[j] = i < RB * F;
     const int xq = xl[j] ? i / F : 0;
     xk[j] = xl[j] ? i - xq * F : 0;
-    xtr[j] = kRB * w + xq;
+    xtr[j] = RB * w + xq;
     xlen[j] = xl[j] ? s_len[xtr[j]] : 0;
     xrow0[j] = s_row0[xtr[j]];
     x_cur[j] = (xl[j] && 0 < xlen[j]) ? (float)tobf_log1p_d(feats[(int64_t)xrow0[j] * 9 + xk[j]]) : 0.0f;
   }
   // head ownership: trace q = rank + CS*(w + NW*s) is decoded by warp w of CTA q % CS
-  int prev[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
-  float c[kRB] = {0.f, 0.f, 0.f, 0.f};
+  int prev[NS], cnt[NS];
+  float c[RB];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) prev[s] = cnt[s] = 0;
+#pragma unroll
+  for (int r = 0; r < RB; ++r) c[r] = 0.0f;
   const uint32_t hv_local = static_cast<uint32_t>(__cvta_generic_to_shared(hv));
-  const uint32_t slot = hv_local + 4u * (uint32_t)((F + unit) * HS + kRB * w);
-  const float* hrow = hv + kRB * w;
+  const uint32_t slot = hv_local + 4u * (uint32_t)((F + unit) * HS + RB * w);
+  const float* hrow = hv + RB * w;
   for (int t = 0; t < tmax; ++t) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < XS; ++j)
       if (xl[j]) hv[xk[j] * HS + xtr[j]] = x_cur[j];
     __syncwarp();
     // accumulators as fp32 PAIRS (traces 0-1, 2-3) updated with FFMA2
@@ -460,20 +468,24 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // per-accumulator sequence bias, x[0..F), h[0..H) as fmaf); the weight
     // is the scalar operand broadcast to both lanes, the h pair comes straight
     // from the 16-B k-major row. 8 FFMA2 per K instead of 16 FFMA.
-    uint64_t acc2[4][2];
+    uint64_t acc2[4][RB / 2];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const float bv = bsm[g * 32 + u];
-      acc2[g][0] = acc2[g][1] = f2pack(bv, bv);
+#pragma unroll
+      for (int r2 = 0; r2 < RB / 2; ++r2) acc2[g][r2] = f2pack(bv, bv);
     }
     const uint2* wrow = wq + u;
 #pragma unroll 2
     for (int kq = 0; kq < Lq; ++kq) {
       const uint2 w0 = wrow[(kq * 4 + 0) * kLstmUnits], w1 = wrow[(kq * 4 + 1) * kLstmUnits];
       const uint2 w2 = wrow[(kq * 4 + 2) * kLstmUnits], w3 = wrow[(kq * 4 + 3) * kLstmUnits];
-      ulonglong2 hq[4];
+      ulonglong2 hq[4][RB / 4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) hq[e] = *reinterpret_cast<const ulonglong2*>(hrow + (kq * 4 + e) * HS);
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int r4 = 0; r4 < RB / 4; ++r4)
+          hq[e][r4] = *reinterpret_cast<const ulonglong2*>(hrow + (kq * 4 + e) * HS + 4 * r4);
       const float wg[4][4] = {{bf16lo(w0.x), bf16hi(w0.x), bf16lo(w0.y), bf16hi(w0.y)},
                               {bf16lo(w1.x), bf16hi(w1.x), bf16lo(w1.y), bf16hi(w1.y)},
                               {bf16lo(w2.x), bf16hi(w2.x), bf16lo(w2.y), bf16hi(w2.y)},
@@ -483,38 +495,47 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const uint64_t wb = f2pack(wg[g][e], wg[g][e]);
-          acc2[g][0] = ffma2(wb, hq[e].x, acc2[g][0]);
-          acc2[g][1] = ffma2(wb, hq[e].y, acc2[g][1]);
+#pragma unroll
+          for (int r4 = 0; r4 < RB / 4; ++r4) {
+            acc2[g][2 * r4] = ffma2(wb, hq[e][r4].x, acc2[g][2 * r4]);
+            acc2[g][2 * r4 + 1] = ffma2(wb, hq[e][r4].y, acc2[g][2 * r4 + 1]);
+          }
         }
     }
     for (int e = 0; e < (L & 3); ++e) {
-      const ulonglong2 hx = *reinterpret_cast<const ulonglong2*>(hrow + (Lq * 4 + e) * HS);
       const uint16_t* wt = wtail + e * 4 * kLstmUnits + u;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const float wv = __uint_as_float((uint32_t)wt[g * 32] << 16);
-        const uint64_t wb = f2pack(wv, wv);
-        acc2[g][0] = ffma2(wb, hx.x, acc2[g][0]);
-        acc2[g][1] = ffma2(wb, hx.y, acc2[g][1]);
+      for (int r4 = 0; r4 < RB / 4; ++r4) {
+        const ulonglong2 hx = *reinterpret_cast<const ulonglong2*>(hrow + (Lq * 4 + e) * HS + 4 * r4);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const float wv = __uint_as_float((uint32_t)wt[g * 32] << 16);
+          const uint64_t wb = f2pack(wv, wv);
+          acc2[g][2 * r4] = ffma2(wb, hx.x, acc2[g][2 * r4]);
+          acc2[g][2 * r4 + 1] = ffma2(wb, hx.y, acc2[g][2 * r4 + 1]);
+        }
       }
     }
-    float acc[4][kRB];
+    float acc[4][RB];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      f2unpack(acc2[g][0], acc[g][0], acc[g][1]);
-      f2unpack(acc2[g][1], acc[g][2], acc[g][3]);
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int r2 = 0; r2 < RB / 2; ++r2) f2unpack(acc2[g][r2], acc[g][2 * r2], acc[g][2 * r2 + 1]);
+    float hval[RB];
+#pragma unroll
+    for (int r4 = 0; r4 < RB / 4; ++r4) {
+      const float4 hold = *reinterpret_cast<const float4*>(hv + (F + unit) * HS + RB * w + 4 * r4);
+      hval[4 * r4] = hold.x; hval[4 * r4 + 1] = hold.y; hval[4 * r4 + 2] = hold.z; hval[4 * r4 + 3] = hold.w;
     }
-    const float4 hold = *reinterpret_cast<const float4*>(hv + (F + unit) * HS + kRB * w);
     // barrier A: every CTA is done reading h_{t-1}; its latency hides behind
     // the activations and the next feature row
     cluster_arrive_relaxed();
-    double f_next[2];
+    double f_next[XS];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < XS; ++j)
       f_next[j] = (xl[j] && t + 1 < xlen[j]) ? feats[(int64_t)(xrow0[j] + t + 1) * 9 + xk[j]] : 0.0;
-    float hval[kRB] = {hold.x, hold.y, hold.z, hold.w};
 #pragma unroll
-    for (int r = 0; r < kRB; ++r) {
+    for (int r = 0; r < RB; ++r) {
       if (t < len[r]) {
         const float ig = tobf_sigmoid(acc[0][r]);
         const float fg = tobf_sigmoid(acc[1][r]);
@@ -525,14 +546,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) x_cur[j] = (xl[j] && t + 1 < xlen[j]) ? (float)tobf_log1p_d(f_next[j]) : 0.0f;
+    for (int j = 0; j < XS; ++j) x_cur[j] = (xl[j] && t + 1 < xlen[j]) ? (float)tobf_log1p_d(f_next[j]) : 0.0f;
     cluster_wait();
-    for (int rr = 0; rr < CS; ++rr) st_cluster_v4(map_shared(slot, rr), hval[0], hval[1], hval[2], hval[3]);
+    for (int rr = 0; rr < CS; ++rr)
+#pragma unroll
+      for (int r4 = 0; r4 < RB / 4; ++r4)
+        st_cluster_v4(map_shared(slot + 16u * r4, rr), hval[4 * r4], hval[4 * r4 + 1], hval[4 * r4 + 2],
+                      hval[4 * r4 + 3]);
     cluster_sync_all();  // barrier B: h_t has landed in every CTA
     // head + greedy CTC of the traces this warp owns (same formula and order as before)
     const float* hn = hv + F * HS;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int q = (int)rank + CS * (w + NW * s);
       if (q >= TPC || t >= s_len[q]) continue;
       int best = 0;
@@ -555,7 +580,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   }
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < NS; ++s) {
     const int q = (int)rank + CS * (w + NW * s);
     if (q < TPC && u == 0 && b0 + q < B) ntok[b0 + q] = cnt[s];
   }
@@ -789,15 +814,15 @@ static int launch_lstm_cluster(const double* feats, const int32_t* offsets, int3
   return tobf_cuda_check("tobf_lstm_ctc");
 }
 
-template <int NW>
+template <int NW, int RB>
 static int launch_lstm_rb(const double* feats, const int32_t* offsets, int32_t B, int32_t F, int32_t H, int32_t NC,
                           const float* w_ihT, const float* w_hhT, const float* b, const float* w_out,
                           const float* b_out, int8_t* tokens, int32_t T_max, int32_t* ntok, cudaStream_t st) {
-  constexpr int TPC = kRB * NW, HS = TPC + 4;
+  constexpr int TPC = RB * NW, HS = TPC + 4;
   const int L = F + H, Lq = L / 4, Lp = (L + 3) & ~3, CS = H / kLstmUnits;
   const size_t smem = (size_t)Lq * 4 * kLstmUnits * 8 + 4 * 4 * kLstmUnits * 2 +
                       sizeof(float) * ((size_t)Lp * HS + 4 * kLstmUnits + NC * H);
-  auto kern = lstm_ctc_rb_kernel<NW>;
+  auto kern = lstm_ctc_rb_kernel<NW, RB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return tobf_fail(TOBF_E_CUDA, "lstm rb attrs: %s", cudaGetErrorString(e));
@@ -827,20 +852,27 @@ extern "C" int tobf_lstm_ctc(const double* feats, const int32_t* offsets, int32_
       NC < 2 || NC > kMaxNC || H < 32 || H > 1024 || H % 32 || T_max < 1)
     return tobf_fail(TOBF_E_INVALID, "tobf_lstm_ctc: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  static const int variant = [] {
-    // A/B measurements only: "cluster16" = the round-1 kernel, "rb4" / "rb8" force the warps per CTA
+  const int variant = [] {
+    // A/B measurements only: "cluster16" = the round-1 kernel; "rb4" / "rb8"
+    // = 4 / 8 warps of 4 traces per thread; "r8w4" / "r8w8" = 4 / 8 warps of
+    // 8 traces per thread
     const char* v = getenv("TOBF_LSTM_VARIANT");
     if (!v) return 0;
-    return strcmp(v, "cluster16") == 0 ? 1 : strcmp(v, "rb4") == 0 ? 4 : strcmp(v, "rb8") == 0 ? 8 : 0;
+    return strcmp(v, "cluster16") == 0 ? 1 : strcmp(v, "rb4") == 0 ? 4 : strcmp(v, "rb8") == 0 ? 8
+         : strcmp(v, "r8w4") == 0 ? 84 : strcmp(v, "r8w8") == 0 ? 88 : 0;
   }();
   if (H % kLstmUnits == 0 && H / kLstmUnits <= 16 && variant != 1) {
+    if (variant == 84)
+      return launch_lstm_rb<4, 8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+    if (variant == 88 && H <= 256)
+      return launch_lstm_rb<8, 8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
     // 8 warps (32 traces) per cluster once the batch fills the GPU with them,
     // else 4 (16 traces): a generation-sized batch (32) keeps twice the clusters
     // (measured, cfg5 10k traces: H=512 169 vs 222 ms, H=256 34 vs 40 ms; H=128 9.7 vs 10.9 ms the other way)
     const bool wide = variant == 8 || (variant == 0 && H >= 256 && (int64_t)B * (H / kLstmUnits) >= 32 * 148);
     if (wide)
-      return launch_lstm_rb<8>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
-    return launch_lstm_rb<4>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+      return launch_lstm_rb<8, 4>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
+    return launch_lstm_rb<4, 4>(feats, offsets, B, F, H, NC, w_ihT, w_hhT, b, w_out, b_out, tokens, T_max, ntok, st);
   }
   if (H % kLstmUnits == 0 && H / kLstmUnits <= 16) {
     // 16 traces per cluster (the h double buffer of 16 traces plus the bf16

@@ -174,9 +174,10 @@ def test_cfg2_headline_population_matches_oracle(ctx):
 
 
 @pytest.mark.parametrize("hidden", [128, 256, 512])
-def test_cfg5_lstm_sweep_matches_oracle(ctx, hidden):
+def test_cfg5_lstm_sweep_matches_oracle(ctx, hidden, monkeypatch):
     """1003 traces (62 full 16-trace cluster rows + a ragged row of 11),
-    T ~ U[119,169], cost-model-scale features: tokens, ED and LER bit-exact."""
+    T ~ U[119,169], cost-model-scale features: tokens, ED and LER bit-exact;
+    every kernel shape (warps per CTA x traces per thread) decodes the same."""
     rng = np.random.default_rng(hidden + 5)
     nt = 1003
     lens = rng.integers(119, 170, nt)
@@ -201,6 +202,13 @@ def test_cfg5_lstm_sweep_matches_oracle(ctx, hidden):
         assert tk[i, :nk[i]].tolist() == want[i], i
         e = FR.levenshtein(want[i], truth)
         assert ed[i] == e and lr[i] == e / len(truth), i
+    for variant in ("rb4", "rb8", "r8w4", "r8w8"):
+        monkeypatch.setenv("TOBF_LSTM_VARIANT", variant)
+        tv, nv = attacker.decode(fd, od, nt, int(lens.max()), pred)
+        nv = nv.cpu().numpy()
+        assert np.array_equal(nv, nk), variant
+        tv = tv.cpu().numpy()
+        assert all(np.array_equal(tv[i, :nk[i]], tk[i, :nk[i]]) for i in range(nt)), variant
 
 
 def test_cfg4_vgg16_dimension_candidates_match_oracle(ctx):
