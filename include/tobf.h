@@ -179,7 +179,7 @@ typedef struct tobf_ew_desc {
   int32_t op, batch, H, W;   /* input geometry */
   int32_t C, ldx, Ho, Wo;    /* C = channels processed; ldx = input channel stride */
   int32_t ldy, a0, a1, nepi; /* ldy = output channel stride */
-  int64_t work_start;        /* prefix of work items (filled by tobf_ew_prepare) */
+  int64_t work_start;        /* prefix of work items, each range padded to a multiple of 32 (tobf_ew_prepare) */
   int32_t Cpo, pad_;         /* output channels to write (zero-fill C..Cpo) */
   tobf_epi_step epi[TOBF_MAX_EPI];
 } tobf_ew_desc;

@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     // one staged block of this thread's row (32 fp32 of K, = TMEM lane t)
     // -> its A stage in tensor memory (tf32 hi/lo split, or the bf16 pair)
-    auto to_tmem = [&](const float4 (&row)[8], int g) {
+    auto to_tmem = [&](const float4 (&row)[8], int g, auto&& release) {
       if constexpr (kBf16) {
         // 32 fp32 -> 16 hi + 16 lo bf16x2 columns (round to nearest even),
         // element k in the low half of column k/2; two staging blocks fill
@@ -639,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pl[2 * q] = pack_bf16x2(a.x - bf16lo_f(pk[2 * q]), a.y - bf16hi_f(pk[2 * q]));
           pl[2 * q + 1] = pack_bf16x2(a.z - bf16lo_f(pk[2 * q + 1]), a.w - bf16hi_f(pk[2 * q + 1]));
         }
+        release();  // every loaded value is consumed: the staging slot may be refilled
         const int half = g & 1;
         if (half == 0) {
           PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           f32x2_split(sub_f32x2(f32x2(a.z, a.w), f32x2(h[2], h[3])), l[2], l[3]);
         }
       }
+      release();  // every loaded value is consumed: the staging slot may be refilled
       PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
       tc_fence_after();
       const uint32_t ta = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + Cfg::kTmemACol + stage * 64;
@@ -724,11 +726,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
       }
-      if (TMA) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&stg_empty[g % SD]);  // every block: keeps warp 7's phases
-      }
-      to_tmem(row, g);
+      // TMA launches: release the slot to warp 7 (every block: keeps its
+      // phases) only once the split has CONSUMED the row: ld.shared results
+      // may still be in flight when a following arrive executes, and warp 7's
+      // next TMA load into the slot then overwrote rows not yet read — a rare
+      // wrong A block (one candidate's forward in ~10 population runs, found
+      // by scripts/race_probe.py; never on the cp.async path, whose refills
+      // follow the consuming split in program order)
+      to_tmem(row, g, [&]() {
+        if (TMA) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
+        }
+      });
     }
     cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF

@@ -45,23 +45,52 @@ __device__ __forceinline__ int find_desc(const tobf_ew_desc* __restrict__ descs,
   return lo;
 }
 
+// Work items of one descriptor (tobf_ew_prepare's count, before its padding
+// to a multiple of 32 so that no warp straddles two descriptors: SOFTMAX
+// reduces with full-warp shuffles).
+__host__ __device__ __forceinline__ int64_t ew_work(const tobf_ew_desc& d) {
+  const int64_t pix_in = (int64_t)d.batch * d.H * d.W;
+  switch (d.op) {
+    case TOBF_OP_MAXPOOL: return (int64_t)d.batch * d.Ho * d.Wo * (d.Cpo / 4);
+    case TOBF_OP_EPI: return pix_in * (d.Cpo / 4);
+    case TOBF_OP_COPYCH: return pix_in * (d.Cpo - d.a0);
+    case TOBF_OP_SOFTMAX: return pix_in * 32;
+    default: return 0;
+  }
+}
+
 // Work items: MAXPOOL / EPI -> one float4 channel group of one output pixel;
 // COPYCH -> one channel of one pixel (a0/a1 need not be 4-aligned);
 // SOFTMAX -> one warp per pixel (work counted in warps * 32 lanes).
+// Each block walks one contiguous chunk of the launch's work items, so a
+// thread finds its descriptor once (binary search) and then only advances it
+// as its items cross into the next descriptor; per-descriptor item indices
+// are 32-bit (tobf_ew_prepare checks the bound). Round 1 binary-searched the
+// descriptors for every item and divided in 64 bits: the headline step's
+// maxpool launches ran at a fraction of HBM bandwidth.
 __global__ void ew_grouped_kernel(const tobf_ew_desc* __restrict__ descs, int n, int64_t total) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total; w += stride) {
-    const int di = find_desc(descs, n, w);
+  const int64_t chunk = ((total + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+  const int64_t w0 = blockIdx.x * chunk, w1 = min(total, w0 + chunk);
+  int di = -1, dwork = 0;
+  int64_t next_start = 0;  // work_start of descriptor di + 1 (or total)
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+    if (w >= next_start) {
+      di = di < 0 ? find_desc(descs, n, w) : di + 1;
+      while (di + 1 < n && descs[di + 1].work_start <= w) ++di;
+      next_start = di + 1 < n ? descs[di + 1].work_start : total;
+      dwork = (int)ew_work(descs[di]);
+    }
     const tobf_ew_desc& d = descs[di];
-    const int64_t local = w - d.work_start;
+    const int local = (int)(w - d.work_start);
+    if (local >= dwork) continue;  // padding to the warp boundary (tobf_ew_prepare)
     switch (d.op) {
       case TOBF_OP_MAXPOOL: {
         const int groups = d.Cpo >> 2;
-        const int64_t pix = local / groups;
-        const int g = (int)(local - pix * groups);
-        const int64_t hw = (int64_t)d.Ho * d.Wo;
-        const int n_img = (int)(pix / hw);
-        const int rem = (int)(pix - (int64_t)n_img * hw);
+        const int pix = local / groups;
+        const int g = local - pix * groups;
+        const int hw = d.Ho * d.Wo;
+        const int n_img = pix / hw;
+        const int rem = pix - n_img * hw;
         const int yo = rem / d.Wo, xo = rem - (rem / d.Wo) * d.Wo;
         const int win = d.a0, st = d.a1;
         const float* base = d.x + ((int64_t)n_img * d.H * d.W) * d.ldx + g * 4;
@@ -73,47 +102,47 @@ __global__ void ew_grouped_kernel(const tobf_ew_desc* __restrict__ descs, int n,
             m.x = fmaxf(m.x, q.x); m.y = fmaxf(m.y, q.y); m.z = fmaxf(m.z, q.z); m.w = fmaxf(m.w, q.w);
           }
         }
-        *reinterpret_cast<float4*>(d.y + pix * d.ldy + g * 4) = m;
+        *reinterpret_cast<float4*>(d.y + (int64_t)pix * d.ldy + g * 4) = m;
         break;
       }
       case TOBF_OP_EPI: {
         const int groups = d.Cpo >> 2;
-        const int64_t pix = local / groups;
-        const int g = (int)(local - pix * groups);
-        const float4 q = __ldg(reinterpret_cast<const float4*>(d.x + pix * d.ldx + g * 4));
-        const int64_t hw = (int64_t)d.H * d.W;
+        const int pix = local / groups;
+        const int g = local - pix * groups;
+        const float4 q = __ldg(reinterpret_cast<const float4*>(d.x + (int64_t)pix * d.ldx + g * 4));
+        const int hw = d.H * d.W;
         int period = 1;
         for (int s = 0; s < d.nepi; ++s)
           if (d.epi[s].op == TOBF_EPI_ADD_CONST) period = d.epi[s].aux;
-        const int64_t n_img = pix / hw;
-        const int64_t cbase = ((n_img % period) * hw + (pix - n_img * hw)) * d.Cpo;
+        const int n_img = pix / hw;
+        const int64_t cbase = ((int64_t)(n_img % period) * hw + (pix - n_img * hw)) * d.Cpo;
         const int c = g * 4;
         float o[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) o[e] = (c + e < d.C) ? ew_epi(o[e], d, pix, c + e, cbase) : 0.0f;
-        *reinterpret_cast<float4*>(d.y + pix * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(d.y + (int64_t)pix * d.ldy + c) = make_float4(o[0], o[1], o[2], o[3]);
         break;
       }
       case TOBF_OP_COPYCH: {
         // channels [0, C) copied; channels [a0+C, Cpo) of the output zero-filled
         const int span = d.Cpo - d.a0;  // >= C
-        const int64_t pix = local / span;
-        const int c = (int)(local - pix * span);
-        const float v = c < d.C ? __ldg(d.x + pix * d.ldx + d.a1 + c) : 0.0f;
-        d.y[pix * d.ldy + d.a0 + c] = v;
+        const int pix = local / span;
+        const int c = local - pix * span;
+        const float v = c < d.C ? __ldg(d.x + (int64_t)pix * d.ldx + d.a1 + c) : 0.0f;
+        d.y[(int64_t)pix * d.ldy + d.a0 + c] = v;
         break;
       }
       case TOBF_OP_SOFTMAX: {
-        const int64_t pix = local >> 5;
-        const int lane = (int)(local & 31);
-        const float* xr = d.x + pix * d.ldx;
+        const int pix = local >> 5;
+        const int lane = local & 31;
+        const float* xr = d.x + (int64_t)pix * d.ldx;
         float mx = -INFINITY;
         for (int c = lane; c < d.C; c += 32) mx = fmaxf(mx, xr[c]);
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float sum = 0.0f;
         for (int c = lane; c < d.C; c += 32) sum += expf(xr[c] - mx);
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        float* yr = d.y + pix * d.ldy;
+        float* yr = d.y + (int64_t)pix * d.ldy;
         for (int c = lane; c < d.Cpo; c += 32) yr[c] = c < d.C ? expf(xr[c] - mx) / sum : 0.0f;
         break;
       }
@@ -200,31 +229,27 @@ extern "C" int tobf_ew_prepare(tobf_ew_desc* descs, int n, int64_t* total_work) 
   int64_t acc = 0;
   for (int i = 0; i < n; ++i) {
     tobf_ew_desc& d = descs[i];
-    const int64_t pix_in = (int64_t)d.batch * d.H * d.W;
-    int64_t work = 0;
     switch (d.op) {
       case TOBF_OP_MAXPOOL:
         if (d.Cpo % 4 || d.ldx % 4 || d.ldy % 4 || d.a0 < 1 || d.a1 < 1)
           return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad maxpool geometry", i);
-        work = (int64_t)d.batch * d.Ho * d.Wo * (d.Cpo / 4);
         break;
       case TOBF_OP_EPI:
         if (d.Cpo % 4 || d.ldx % 4 || d.ldy % 4 || d.nepi < 0 || d.nepi > TOBF_MAX_EPI)
           return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad epilogue op", i);
-        work = pix_in * (d.Cpo / 4);
         break;
       case TOBF_OP_COPYCH:
         if (d.Cpo < d.a0 + d.C) return tobf_fail(TOBF_E_INVALID, "ew desc %d: bad channel copy", i);
-        work = pix_in * (d.Cpo - d.a0);
         break;
       case TOBF_OP_SOFTMAX:
-        work = pix_in * 32;
         break;
       default:
         return tobf_fail(TOBF_E_INVALID, "ew desc %d: unknown op %d", i, d.op);
     }
+    const int64_t work = ew_work(d);
+    if (work >= ((int64_t)1 << 31) - 32) return tobf_fail(TOBF_E_INVALID, "ew desc %d: more than 2^31 work items", i);
     d.work_start = acc;
-    acc += work;
+    acc += (work + 31) & ~int64_t(31);  // warp-aligned descriptor ranges
   }
   *total_work = acc;
   return TOBF_OK;
@@ -276,30 +301,36 @@ extern "C" int tobf_nchw_to_nhwc(const float* x, float* y, int32_t B, int32_t C,
 // 7x7x4 blocks gathered with cp.async). One thread per 4 output columns.
 __global__ void im2col_kernel(const float* __restrict__ x, int B, int H, int W, int ldx, int c, int k1, int k2,
                               int stride, int pad, int Ho, int Wo, int Kp, float* __restrict__ out) {
-  const int64_t quads = (int64_t)B * Ho * Wo * (Kp / 4);
+  // per K element: its tap offsets and channel (-1: padding past K), decoded
+  // once per block instead of three integer divisions per element
+  extern __shared__ int4 ktab[];
   const int K = k1 * k2 * c;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < quads;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int kq = (int)(q % (Kp / 4));
-    const int64_t pix = q / (Kp / 4);
-    const int xo = (int)(pix % Wo);
-    const int64_t r = pix / Wo;
-    const int yo = (int)(r % Ho);
-    const int n = (int)(r / Ho);
+  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
+    const int uv = k / c, cc = k - uv * c, u = uv / k2;
+    ktab[k] = k < K ? make_int4(u, uv - u * k2, cc, 0) : make_int4(0, 0, -1, 0);
+  }
+  __syncthreads();
+  const unsigned kq4 = Kp / 4;
+  const unsigned quads = (unsigned)B * Ho * Wo * kq4;  // < 2^31 (checked by the caller): 32-bit divisions
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+    const unsigned pix = q / kq4;
+    const int kq = (int)(q - pix * kq4);
+    const unsigned r = pix / (unsigned)Wo;
+    const int xo = (int)(pix - r * Wo);
+    const unsigned n_ = r / (unsigned)Ho;
+    const int yo = (int)(r - n_ * Ho);
+    const int n = (int)n_;
+    const int y0 = yo * stride - pad, x0 = xo * stride - pad;
+    const float* xn = x + (int64_t)n * H * W * ldx;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int k = kq * 4 + e;
-      v[e] = 0.0f;
-      if (k < K) {
-        const int uv = k / c, cc = k - uv * c;
-        const int u = uv / k2, vv = uv - u * k2;
-        const int yi = yo * stride - pad + u, xi = xo * stride - pad + vv;
-        if ((unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W)
-          v[e] = __ldg(x + (((int64_t)n * H + yi) * W + xi) * ldx + cc);
-      }
+      const int4 t = ktab[kq * 4 + e];
+      const int yi = y0 + t.x, xi = x0 + t.y;
+      v[e] = (t.z >= 0 && (unsigned)yi < (unsigned)H && (unsigned)xi < (unsigned)W)
+                 ? __ldg(xn + ((int64_t)yi * W + xi) * ldx + t.z) : 0.0f;
     }
-    *reinterpret_cast<float4*>(out + pix * Kp + kq * 4) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(out + (int64_t)pix * Kp + kq * 4) = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -310,7 +341,9 @@ extern "C" int tobf_im2col(const float* x, int32_t B, int32_t H, int32_t W, int3
       Ho < 1 || Wo < 1 || Kp % 4 || Kp < k1 * k2 * c)
     return tobf_fail(TOBF_E_INVALID, "tobf_im2col: bad arguments");
   const int64_t quads = (int64_t)B * Ho * Wo * (Kp / 4);
-  im2col_kernel<<<grid_for(quads, 256), 256, 0, (cudaStream_t)stream>>>(x, B, H, W, ldx, c, k1, k2, stride, pad, Ho,
-                                                                          Wo, Kp, out);
+  if ((size_t)Kp * sizeof(int4) > 48 * 1024 || quads >= ((int64_t)1 << 31))
+    return tobf_fail(TOBF_E_INVALID, "tobf_im2col: Kp or the matrix too large");
+  im2col_kernel<<<grid_for(quads, 256), 256, (size_t)Kp * sizeof(int4), (cudaStream_t)stream>>>(
+      x, B, H, W, ldx, c, k1, k2, stride, pad, Ho, Wo, Kp, out);
   return tobf_cuda_check("tobf_im2col");
 }

@@ -463,13 +463,14 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
             w = n.weights if op.w is None else op.w
             epi = epi_rows(op.steps)
             nepi = sum(1 for e in epi if e[0])
-            if INPUT_IM2COL and op.src < 0 and n.kind is K.Conv2D and cp % 32 and k1 * k2 > 1:
+            kx = -(-(k1 * k2 * s_in.channels) // 32) * 32
+            if (INPUT_IM2COL and op.src < 0 and n.kind is K.Conv2D and cp % 32 and k1 * k2 > 1 and kx <= 3072
+                    and batch * shapes[op.node].height * shapes[op.node].width * kx < (1 << 33)):
                 # a conv reading the staged input with few channels: a 1x1 GEMM
                 # over the input's im2col matrix (shared by every candidate of
                 # the run, built once per staged input), K = k1*k2*c rounded up
                 # to 32 (RN18 stem: 160 instead of 7x7x4 = 196 -> 224), A by TMA
-                ho, wo = s_out.height, s_out.width
-                kp = -(-(k1 * k2 * s_in.channels) // 32) * 32
+                ho, wo, kp = s_out.height, s_out.width, kx
                 xi = index("xcol", (batch, s_in.height, s_in.width, s_in.channels, k1, k2, stride, pad, ho, wo, kp))
                 wi = index("wimg", (refs.ref(w), 2, s_in.height, s_in.width, s_in.channels, k1, k2, kp, j, bn, prec))
                 conv_rows.append((_sym(SP_XCOL, xi), _sym(SP_WIMG, wi), buf(op.out), batch, ho, wo, kp, ho, wo,
@@ -582,6 +583,127 @@ def _runs(keys: np.ndarray) -> list[tuple[int, int]]:
         return []
     b = (np.flatnonzero(np.any(keys[1:] != keys[:-1], axis=1)) + 1).tolist()
     return list(zip([0] + b, b + [n]))
+
+
+#: tail alignment (TOBF_TAIL_ALIGN, a fraction of each graph's depth; 0 = off):
+#: the ops of a graph at dependency levels >= f * its depth are shifted so that
+#: every graph of the population ends at the same level (RN18 headline step,
+#: same box: f = 0 2836, 0.3 2945, 0.5 2960, 0.7 2936, 0.9 2822 candidates/s)
+TAIL_ALIGN = float(__import__("os").environ.get("TOBF_TAIL_ALIGN", "0.5"))
+
+
+def _aligned_levels(plans: list) -> tuple[np.ndarray, np.ndarray]:
+    """Launch levels of every plan's conv and ew rows. The population's graphs
+    differ in depth (deepening adds layers), so with as-soon-as-possible levels
+    the last layers of the deep candidates run alone in the final levels —
+    small problems (7x7 spatial, the FC) that fill a fraction of the SMs. With
+    TAIL_ALIGN = f, a graph's ops at levels >= f * depth move down by its slack
+    (population depth - its depth): shifting a suffix of levels by one amount
+    keeps every producer before its consumers, and the tails of all graphs
+    share launches."""
+    conv = [p.conv_level for p in plans]
+    ew = [p.ew_level for p in plans]
+    if TAIL_ALIGN <= 0 or len(plans) < 2:
+        return np.concatenate(conv), np.concatenate(ew)
+    depth = [max(int(c.max(initial=0)), int(e.max(initial=0))) for c, e in zip(conv, ew)]
+    top = max(depth)
+    out_c, out_e = [], []
+    for c, e, dp in zip(conv, ew, depth):
+        t = int(np.ceil(TAIL_ALIGN * dp))
+        slack = top - dp
+        out_c.append(np.where(c >= t, c + slack, c))
+        out_e.append(np.where(e >= t, e + slack, e))
+    return np.concatenate(out_c), np.concatenate(out_e)
+
+
+class TensorMapStore:
+    """Device home of the conv A-operand tensor maps (128-B CUtensorMaps in
+    global memory), content-addressed: a map is written once, at an address
+    that never holds another map. The TMA unit caches tensor maps by address;
+    with a fresh map buffer per run, a later run could write different maps
+    at addresses an earlier run's maps had occupied, and nothing but timing
+    would keep a cached copy from being used. Here that cannot happen, and a
+    run uploads only the maps not seen before (they repeat across runs: the
+    activation arena and the input im2col buffers are reused). Blocks are
+    never freed. (The wrong forwards scripts/race_probe.py found were the
+    A-staging release race in conv_tc.cu, not this; the store makes the
+    map side race-free by construction.)"""
+
+    BLOCK = 4096  # maps per device block
+
+    def __init__(self, ctx: DeviceContext):
+        self.ctx = ctx
+        self.addr: dict[bytes, int] = {}
+        self.blocks: list[torch.Tensor] = []
+        self.free = 0
+
+    def place(self, maps: np.ndarray) -> np.ndarray:
+        """Device addresses of ``maps`` (rows of 128 B), uploading the new ones."""
+        out = np.zeros(len(maps), np.uint64)
+        new_rows, new_at = [], []
+        for i, m in enumerate(maps):
+            key = m.tobytes()
+            a = self.addr.get(key)
+            if a is None:
+                if self.free == 0:
+                    blk = torch.empty(128 * self.BLOCK + 128, dtype=torch.uint8, device=self.ctx.device)
+                    self.blocks.append(blk)
+                    self.base = (blk.data_ptr() + 127) & ~127
+                    self.free = self.BLOCK
+                a = self.base + 128 * (self.BLOCK - self.free)
+                self.free -= 1
+                self.addr[key] = a
+                new_rows.append(m)
+                new_at.append(a)
+            out[i] = a
+        # one staged copy per contiguous run of new slots
+        j = 0
+        while j < len(new_at):
+            k = j + 1
+            while k < len(new_at) and new_at[k] == new_at[k - 1] + 128:
+                k += 1
+            blk = next(b for b in self.blocks if b.data_ptr() <= new_at[j] < b.data_ptr() + b.numel())
+            off = new_at[j] - blk.data_ptr()
+            self.ctx._staged(np.concatenate(new_rows[j:k]), blk[off:off + 128 * (k - j)])
+            j = k
+        return out
+
+
+def _regroup(conv: np.ndarray, conv_tma: np.ndarray, level: np.ndarray, bn: np.ndarray, k: np.ndarray):
+    """Prepared conv rows (K/tiles/split-K filled) regrouped into one launch
+    per (level, BN), long K first: tile_start prefixes and the split-K
+    workspace / counter offsets (NULL-based bytes, rebased by the caller)
+    recomputed per group, each descriptor's ksplit/kper kept."""
+    order = np.lexsort((-k, -bn, level))
+    conv, conv_tma = conv[order], conv_tma[order]
+    key = np.stack([level[order], bn[order]], 1)
+    launches = []
+    ws_need = cnt_need = 0
+    for lo, hi in _runs(key):
+        g = conv[lo:hi]
+        tiles = g["mtiles"].astype(np.int64) * g["ntiles"]
+        units = tiles * g["ksplit"]
+        start = np.zeros(hi - lo, np.int64)
+        np.cumsum(units[:-1], out=start[1:])
+        g["tile_start"] = start
+        split = g["ksplit"] > 1
+        b = int(key[lo, 1])
+        wsf = np.where(split, units * kBM_ROWS * b, 0)
+        cnts = np.where(split, tiles, 0)
+        wo = np.zeros(hi - lo, np.int64)
+        co = np.zeros(hi - lo, np.int64)
+        np.cumsum(wsf[:-1], out=wo[1:])
+        np.cumsum(cnts[:-1], out=co[1:])
+        g["ws"] = np.where(split, 4 * wo, 0).astype(np.uint64)
+        g["cnt"] = np.where(split, 4 * co, 0).astype(np.uint64)
+        conv[lo:hi] = g
+        ws_need, cnt_need = max(ws_need, int(wsf.sum())), max(cnt_need, int(cnts.sum()))
+        tma_flag = N.CONV_TMA if conv_tma[lo:hi].any() else 0
+        launches.append((int(key[lo, 0]), 0, "conv", lo, hi - lo, int(units.sum()), b | tma_flag))
+    return conv, conv_tma, launches, ws_need, cnt_need
+
+
+kBM_ROWS = 128  # rows of a conv tile (conv_tc.cu kBM): a split-K partial tile is kBM_ROWS x BN floats
 
 
 class PlanTables:
@@ -902,22 +1024,26 @@ class PopulationRun:
                 arr[f] = _link(arr[f], rp, self.x_ptr, bases, tabs)
             arr["epi"]["ptr"] = _link(arr["epi"]["ptr"], rp, self.x_ptr, bases, tabs)
         conv_level = np.concatenate([p.conv_level for p in plans])
+        conv_launch_level, ew_level = _aligned_levels(plans)
         conv_bn = np.concatenate([p.conv_bn for p in plans])
         conv_k = np.concatenate([p.conv_k for p in plans])
-        ew_level = np.concatenate([p.ew_level for p in plans])
         # TMA im2col for the A operand of every conv: one 128-B tensor map per
         # problem, encoded on the host now that the input pointers are final
         conv_tma = np.zeros(len(conv), np.int64)
         if len(conv) and TMA_A:
-            self._tmaps = torch.empty(128 * len(conv) + 128, dtype=torch.uint8, device=ctx.device)
-            tbase = (self._tmaps.data_ptr() + 127) & ~127
             host_maps = np.zeros(128 * len(conv), np.uint8)
             ntma = C.c_int()
+            # encoded against a 0 base (d.tmap = 128 * i), then placed in the
+            # context's content-addressed store
             ctx.check(lib.tobf_conv_tmaps(C.c_void_p(conv.ctypes.data), len(conv), C.c_void_p(host_maps.ctypes.data),
-                                          tbase, C.byref(ntma)), "conv tensor maps")
-            if ntma.value:
-                ctx._staged(host_maps, self._tmaps[tbase - self._tmaps.data_ptr():][:len(host_maps)])
+                                          0, C.byref(ntma)), "conv tensor maps")
             conv_tma = (conv["tma"] > 0).astype(np.int64)
+            if ntma.value:
+                idx = np.nonzero(conv_tma)[0]
+                store = ctx.__dict__.get("tmap_store")
+                if store is None:
+                    store = ctx.tmap_store = TensorMapStore(ctx)
+                conv["tmap"][idx] = store.place(host_maps.reshape(-1, 128)[idx])
         # one launch per (level, BN), long K first (TMA-capable when any of its
         # problems is: the A mode is per tile); one ew launch per level
         order = np.lexsort((-conv_k, -conv_bn, conv_level))
@@ -942,6 +1068,13 @@ class PopulationRun:
                                                      C.byref(wsf), C.byref(cnts)), "conv prepare")
             ws_need, cnt_need = max(ws_need, wsf.value), max(cnt_need, cnts.value)
             launches.append((int(ckey[lo, 0]), 0, "conv", lo, hi - lo, tot.value, bn | tma_flag))
+        if len(conv) and not np.array_equal(conv_launch_level, conv_level):
+            # tail alignment: the split-K decisions above were taken on the
+            # as-soon-as-possible groups and stay with each problem, so every
+            # problem's arithmetic (hence every output bit) is that of the
+            # unaligned run; only the launch grouping changes
+            conv, conv_tma, launches, ws_need, cnt_need = _regroup(conv, conv_tma, conv_launch_level[order], conv_bn[order],
+                                                                  conv_k[order])
         if ws_need:
             ws, cnt = splitk_workspace(ctx, ws_need, cnt_need)
             split = conv["ksplit"] > 1
@@ -958,6 +1091,7 @@ class PopulationRun:
         pad = (-len(conv_bytes)) % 256
         host = conv_bytes + bytes(pad) + ew.tobytes()
         self.desc_dev = ctx.upload_bytes(host) if host else None
+        self.conv_rows, self.ew_rows = conv, ew  # linked host copies (diagnostics: scripts/race_probe.py)
         base = self.desc_dev.data_ptr() if host else 0
         ew_base = base + len(conv_bytes) + pad
         self.launches = [(k, (base + lo * CONV_DTYPE.itemsize) if k == "conv" else (ew_base + lo * EW_DTYPE.itemsize),

@@ -1,0 +1,5 @@
+# round 2 session 2: race probe with element-level diff of the racing problem
+set -x
+mkdir -p gpurun_out; rm -f gpurun_out/status.txt gpurun_out/race.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python scripts/race_probe.py 30 > gpurun_out/race.txt 2>&1; echo race=$? >> gpurun_out/status.txt

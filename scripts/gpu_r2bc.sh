@@ -1,0 +1,16 @@
+# round 2 session 2: staging-slot release after the split (race fix): determinism probe, records stress, perf A/B, GPU suite
+set -x
+mkdir -p gpurun_out; rm -f gpurun_out/status.txt gpurun_out/race_fix.txt gpurun_out/stress.txt gpurun_out/variants.txt
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/status.txt
+timeout 900 python scripts/race_probe.py 40 > gpurun_out/race_fix.txt 2>&1; echo race=$? >> gpurun_out/status.txt
+echo "== fix" >> gpurun_out/stress.txt; timeout 900 python scripts/stress_records.py 24 >> gpurun_out/stress.txt 2>&1
+for rep in 1 2; do
+  for v in fix racy; do
+    lib=paper_2107_09789_b200/libtobf.so; [ $v = racy ] && lib=scripts/_probe_libs/libtobf_opshead.so
+    for prec in fp32 bf16; do
+      TOBF_LIB=$lib timeout 300 python scripts/conv_levels.py --prec $prec > gpurun_out/levels_${v}_${prec}_$rep.txt 2>&1
+      echo "== $v $prec rep$rep $(grep 'conv launches' gpurun_out/levels_${v}_${prec}_$rep.txt)" >> gpurun_out/variants.txt
+    done
+  done
+done
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/status.txt

@@ -80,3 +80,37 @@ def test_forward_plan_symbolic_rows():
         for e in plan.wimg:
             w = refs.resolve(e[0])
             assert w.dtype == np.float32 and w.ndim in (2, 4)
+
+
+def test_tail_alignment_keeps_dependencies(monkeypatch):
+    """executor._aligned_levels: with TAIL_ALIGN = f, each graph's ops at
+    levels >= f * depth move down by the graph's slack, so every graph ends
+    at the population's last level and no op lands at or before a producer's
+    level (the whole suffix moves by one amount)."""
+    S = executor
+    plans, lws = [], []
+    for g, og in _plans("sequence", 6, seed=7):
+        lw = S.lower(og)
+        lws.append(lw)
+        plans.append(S.plan_forward(lw, 8, S.ArrayRefs()))
+    depth = [max(int(p.conv_level.max()), int(p.ew_level.max(initial=0))) for p in plans]
+    assert len(set(depth)) > 1  # deepened candidates: unequal depths
+    for f in (0.0, 0.3, 0.5, 1.0):
+        monkeypatch.setattr(S, "TAIL_ALIGN", f)
+        cl, el = S._aligned_levels(plans)
+        ci = ei = 0
+        for p, dp in zip(plans, depth):
+            c, e = cl[ci:ci + len(p.conv)], el[ei:ei + len(p.ew)]
+            ci += len(p.conv)
+            ei += len(p.ew)
+            if f <= 0:
+                assert np.array_equal(c, p.conv_level) and np.array_equal(e, p.ew_level)
+                continue
+            assert max(int(c.max()), int(e.max(initial=0))) == max(depth)
+            # order-preserving per graph: a strictly increasing map of the old levels
+            old = np.concatenate([p.conv_level, p.ew_level])
+            new = np.concatenate([c, e])
+            for a in np.unique(old):
+                assert len(np.unique(new[old == a])) == 1
+            pairs = sorted({(int(a), int(b)) for a, b in zip(old, new)})
+            assert all(b1 < b2 for (_, b1), (_, b2) in zip(pairs, pairs[1:]))

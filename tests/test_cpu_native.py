@@ -83,8 +83,10 @@ def test_ew_prepare(lib):
     arr[2].op, arr[2].batch, arr[2].H, arr[2].W = N.OP_SOFTMAX, 4, 1, 1
     tot = C.c_int64()
     assert lib.tobf_ew_prepare(arr, 3, C.byref(tot)) == 0
-    assert arr[1].work_start == 2 * 3 * 3 * 2
-    assert arr[2].work_start == arr[1].work_start + 4 * (36 - 17)
+    # each descriptor's range is padded to a multiple of 32 items (no warp
+    # straddles two descriptors: the softmax reduces with full-warp shuffles)
+    assert arr[1].work_start == 64  # 2*3*3*2 = 36 maxpool items
+    assert arr[2].work_start == arr[1].work_start + 96  # 4*(36-17) = 76 channel copies
     assert tot.value == arr[2].work_start + 4 * 32
     arr[0].op = 99
     assert lib.tobf_ew_prepare(arr, 3, C.byref(tot)) != 0

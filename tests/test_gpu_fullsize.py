@@ -285,3 +285,33 @@ def test_cfg4_vgg16_bf16_mode_matches_oracle(ctx):
         og, _ = knobs.apply_plan(g, p)
         got = executor.execute(og, x0, precision="bf16")
         assert _rel(got, IR.execute(og, x0).astype(np.float64)) <= BF16_TOL
+
+
+def test_headline_forward_bit_deterministic(ctx):
+    """The headline population's forward, repeated on one linked run and on
+    freshly linked runs, is bit-identical every time: tiles are claimed
+    dynamically, split-K partials summed in unit order, and the TMA-fed
+    A staging ring releases a slot only after its rows were consumed (an early
+    release let a TMA refill overwrite rows still being read: a wrong block in
+    roughly one population forward in ten, scripts/race_probe.py)."""
+    g = fixtures.resnet18()
+    plans = bench_plans(g, 32, seed=0)
+    pe = PopulationEvaluator(g, Evaluator(), budget=0.02, trials=8, seed=0, memo={})
+    x = pe.x_host.to(ctx.device)
+
+    def outputs(run):
+        return torch.stack([run.output_nchw(i).reshape(-1) for i in range(len(run.plans))]).cpu()
+
+    try:
+        ref = None
+        for relink in range(3):
+            run = pe.prepare(plans, memo={})["run"]
+            for _ in range(6):
+                run.set_input(x)
+                run.run()
+                out = outputs(run)
+                if ref is None:
+                    ref = out
+                assert torch.equal(out.view(torch.int32), ref.view(torch.int32)), relink
+    finally:
+        pe.close()
