@@ -40,6 +40,12 @@ namespace tobf {
 
 // A staging ring depth (K blocks the cp.async gather / TMA im2col loads run
 // ahead of the split into TMEM), per BN.
+// TMA A staging (fp32 mode): release a slot after the whole split (1)
+// instead of as soon as its rows have landed (0); bf16 mode always releases
+// after the split
+#ifndef TOBF_CONV_RELEASE_LATE
+#define TOBF_CONV_RELEASE_LATE 0
+#endif
 #ifndef TOBF_CONV_SD64
 #define TOBF_CONV_SD64 4
 #endif
@@ -500,6 +506,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // A warp only reads rows it copied itself, so __syncwarp orders the two.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProducer));
     constexpr int SD = Cfg::kStagingKB;
+    // measured (RN18 step, same box): fp32 9.42 ms released on landing vs
+    // 9.55 after the split; bf16 8.11 vs 7.74 — the other way round
+    constexpr bool kReleaseLate = kBf16 || TOBF_CONV_RELEASE_LATE;
     const int t = threadIdx.x;
     const int chunk = lane & 7;
     const int rsub = lane >> 3;
@@ -727,14 +736,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
       }
       // TMA launches: release the slot to warp 7 (every block: keeps its
-      // phases) only once the split has CONSUMED the row: ld.shared results
-      // may still be in flight when a following arrive executes, and warp 7's
-      // next TMA load into the slot then overwrote rows not yet read — a rare
-      // wrong A block (one candidate's forward in ~10 population runs, found
-      // by scripts/race_probe.py; never on the cp.async path, whose refills
-      // follow the consuming split in program order)
+      // phases) only once the row has LANDED: ld.shared results may still be
+      // in flight when a following arrive executes, and warp 7's next TMA
+      // load into the slot then overwrote rows not yet read — a rare wrong A
+      // block (one candidate's forward in ~10 population runs, found by
+      // scripts/race_probe.py; never on the cp.async path, whose refills
+      // follow the consuming split in program order). A branch on a value
+      // that depends on all eight loads makes the warp wait for them (cheaper
+      // than releasing after the whole split: TOBF_CONV_RELEASE_LATE=1).
+      if (TMA && !kReleaseLate) {
+        float landed = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) landed += row[q].x;
+        if (__float_as_uint(landed) == 0x7fbfe001u) atomicAdd(&g_tobf_fault, 0);  // never taken; keeps the dependency
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
+      }
       to_tmem(row, g, [&]() {
-        if (TMA) {
+        if (TMA && kReleaseLate) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
         }
