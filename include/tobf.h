@@ -76,7 +76,15 @@ typedef struct tobf_conv_desc {
    * 32 channels x 128 output pixels per load, 128B swizzle), tma = 32.
    * tma = 0: the A operand is gathered with cp.async. */
   const void* tmap;
-  int32_t tma, pad_;
+  int32_t tma;
+  /* Paired problem (executor stem pairing): two 64-channel problems reading
+   * the same A (the input's im2col matrix) with the same weights, run as ONE
+   * 128-channel problem: columns [0, 64) are written to `y`, [64, 128) to
+   * `y2` (same ldy), each half's folded BatchNorm (the chain's AFFINE step)
+   * read from its own array (`aff2` for the upper half). 0 = unpaired. */
+  int32_t pair;
+  float* y2;
+  const float* aff2;
 } tobf_conv_desc;
 
 /* Conv arithmetic (the `prec` argument of the *_ex entry points):

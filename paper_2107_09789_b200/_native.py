@@ -45,7 +45,7 @@ class ConvDesc(C.Structure):
         ("tile_start", C.c_int32), ("nepi", C.c_int32), ("ldx", C.c_int32), ("ldy", C.c_int32),
         ("epi", EpiStep * TOBF_MAX_EPI),
         ("ws", C.c_void_p), ("cnt", C.c_void_p), ("ksplit", C.c_int32), ("kper", C.c_int32),
-        ("tmap", C.c_void_p), ("tma", C.c_int32), ("pad_", C.c_int32),
+        ("tmap", C.c_void_p), ("tma", C.c_int32), ("pair", C.c_int32), ("y2", C.c_void_p), ("aff2", C.c_void_p),
     ]
 
 
@@ -83,7 +83,7 @@ class DeviceProfileC(C.Structure):
     ]
 
 
-assert C.sizeof(ConvDesc) == 240, C.sizeof(ConvDesc)
+assert C.sizeof(ConvDesc) == 256, C.sizeof(ConvDesc)  # <= one 256-B tile-info ring slot (conv_tc.cu)
 assert C.sizeof(EwDesc) == 176, C.sizeof(EwDesc)
 assert C.sizeof(KernDesc) == 136, C.sizeof(KernDesc)
 

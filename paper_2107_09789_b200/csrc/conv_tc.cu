@@ -88,6 +88,7 @@ struct ConvCfg {
   static constexpr int kEpiOff = kStagingOff + kStagingKB * kABytes;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
   static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
+  static_assert(sizeof(tobf_conv_desc) <= 256, "a descriptor fills at most one 256-B ring slot (32 lanes x 8 B)");
   static constexpr int kBarOff = kEpiOff + kEpiBytes + kInfoBytes;
   static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (kSchedTab ints)
   static constexpr int kSmem = kTabOff + 4 * TOBF_CONV_TAB + 1024 /*align*/;
@@ -1094,6 +1095,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ea.j = d.j;
       ea.y = d.y;
       ea.ldy = d.ldy;
+      // a paired problem (two 64-channel halves, tobf_conv_desc.pair): the
+      // upper half's lanes write y2 with their own folded BatchNorm
+      const bool upper = d.pair != 0 && ea.c >= 64;
+      if (d.pair != 0) {
+        ea.j = 64;
+        if (upper) {
+          ea.c -= 64;
+          ea.y = d.y2;
+        }
+        ea.cvalid = ea.c < 64;
+      }
       ea.sc = ea.sh = make_float4(0.f, 0.f, 0.f, 0.f);
       ea.res0 = ea.res1 = nullptr;
       ea.ldr = ea.ldr1 = 0;
@@ -1102,8 +1114,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int s = 0; s < TOBF_MAX_EPI; ++s) {
           if (eop[s] == TOBF_EPI_AFFINE && ea.cvalid) {
-            ea.sc = __ldg(reinterpret_cast<const float4*>(eptr[s] + ea.c));
-            ea.sh = __ldg(reinterpret_cast<const float4*>(eptr[s] + eaux[s] + ea.c));
+            const float* ap = upper ? d.aff2 : eptr[s];
+            ea.sc = __ldg(reinterpret_cast<const float4*>(ap + ea.c));
+            ea.sh = __ldg(reinterpret_cast<const float4*>(ap + eaux[s] + ea.c));
           }
           if (eop[s] == TOBF_EPI_ADD_TENSOR) {
             if (ti == 0) { ea.res0 = eptr[s]; ea.ldr = eaux[s]; } else { ea.res1 = eptr[s]; ea.ldr1 = eaux[s]; }

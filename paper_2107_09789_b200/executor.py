@@ -474,7 +474,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
                 xi = index("xcol", (batch, s_in.height, s_in.width, s_in.channels, k1, k2, stride, pad, ho, wo, kp))
                 wi = index("wimg", (refs.ref(w), 2, s_in.height, s_in.width, s_in.channels, k1, k2, kp, j, bn, prec))
                 conv_rows.append((_sym(SP_XCOL, xi), _sym(SP_WIMG, wi), buf(op.out), batch, ho, wo, kp, ho, wo,
-                                  _rup4(j), j, 1, 1, 1, 0, 0, 0, 0, 0, 0, nepi, kp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
+                                  _rup4(j), j, 1, 1, 1, 0, 0, 0, 0, 0, 0, nepi, kp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0, 0, 0))
                 conv_lv.append(op.level)
                 conv_bn.append(bn)
                 conv_k.append(kp)
@@ -483,7 +483,7 @@ def plan_forward(lw: Lowered, reps: int, refs: ArrayRefs, prec: int = N.PREC_TF3
                                 k1, k2, cp, j, bn, prec))
             conv_rows.append((buf(op.src), _sym(SP_WIMG, wi), buf(op.out), batch, s_in.height, s_in.width, cp,
                               s_out.height, s_out.width, _rup4(j), j, k1, k2, stride, pad, 0, 0, 0, 0, 0,
-                              nepi, cp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0))
+                              nepi, cp, _rup4(j), epi, 0, 0, 1, 0, 0, 0, 0, 0, 0))
             conv_lv.append(op.level)
             conv_bn.append(bn)
             conv_k.append(k1 * k2 * cp)
@@ -614,6 +614,69 @@ def _aligned_levels(plans: list) -> tuple[np.ndarray, np.ndarray]:
         out_c.append(np.where(c >= t, c + slack, c))
         out_e.append(np.where(e >= t, e + slack, e))
     return np.concatenate(out_c), np.concatenate(out_e)
+
+
+#: stem pairing (TOBF_PAIR_STEMS=0: off): see _pair_stems
+PAIR_STEMS = __import__("os").environ.get("TOBF_PAIR_STEMS", "1") != "0"
+
+
+def _stem_key(p: "ForwardPlan", r: np.ndarray, bn: int):
+    """Pairing key of a conv row reading the input's im2col matrix (None if it
+    may not pair): its matrix, its weight entry, its output row stride and its
+    epilogue chain (folded BatchNorm and/or ReLU only, the same ops)."""
+    space, val = int(np.uint64(r["x"]) >> np.uint64(_SP_SHIFT)), int(np.uint64(r["x"]) & np.uint64(_SP_LOW))
+    if space != SP_XCOL or bn != 64 or int(r["j"]) != 64 or int(r["Cpo"]) != 64:
+        return None
+    ops = []
+    for e in r["epi"][:int(r["nepi"])]:
+        op = int(e["op"])
+        if op not in (N.EPI_AFFINE, N.EPI_RELU) or (op == N.EPI_AFFINE and N.EPI_AFFINE in ops):
+            return None
+        ops.append(op)
+    wsp, wi = int(np.uint64(r["wimg"]) >> np.uint64(_SP_SHIFT)), int(np.uint64(r["wimg"]) & np.uint64(_SP_LOW))
+    if wsp != SP_WIMG:
+        return None
+    return (p.xcol[val], p.wimg[wi], int(r["ldy"]), tuple(ops), tuple(int(e["aux"]) for e in r["epi"][:int(r["nepi"])]))
+
+
+def _pair_stems(plans, conv, conv_plan, level, launch_level, conv_bn, tables) -> np.ndarray | None:
+    """Stems of different candidates read the same A (the staged input's
+    im2col matrix) and usually the same weights (most candidates leave the
+    stem alone): two such 64-channel problems of one launch run as ONE
+    128-channel problem (tobf_conv_desc.pair) over a weight image holding the
+    weights twice — the MMA at N = 128 (2048 vs 1470 MAC/clk/SM), half the A
+    staging and half the tiles. Each half keeps its own output buffer and
+    folded BatchNorm, so every output bit equals the unpaired run's (same K
+    order, same per-element sums). Returns the rows to keep (None: no pair).
+    The symbolic rows of the plans are left untouched; `conv` is linked."""
+    offs = np.zeros(len(plans) + 1, np.int64)
+    np.cumsum([len(p.conv) for p in plans], out=offs[1:])
+    groups: dict = {}
+    for pi, p in enumerate(plans):
+        for k, r in enumerate(p.conv):
+            i = offs[pi] + k
+            key = _stem_key(p, r, int(conv_bn[i]))
+            if key is not None:
+                groups.setdefault(key + (int(level[i]), int(launch_level[i])), []).append(i)
+    drop = []
+    for key, rows in groups.items():
+        for a, b in zip(rows[0::2], rows[1::2]):
+            img = tables.pair_image(key[1])
+            ra, rb = conv[a], conv[b]
+            aff = [k for k, e in enumerate(rb["epi"][:int(rb["nepi"])]) if int(e["op"]) == N.EPI_AFFINE]
+            conv["j"][a] = 128
+            conv["Cpo"][a] = 128
+            conv["wimg"][a] = np.uint64(img)
+            conv["pair"][a] = 1
+            conv["y2"][a] = rb["y"]
+            conv["aff2"][a] = rb["epi"][aff[0]]["ptr"] if aff else np.uint64(0)
+            conv_bn[a] = 128
+            drop.append(b)
+    if not drop:
+        return None
+    keep = np.ones(len(conv), bool)
+    keep[drop] = False
+    return keep
 
 
 class TensorMapStore:
@@ -776,7 +839,18 @@ class PlanTables:
         self.keep.append(buf)
         return buf
 
-    def _xcol_wimg_ptr(self, w, in_c, k1, k2, kp, j, bn, prec) -> int:
+    def pair_image(self, entry: tuple) -> int:
+        """Weight image of a paired stem (executor._pair_stems): the im2col
+        weight of ``entry`` twice along N (rows 0-63 and 64-127 of one
+        BN = 128 tile), cached like every image."""
+        ref, is_conv, in_h, in_w, in_c, k1, k2, cp, j, bn, prec = entry
+        hit = self._wimg_memo.get(("pair",) + entry)
+        if hit is None:
+            hit = self._wimg_memo[("pair",) + entry] = self._xcol_wimg_ptr(self.refs.resolve(ref), in_c, k1, k2, cp, j,
+                                                                         128, prec, twice=True)
+        return hit
+
+    def _xcol_wimg_ptr(self, w, in_c, k1, k2, kp, j, bn, prec, twice: bool = False) -> int:
         """Weight image of an input conv run as a 1x1 GEMM over the input's
         im2col: K index (u*k2 + v)*c + ch of the (k1, k2, c, j) weight, packed
         through gather maps (the flattened (u, v, c) offsets; knob-derived
@@ -788,12 +862,14 @@ class PlanTables:
             if (len(mu), len(mv), len(mc), len(mn)) != (k1, k2, in_c, j):
                 raise ShapeMismatch(-1, f"derived weight maps {(len(mu), len(mv), len(mc), len(mn))} "
                                         f"!= conv geometry {(k1, k2, in_c, j)}")
-            key = ("XD", wptr, st, w.key(), k1, k2, in_c, kp, j, bn, prec)
+            key = ("XD", wptr, st, w.key(), k1, k2, in_c, kp, j, bn, prec, twice)
         else:
             wptr, st = ctx.cached_view(w)
             mu, mv, mc, mn = np.arange(k1), np.arange(k2), np.arange(in_c), np.arange(j)
             s_c, s_n = np.ones(in_c, np.float32), np.ones(j, np.float32)
-            key = ("X", wptr, st, k1, k2, in_c, kp, j, bn, prec)
+            key = ("X", wptr, st, k1, k2, in_c, kp, j, bn, prec, twice)
+        if twice:  # the output channels twice: rows n and j + n of the image are channel n
+            mn, s_n, j = np.concatenate([mn, mn]), np.concatenate([s_n, s_n]), 2 * j
         cache = ctx.__dict__.setdefault("wimg_cache", {})
         hit = cache.get(key)
         if hit is not None:
@@ -1027,6 +1103,11 @@ class PopulationRun:
         conv_launch_level, ew_level = _aligned_levels(plans)
         conv_bn = np.concatenate([p.conv_bn for p in plans])
         conv_k = np.concatenate([p.conv_k for p in plans])
+        if PAIR_STEMS and len(conv):
+            keep = _pair_stems(plans, conv, conv_plan, conv_level, conv_launch_level, conv_bn, tables)
+            if keep is not None:
+                conv, conv_plan, conv_level, conv_launch_level, conv_bn, conv_k = (
+                    a[keep] for a in (conv, conv_plan, conv_level, conv_launch_level, conv_bn, conv_k))
         # TMA im2col for the A operand of every conv: one 128-B tensor map per
         # problem, encoded on the host now that the input pointers are final
         conv_tma = np.zeros(len(conv), np.int64)

@@ -569,3 +569,24 @@ def test_bf16_population_records(ctx):
         lers = [FR.ler(FR.lstm_ctc(feats, 9, pr.weights()), truth) for pr in ev.predictors]
         R, mean = FR.eq10(lers, T, ok, t_star, 0.02)
         assert rec["mean_ler"][i] == mean and rec["reward"][i] == R, i
+
+
+def test_paired_stems_match_unpaired(ctx, monkeypatch):
+    """executor._pair_stems: stems of different candidates reading the same
+    input im2col matrix with the same weights run as one 128-channel problem
+    (tobf_conv_desc.pair); every candidate's forward is bit-identical to the
+    unpaired run, and pairs were actually formed."""
+    g = fixtures.resnet18(size=64)
+    cands = [g] + [knobs.apply_plan(g, p)[0] for p in _plans(g, "sequence", 9, 11)]
+    x = torch.from_numpy(np.stack(IR.trial_inputs(g.input_shape.as_tuple(), 2, 0))[:, 0]).to(ctx.device)
+    outs = {}
+    for flag in (True, False):
+        monkeypatch.setattr(executor, "PAIR_STEMS", flag)
+        run = executor.PopulationRun(ctx, [executor.lower(c) for c in cands], reps=2)
+        if flag:
+            assert (run.conv_rows["pair"] == 1).sum() >= 4
+        run.set_input(x)
+        run.run()
+        outs[flag] = [run.output_nchw(i).cpu() for i in range(len(cands))]
+    for a, b in zip(outs[True], outs[False]):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
