@@ -46,6 +46,13 @@ namespace tobf {
 #ifndef TOBF_CONV_RELEASE_LATE
 #define TOBF_CONV_RELEASE_LATE 0
 #endif
+// drain: tcgen05.ld x16 loads in flight per wait::ld, per BN
+#ifndef TOBF_TMEM_GROUP64
+#define TOBF_TMEM_GROUP64 4
+#endif
+#ifndef TOBF_TMEM_GROUP128
+#define TOBF_TMEM_GROUP128 2
+#endif
 #ifndef TOBF_CONV_SD64
 #define TOBF_CONV_SD64 4
 #endif
@@ -183,6 +190,27 @@ __device__ __forceinline__ int find_problem(const tobf_conv_desc* __restrict__ d
   return lo;
 }
 
+
+// sum[i] += TMEM column i of this thread's lane (i < BN), G x16 loads in
+// flight per tcgen05.wait::ld (TOBF_TMEM_GROUP; 1 = a wait after every load)
+template <int BN>
+__device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float (&sum)[BN]) {
+  constexpr int kG0 = BN >= 128 ? TOBF_TMEM_GROUP128 : TOBF_TMEM_GROUP64;
+  constexpr int kG = kG0 < BN / 16 ? kG0 : BN / 16;
+#pragma unroll
+  for (int c0 = 0; c0 < BN / 16; c0 += kG) {
+    uint32_t r[kG][16];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) tmem_ld16_nw(taddr + (c0 + g) * 16, r[g]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+      reg_fence16(r[g]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sum[(c0 + g) * 16 + i] += __uint_as_float(r[g][i]);
+    }
+  }
+}
 
 // ---------------------------------------------------------------- epilogue
 struct EpiArgs {
@@ -981,13 +1009,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + Cfg::kTmemMainCol + buf * BN;
 #ifndef TOBF_CONV_DIAG_NOD  // diagnostic build: no drain / epilogue (wrong results)
-#pragma unroll
-        for (int cc = 0; cc < BN / 16; ++cc) {
-          float part[16];
-          tmem_ld16(taddr + cc * 16, part);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
-        }
+        tmem_add_cols<BN>(taddr, sum);
 #endif
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
@@ -996,13 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the tile's last acc_full commit covered every MMA of the tile, so the
         // correction accumulator of this slot is complete as well
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + slot * BN;
-#pragma unroll
-        for (int cc = 0; cc < BN / 16; ++cc) {
-          float part[16];
-          tmem_ld16(taddr + cc * 16, part);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) sum[cc * 16 + i] += part[i];
-        }
+        tmem_add_cols<BN>(taddr, sum);
         tc_fence_before();
         mbar_arrive(&small_empty[slot]);
       }
