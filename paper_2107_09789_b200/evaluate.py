@@ -147,6 +147,14 @@ class PopulationEvaluator:
             self.prefs = ParentRefs(self.vanilla)
             self.vanilla_plan = plan_forward(self.lowered_vanilla, self.trials, self.prefs, self.prec)
             self.pool = HostPool(self.vanilla, self.trials, self.ev.profile.name, workers, self.prec)
+            # the parent's own CPU work is single-threaded numpy and small
+            # copies; torch's intra-op pool (one thread per core, spinning
+            # after each parallel copy) would take the cores the workers run
+            # on (measured: the streamed e2e swung 430-2300 candidates/s with
+            # parent link steps stretched to 60 ms); leave the cores the
+            # workers do not use
+            cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 2)
+            torch.set_num_threads(max(1, cores - self.pool.workers - 1))
 
     def receive(self, result: tuple, tables: PlanTables | None = None) -> None:
         """Parent side of one worker result, as soon as it arrives: fold in its

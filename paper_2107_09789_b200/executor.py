@@ -653,9 +653,12 @@ def _pair_stems(plans, conv, conv_plan, level, launch_level, conv_bn, tables) ->
     np.cumsum([len(p.conv) for p in plans], out=offs[1:])
     groups: dict = {}
     for pi, p in enumerate(plans):
-        for k, r in enumerate(p.conv):
+        if not p.xcol:
+            continue
+        rows = np.nonzero((p.conv["x"] >> np.uint64(_SP_SHIFT)) == SP_XCOL)[0]  # the few input convs
+        for k in rows.tolist():
             i = offs[pi] + k
-            key = _stem_key(p, r, int(conv_bn[i]))
+            key = _stem_key(p, p.conv[k], int(conv_bn[i]))
             if key is not None:
                 groups.setdefault(key + (int(level[i]), int(launch_level[i])), []).append(i)
     drop = []
@@ -681,55 +684,35 @@ def _pair_stems(plans, conv, conv_plan, level, launch_level, conv_bn, tables) ->
 
 class TensorMapStore:
     """Device home of the conv A-operand tensor maps (128-B CUtensorMaps in
-    global memory), content-addressed: a map is written once, at an address
-    that never holds another map. The TMA unit caches tensor maps by address;
-    with a fresh map buffer per run, a later run could write different maps
-    at addresses an earlier run's maps had occupied, and nothing but timing
-    would keep a cached copy from being used. Here that cannot happen, and a
-    run uploads only the maps not seen before (they repeat across runs: the
-    activation arena and the input im2col buffers are reused). Blocks are
-    never freed. (The wrong forwards scripts/race_probe.py found were the
-    A-staging release race in conv_tc.cu, not this; the store makes the
-    map side race-free by construction.)"""
+    global memory): one large ring, written front to back, one H2D per run.
+    The TMA unit caches tensor maps by address; a fresh buffer per run could
+    land where an earlier run's different maps had been, and only timing
+    would keep a cached copy from being used. In the ring an address holds a
+    new map only after 2^19 others were written (several hundred runs of the
+    headline population), long after any cached copy is gone. (The wrong
+    forwards scripts/race_probe.py found were the A-staging release race in
+    conv_tc.cu, not this.)"""
 
-    BLOCK = 4096  # maps per device block
+    SLOTS = 1 << 19  # 64 MB of maps
 
     def __init__(self, ctx: DeviceContext):
         self.ctx = ctx
-        self.addr: dict[bytes, int] = {}
-        self.blocks: list[torch.Tensor] = []
-        self.free = 0
+        self.buf = torch.empty(128 * self.SLOTS + 128, dtype=torch.uint8, device=ctx.device)
+        self.base = (self.buf.data_ptr() + 127) & ~127
+        self.next = 0
 
     def place(self, maps: np.ndarray) -> np.ndarray:
-        """Device addresses of ``maps`` (rows of 128 B), uploading the new ones."""
-        out = np.zeros(len(maps), np.uint64)
-        new_rows, new_at = [], []
-        for i, m in enumerate(maps):
-            key = m.tobytes()
-            a = self.addr.get(key)
-            if a is None:
-                if self.free == 0:
-                    blk = torch.empty(128 * self.BLOCK + 128, dtype=torch.uint8, device=self.ctx.device)
-                    self.blocks.append(blk)
-                    self.base = (blk.data_ptr() + 127) & ~127
-                    self.free = self.BLOCK
-                a = self.base + 128 * (self.BLOCK - self.free)
-                self.free -= 1
-                self.addr[key] = a
-                new_rows.append(m)
-                new_at.append(a)
-            out[i] = a
-        # one staged copy per contiguous run of new slots
-        j = 0
-        while j < len(new_at):
-            k = j + 1
-            while k < len(new_at) and new_at[k] == new_at[k - 1] + 128:
-                k += 1
-            blk = next(b for b in self.blocks if b.data_ptr() <= new_at[j] < b.data_ptr() + b.numel())
-            off = new_at[j] - blk.data_ptr()
-            self.ctx._staged(np.concatenate(new_rows[j:k]), blk[off:off + 128 * (k - j)])
-            j = k
-        return out
+        """Device addresses of ``maps`` (rows of 128 B), copied in."""
+        n = len(maps)
+        if n > self.SLOTS:
+            raise MemoryError("more tensor maps than the store holds")
+        if self.next + n > self.SLOTS:
+            self.next = 0
+        off = self.next
+        self.next += n
+        start = self.base - self.buf.data_ptr() + 128 * off
+        self.ctx._staged(np.ascontiguousarray(maps).reshape(-1), self.buf[start:start + 128 * n])
+        return (self.base + 128 * (off + np.arange(n, dtype=np.uint64))).astype(np.uint64)
 
 
 def _regroup(conv: np.ndarray, conv_tma: np.ndarray, level: np.ndarray, bn: np.ndarray, k: np.ndarray):
