@@ -16,10 +16,26 @@ from paper_2107_09789_b200 import fixtures  # noqa: E402
 from paper_2107_09789_b200.evaluate import Evaluator, PopulationEvaluator  # noqa: E402
 from paper_2107_09789_b200.executor import CONV_DTYPE, EW_DTYPE, conv_sched  # noqa: E402
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-g = fixtures.resnet18()
-plans = population_plans(g, 32, 0)
-pe = PopulationEvaluator(g, Evaluator(), budget=0.02, trials=8, seed=0, memo={})
+import argparse  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("reps", type=int, nargs="?", default=30)
+ap.add_argument("--prec", default="fp32")
+ap.add_argument("--fixture", default="resnet18")
+ap.add_argument("--mode", default="sequence")
+ap.add_argument("--pop", type=int, default=32)
+a = ap.parse_args()
+reps = a.reps
+g = getattr(fixtures, a.fixture)()
+if a.mode == "sequence":
+    plans = population_plans(g, a.pop, 0)
+else:
+    from paper_2107_09789_b200 import ga  # noqa: E402
+    _rng = np.random.default_rng(0)
+    _space = ga.search_space(g, a.mode)
+    plans = [ga.decode_genome(g, a.mode, _space, x)
+             for x in ga.random_genomes(_rng, ga.domain_sizes(a.mode, _space), a.pop)]
+pe = PopulationEvaluator(g, Evaluator(), budget=0.02, trials=8, seed=0, memo={}, precision=a.prec)
 prep = pe.prepare(plans, memo={})
 run = prep["run"]
 ctx = pe.ctx
