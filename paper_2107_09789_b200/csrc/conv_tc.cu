@@ -53,6 +53,11 @@ namespace tobf {
 #ifndef TOBF_TMEM_GROUP128
 #define TOBF_TMEM_GROUP128 2
 #endif
+// A producer: load the next staging block's row right after the current
+// block's split (1) instead of at the top of the next iteration (0)
+#ifndef TOBF_CONV_APF
+#define TOBF_CONV_APF 1
+#endif
 #ifndef TOBF_CONV_SD64
 #define TOBF_CONV_SD64 4
 #endif
@@ -729,6 +734,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&full_bar[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     };
+    // A row of staging block h (this thread's 32 fp32 of K): waits until the
+    // block has landed (TMA: stg_full; cp.async: the warp's group h, with
+    // `pend` groups issued after it still allowed in flight), then ld.shared
+    auto load_row = [&](int h, float4 (&r)[8], auto pend) {
+      const uint32_t sbit = 1u << (h % SD);
+      const bool blk_tma = TMA && (tma_bits & sbit);
+      // TMA launches: EVERY block passes stg_full (warp 7 arrives for
+      // cp.async blocks too), so the A warps can never run SD blocks ahead of
+      // warp 7 and complete two phases of a slot's stg_empty before it waits
+      // on the first (a mixed cp.async / TMA launch hung or faulted that way)
+      if (TMA) PROF_WAIT(2, mbar_wait(&stg_full[h % SD], (h / SD) & 1, 0x11a));
+      if (!blk_tma) PROF_WAIT(2, cp_async_wait<decltype(pend)::value>(); __syncwarp());
+      const uint32_t src = stg_s + (h % SD) * kABytes + t * kRowBytes;
+      if (TMA && (zero_bits & sbit)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = lds128(src + ((q ^ (t & 7)) << 4));
+      }
+    };
+    float4 row[8];
+    bool have_row = false;  // row already holds block g (loaded during block g-1's split)
 #pragma unroll 1
     for (int g = 0;; ++g) {
       __syncwarp();  // every lane is done reading the slot about to be refilled
@@ -747,23 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_WAIT(4, if (ensure()) issue());
       cp_async_commit();  // one group per block (empty past the end): group g holds block g
       if (g >= issued) break;
-      const uint32_t sbit = 1u << (g % SD);
-      const bool blk_tma = TMA && (tma_bits & sbit);
-      // TMA launches: EVERY block passes stg_full (warp 7 arrives for
-      // cp.async blocks too), so the A warps can never run SD blocks ahead of
-      // warp 7 and complete two phases of a slot's stg_empty before it waits
-      // on the first (a mixed cp.async / TMA launch hung or faulted that way)
-      if (TMA) PROF_WAIT(2, mbar_wait(&stg_full[g % SD], (g / SD) & 1, 0x11a));
-      if (!blk_tma) PROF_WAIT(2, cp_async_wait<SD - 1>(); __syncwarp());
-      const uint32_t src = stg_s + (g % SD) * kABytes + t * kRowBytes;
-      float4 row[8];
-      if (TMA && (zero_bits & sbit)) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
-      }
+      if (!have_row) load_row(g, row, std::integral_constant<int, SD - 1>{});
       // TMA launches: release the slot to warp 7 (every block: keeps its
       // phases) only once the row has LANDED: ld.shared results may still be
       // in flight when a following arrive executes, and warp 7's next TMA
@@ -786,6 +798,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
         }
+        // row is consumed (split into registers): load block g+1's row now,
+        // so its shared-memory latency overlaps this block's TMEM stores
+        // (TOBF_CONV_APF=0: load at the top of the next iteration instead)
+        have_row = TOBF_CONV_APF && g + 1 < issued;
+        if (have_row) load_row(g + 1, row, std::integral_constant<int, SD - 2>{});
       });
     }
     cp_async_wait<0>();
