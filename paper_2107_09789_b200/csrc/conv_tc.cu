@@ -54,9 +54,20 @@ namespace tobf {
 #define TOBF_TMEM_GROUP128 2
 #endif
 // A producer: load the next staging block's row right after the current
-// block's split (1) instead of at the top of the next iteration (0)
-#ifndef TOBF_CONV_APF
-#define TOBF_CONV_APF 1
+// block's split when it has already landed (1) instead of at the top of the
+// next iteration (0), per precision. Measured (RN18 step conv, same box):
+// bf16 7.77 -> 7.43 ms; fp32 10.75 -> 10.92 ms (the extra live row spills in
+// the fp32 split), so off there
+// fp32 A split: hi = the raw fp32 (truncated by the tensor core), lo = a -
+// trunc(a) (1), or hi = rna(a), lo = a - hi (0)
+#ifndef TOBF_CONV_RAWHI
+#define TOBF_CONV_RAWHI 1
+#endif
+#ifndef TOBF_CONV_APF_F32
+#define TOBF_CONV_APF_F32 1
+#endif
+#ifndef TOBF_CONV_APF_BF16
+#define TOBF_CONV_APF_BF16 1
 #endif
 #ifndef TOBF_CONV_SD64
 #define TOBF_CONV_SD64 4
@@ -710,6 +721,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4 a = row[half * 4 + q];
           float* h = &hh[half][4 * q];
           float* l = &ll[half][4 * q];
+#if TOBF_CONV_RAWHI
+          // the tensor core reads a tf32 operand by truncation (low 13 bits
+          // ignored; scripts/tf32_trunc_probe.cu, both A from TMEM and B from
+          // SMEM), so the raw fp32 IS the truncated hi and lo = a - trunc(a)
+          // (exact): no rounding ops for hi
+          h[0] = a.x; h[1] = a.y; h[2] = a.z; h[3] = a.w;
+          const float t0 = __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
+          const float t1 = __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
+          const float t2 = __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
+          const float t3 = __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
+          f32x2_split(sub_f32x2(f32x2(a.x, a.y), f32x2(t0, t1)), l[0], l[1]);
+          f32x2_split(sub_f32x2(f32x2(a.z, a.w), f32x2(t2, t3)), l[2], l[3]);
+          continue;
+#endif
           h[0] = tf32_rna_finite(a.x);
           h[1] = tf32_rna_finite(a.y);
           h[2] = tf32_rna_finite(a.z);
@@ -755,6 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < 8; ++q) r[q] = lds128(src + ((q ^ (t & 7)) << 4));
       }
     };
+    constexpr bool kApf = TMA && (kBf16 ? TOBF_CONV_APF_BF16 : TOBF_CONV_APF_F32);
     float4 row[8];
     bool have_row = false;  // row already holds block g (loaded during block g-1's split)
 #pragma unroll 1
@@ -775,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_WAIT(4, if (ensure()) issue());
       cp_async_commit();  // one group per block (empty past the end): group g holds block g
       if (g >= issued) break;
-      if (!have_row) load_row(g, row, std::integral_constant<int, SD - 1>{});
+      if (!kApf || !have_row) load_row(g, row, std::integral_constant<int, SD - 1>{});
       // TMA launches: release the slot to warp 7 (every block: keeps its
       // phases) only once the row has LANDED: ld.shared results may still be
       // in flight when a following arrive executes, and warp 7's next TMA
@@ -793,17 +819,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
       }
+      // row is consumed (split into registers): if block g+1 has already
+      // landed by TMA (a non-blocking test: waiting for it here would put the
+      // next block's arrival on this block's critical path — measured 9.3 ->
+      // 12.0 ms), load its row now so the shared-memory latency overlaps this
+      // block's TMEM stores (bf16: right after the split; fp32: after the
+      // stores, where the split's 64 registers are free again)
+      auto prefetch = [&]() {
+        if constexpr (kApf) {
+          have_row = false;
+          if (g + 1 < issued) {
+            const int h = g + 1;
+            const uint32_t hbit = 1u << (h % SD);
+            if ((tma_bits & hbit) && !(zero_bits & hbit) &&
+                mbar_test_wait(smem_u32(&stg_full[h % SD]), (h / SD) & 1)) {
+              const uint32_t src = stg_s + (h % SD) * kABytes + t * kRowBytes;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) row[q] = lds128(src + ((q ^ (t & 7)) << 4));
+              have_row = true;
+            }
+          }
+          have_row = __all_sync(0xffffffffu, have_row);  // warp-uniform (lanes test independently)
+        }
+      };
       to_tmem(row, g, [&]() {
         if (TMA && kReleaseLate) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
         }
-        // row is consumed (split into registers): load block g+1's row now,
-        // so its shared-memory latency overlaps this block's TMEM stores
-        // (TOBF_CONV_APF=0: load at the top of the next iteration instead)
-        have_row = TOBF_CONV_APF && g + 1 < issued;
-        if (have_row) load_row(g + 1, row, std::integral_constant<int, SD - 2>{});
+        if constexpr (kBf16) prefetch();
       });
+      if constexpr (!kBf16) prefetch();
     }
     cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF
