@@ -174,6 +174,9 @@ int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_t total_til
  * warp), the others by the cp.async gather. Without the flag every problem
  * uses cp.async (tma ignored). */
 #define TOBF_CONV_TMA 0x100
+/* block_n | TOBF_CONV_TMA | TOBF_CONV_TMA_ALL: every problem of the launch
+ * has tma != 0 (the kernel variant without the cp.async gather). */
+#define TOBF_CONV_TMA_ALL 0x200
 
 /* Generic fused element-wise / pooling / copy ops (one op per descriptor). */
 #define TOBF_OP_MAXPOOL 1  /* y = maxpool(x, window=a0, stride=a1) */

@@ -19,7 +19,8 @@ TOBF_MAX_EPI = 6
 EPI_NONE, EPI_AFFINE, EPI_RELU, EPI_ADD_TENSOR, EPI_ADD_CONST = 0, 1, 2, 3, 4
 OP_MAXPOOL, OP_EPI, OP_COPYCH, OP_SOFTMAX = 1, 2, 3, 4
 PREC_TF32X3, PREC_BF16 = 0, 1
-CONV_TMA = 0x100  # block_n flag of an all-TMA conv launch (include/tobf.h TOBF_CONV_TMA)
+CONV_TMA = 0x100  # block_n flag of a TMA-capable conv launch (include/tobf.h TOBF_CONV_TMA)
+CONV_TMA_ALL = 0x200  # ... whose problems all take A by TMA (TOBF_CONV_TMA_ALL)
 PRECISIONS = {"fp32": PREC_TF32X3, "bf16": PREC_BF16}
 
 

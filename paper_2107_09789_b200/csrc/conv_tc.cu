@@ -63,6 +63,13 @@ namespace tobf {
 #ifndef TOBF_CONV_RAWHI
 #define TOBF_CONV_RAWHI 1
 #endif
+// tiles the scheduler may hold claimed ahead of the A producer in launches of
+// many short tiles (1 = claim only once the A warps took the previous tile).
+// 2 measured equal (RN18 step conv 8.84 / 7.26 ms fp32 / bf16 either way):
+// the A warps' info_full waits are not the claim gating
+#ifndef TOBF_CONV_LOOK
+#define TOBF_CONV_LOOK 1
+#endif
 #ifndef TOBF_CONV_APF_F32
 #define TOBF_CONV_APF_F32 1
 #endif
@@ -472,11 +479,16 @@ __device__ __forceinline__ void epi_rows_generic(const EpiArgs ea, const tobf_co
   }
 }
 
-template <int BN, int PREC, bool TMA>
+// AM: A-operand mode of the launch — 0 cp.async gather only, 1 mixed (per
+// problem: TMA im2col where tobf_conv_desc.tma != 0, else cp.async), 2 TMA
+// only (the gather code is compiled out: a smaller A loop, fewer registers)
+template <int BN, int PREC, int AM>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const tobf_conv_desc* __restrict__ descs, int nprob, int total_tiles, int* __restrict__ sched,
                    int claim) {
   using Cfg = ConvCfg<BN, PREC>;
+  constexpr bool TMA = AM != 0;
+  constexpr bool kAllTma = AM == 2;
   constexpr int STAGES = Cfg::kStages;
   constexpr bool kBf16 = Cfg::kBf16;
   constexpr int kChunk = kBf16 ? (1 << 30) : kChunkKB;  // K blocks per main-accumulator drain
@@ -492,8 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* small_empty = acc_empty + 4;     // [2] drain -> MMA (tile-slot correction accumulator)
   uint64_t* info_full = small_empty + 2;     // [kInfoSlots] scheduler -> roles
   uint64_t* info_empty = info_full + kInfoSlots;  // [kInfoSlots] roles -> scheduler
-  uint64_t* a_took = info_empty + kInfoSlots;     // A producer took tile k's descriptor (phase k)
-  uint64_t* stg_full = a_took + 1;                // [kStagingKB] TMA im2col -> A warps (TMA mode)
+  uint64_t* a_took = info_empty + kInfoSlots;     // [2] A producer took tile k's descriptor (a_took[k&1], phase k>>1)
+  uint64_t* stg_full = a_took + 2;                // [kStagingKB] TMA im2col -> A warps (TMA mode)
   uint64_t* stg_empty = stg_full + Cfg::kStagingKB;  // [kStagingKB] A warps -> TMA issuer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + Cfg::kStagingKB);
   volatile int* info_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kInfoSlots], -1 = no more tiles
@@ -526,7 +538,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&info_empty[s], kInfoConsumers + (TMA ? 1 : 0));  // + the TMA issuer warp
     }
     // the scheduler claims tile k+1 once the A warps' issue cursor took tile k
-    mbar_init(a_took, 4);
+    mbar_init(&a_took[0], 4);
+    mbar_init(&a_took[1], 4);
     for (int s = 0; s < Cfg::kStagingKB; ++s) {
       mbar_init(&stg_full[s], 1);
       mbar_init(&stg_empty[s], 4);
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ikblocks = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);  // staging blocks
         Cp = d.Cp; k1 = d.k1; k2 = d.k2; H = d.H; W = d.W; ldx = d.ldx;
         x = d.x;
-        itma = TMA && d.tma != 0;             // this tile's A blocks come by TMA (warp 7)
+        itma = kAllTma || (TMA && d.tma != 0);             // this tile's A blocks come by TMA (warp 7)
         isb0 = kb0 * Cfg::kStgPerKB;
         insb = d.K / kBK;
 #pragma unroll
@@ -622,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&info_empty[islot]);  // descriptor fully read into registers
-          mbar_arrive(a_took);              // the scheduler may claim the next tile
+          mbar_arrive(&a_took[iit & 1]);    // the scheduler may claim a further tile
         }
         ikb = 0;
         ++iit;
@@ -764,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // `pend` groups issued after it still allowed in flight), then ld.shared
     auto load_row = [&](int h, float4 (&r)[8], auto pend) {
       const uint32_t sbit = 1u << (h % SD);
-      const bool blk_tma = TMA && (tma_bits & sbit);
+      const bool blk_tma = kAllTma || (TMA && (tma_bits & sbit));
       // TMA launches: EVERY block passes stg_full (warp 7 arrives for
       // cp.async blocks too), so the A warps can never run SD blocks ahead of
       // warp 7 and complete two phases of a slot's stg_empty before it waits
@@ -811,6 +824,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // follow the consuming split in program order). A branch on a value
       // that depends on all eight loads makes the warp wait for them (cheaper
       // than releasing after the whole split: TOBF_CONV_RELEASE_LATE=1).
+#ifdef TOBF_CONV_PROF
+      const long long _l0 = clock64();
+#endif
       if (TMA && !kReleaseLate) {
         float landed = 0.0f;
 #pragma unroll
@@ -819,6 +835,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&stg_empty[g % SD]);
       }
+#ifdef TOBF_CONV_PROF
+      _pacc[5] += clock64() - _l0;  // A.lds: the row's loads landing (+ release)
+#endif
       // row is consumed (split into registers): if block g+1 has already
       // landed by TMA (a non-blocking test: waiting for it here would put the
       // next block's arrival on this block's critical path — measured 9.3 ->
@@ -831,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g + 1 < issued) {
             const int h = g + 1;
             const uint32_t hbit = 1u << (h % SD);
-            if ((tma_bits & hbit) && !(zero_bits & hbit) &&
+            if ((kAllTma || (tma_bits & hbit)) && !(zero_bits & hbit) &&
                 mbar_test_wait(smem_u32(&stg_full[h % SD]), (h / SD) & 1)) {
               const uint32_t src = stg_s + (h % SD) * kABytes + t * kRowBytes;
 #pragma unroll
@@ -849,7 +868,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if constexpr (kBf16) prefetch();
       });
+#ifdef TOBF_CONV_PROF
+      const long long _p6 = clock64();
+#endif
       if constexpr (!kBf16) prefetch();
+#ifdef TOBF_CONV_PROF
+      _pacc[6] += clock64() - _p6;  // A.sts: the fp32 prefetch test + issue
+#endif
     }
     cp_async_wait<0>();
 #ifdef TOBF_CONV_PROF
@@ -879,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kb0 = (lt - t2 * d.ksplit) * d.kper;
       const int nsb = Cfg::kStgPerKB * min(d.kper, d.kblocks - kb0);
       const int sb0 = kb0 * Cfg::kStgPerKB, K = d.K;
-      const bool tile_tma = d.tma != 0;
+      const bool tile_tma = kAllTma || d.tma != 0;
       const int m0 = (t2 / d.ntiles) * kBM;
       const int HWo = d.Ho * d.Wo;
       const int n0 = m0 / HWo;
@@ -1290,13 +1315,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tstart = [&](int i) { return i < kTab ? s_tstart[i] : __ldg(&descs[i].tile_start); };
     int prob = 0, prev_slot = -1;
     int bnext = 0, bend = 0;
+    const int look = claim > 1 ? TOBF_CONV_LOOK : 1;
     for (int it = 0;; ++it) {
       const int islot = it % kInfoSlots;
       mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
-      // claim lazily: only once the A producer has taken tile it-1, so a CTA
-      // holds at most one claimed-but-unstarted tile and the launch's tail
-      // stays balanced (the info ring would otherwise let it claim 3 ahead)
-      if (it > 0) mbar_wait(a_took, (it - 1) & 1, 0x118);
+      // claim lazily: only once the A producer has taken tile it-look, so a
+      // CTA holds at most `look` claimed-but-unstarted tiles and the launch's
+      // tail stays balanced (the info ring would otherwise let it claim 3 ahead)
+      // launches of many short tiles (claim > 1) may keep TOBF_CONV_LOOK
+      // tiles claimed ahead; two alternating barriers, so a wait never
+      // targets a phase two behind
+      if (it >= look) {
+        const int k = it - look;
+        mbar_wait(&a_took[k & 1], (k >> 1) & 1, 0x118);
+      }
       if (bnext == bend) {
         int first = 0;
         if (lane == 0) first = it == 0 ? (int)blockIdx.x * claim : (int)gridDim.x * claim + atomicAdd(&sched[0], claim);
@@ -1643,7 +1675,7 @@ extern "C" int tobf_conv_tmaps(tobf_conv_desc* descs, int n, void* tmap_host, ui
 
 // Per-device launch state of one kernel variant: SM count and the one-time
 // dynamic shared-memory opt-in (a context may drive several devices).
-template <int BN, int PREC, bool TMA>
+template <int BN, int PREC, int AM>
 static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int32_t* sched, cudaStream_t st) {
   constexpr int kMaxDev = 64;
   static int sms[kMaxDev] = {0};
@@ -1654,7 +1686,7 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
   if (sms[dev] == 0) {
     int count = 0;
     cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaFuncSetAttribute(conv_tc_kernel<BN, PREC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(conv_tc_kernel<BN, PREC, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ConvCfg<BN, PREC>::kSmem);
     if (e != cudaSuccess || count < 1) return tobf_fail(TOBF_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     sms[dev] = count;
@@ -1663,20 +1695,20 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
   // 1x1 convs); one at a time otherwise (few long tiles: LPT balance)
   const int claim = total_tiles >= 16 * (int64_t)sms[dev] ? 4 : 1;
   const int grid = (int)std::min<int64_t>((total_tiles + claim - 1) / claim, sms[dev]);
-  conv_tc_kernel<BN, PREC, TMA><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles,
+  conv_tc_kernel<BN, PREC, AM><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles,
                                                                                 sched, claim);
   return tobf_cuda_check("tobf_conv_grouped");
 }
 
-template <bool TMA>
+template <int AM>
 static int launch_variant(const tobf_conv_desc* d_descs, int n, int64_t total_tiles, int block_n, int prec,
                           int32_t* sched, cudaStream_t st) {
   if (prec == TOBF_PREC_TF32X3) {
-    if (block_n == 128) return launch_conv<128, 0, TMA>(d_descs, n, total_tiles, sched, st);
-    if (block_n == 64) return launch_conv<64, 0, TMA>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 128) return launch_conv<128, 0, AM>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 0, AM>(d_descs, n, total_tiles, sched, st);
   } else if (prec == TOBF_PREC_BF16) {
-    if (block_n == 128) return launch_conv<128, 1, TMA>(d_descs, n, total_tiles, sched, st);
-    if (block_n == 64) return launch_conv<64, 1, TMA>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 128) return launch_conv<128, 1, AM>(d_descs, n, total_tiles, sched, st);
+    if (block_n == 64) return launch_conv<64, 1, AM>(d_descs, n, total_tiles, sched, st);
   }
   return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: block_n must be 64 or 128, prec 0 or 1");
 }
@@ -1687,12 +1719,14 @@ extern "C" int tobf_conv_grouped_ex(const tobf_conv_desc* d_descs, int n, int64_
   if (!d_descs) return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: null descriptors");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // the A-operand mode of a launch is that of its problems (tobf_conv_tmaps);
-  // block_n | 0x100 marks an all-TMA launch
-  const bool tma = (block_n & 0x100) != 0;
+  // block_n | TOBF_CONV_TMA marks a TMA-capable launch, | TOBF_CONV_TMA_ALL
+  // one whose problems all take A by TMA
+  const int am = (block_n & TOBF_CONV_TMA_ALL) ? 2 : (block_n & TOBF_CONV_TMA) ? 1 : 0;
   block_n &= 0xFF;
   if (prec == TOBF_PREC_TF32X3 || prec == TOBF_PREC_BF16) {
-    return tma ? launch_variant<true>(d_descs, n, total_tiles, block_n, prec, sched, st)
-               : launch_variant<false>(d_descs, n, total_tiles, block_n, prec, sched, st);
+    if (am == 2) return launch_variant<2>(d_descs, n, total_tiles, block_n, prec, sched, st);
+    return am == 1 ? launch_variant<1>(d_descs, n, total_tiles, block_n, prec, sched, st)
+                   : launch_variant<0>(d_descs, n, total_tiles, block_n, prec, sched, st);
   } else {
     return tobf_fail(TOBF_E_INVALID, "tobf_conv_grouped: unknown precision %d", prec);
   }

@@ -546,6 +546,9 @@ def _link(col: np.ndarray, row_plan: np.ndarray, x_ptr: int, arena: np.ndarray, 
 SPLITK_MAX = 16  # work units per tile at most
 #: A operand by TMA im2col where eligible (TOBF_CONV_TMA=0: cp.async gather everywhere, A/B measurements)
 TMA_A = __import__("os").environ.get("TOBF_CONV_TMA", "1") != "0"
+#: launches whose problems all take A by TMA run the kernel variant without the
+#: cp.async gather (TOBF_CONV_TMA_ALL=0: the mixed-mode variant, A/B measurements)
+TMA_ALL = __import__("os").environ.get("TOBF_CONV_TMA_ALL", "1") != "0"
 #: convs reading the graph input with c % 32 != 0 as 1x1 GEMMs over its im2col (TOBF_INPUT_IM2COL=0: direct)
 INPUT_IM2COL = __import__("os").environ.get("TOBF_INPUT_IM2COL", "1") != "0"
 
@@ -744,7 +747,7 @@ def _regroup(conv: np.ndarray, conv_tma: np.ndarray, level: np.ndarray, bn: np.n
         g["cnt"] = np.where(split, 4 * co, 0).astype(np.uint64)
         conv[lo:hi] = g
         ws_need, cnt_need = max(ws_need, int(wsf.sum())), max(cnt_need, int(cnts.sum()))
-        tma_flag = N.CONV_TMA if conv_tma[lo:hi].any() else 0
+        tma_flag = (N.CONV_TMA | (N.CONV_TMA_ALL if TMA_ALL and conv_tma[lo:hi].all() else 0)) if conv_tma[lo:hi].any() else 0
         launches.append((int(key[lo, 0]), 0, "conv", lo, hi - lo, int(units.sum()), b | tma_flag))
     return conv, conv_tma, launches, ws_need, cnt_need
 
@@ -1124,7 +1127,7 @@ class PopulationRun:
         conv_ptr = conv.ctypes.data
         for lo, hi in _runs(ckey):
             bn = int(ckey[lo, 1])
-            tma_flag = N.CONV_TMA if conv_tma[lo:hi].any() else 0
+            tma_flag = (N.CONV_TMA | (N.CONV_TMA_ALL if TMA_ALL and conv_tma[lo:hi].all() else 0)) if conv_tma[lo:hi].any() else 0
             # split-K for groups too small to fill the SMs; workspace offsets
             # now, one workspace shared by every (stream-ordered) conv launch
             ctx.check(lib.tobf_conv_prepare_split_ex(C.c_void_p(conv_ptr + lo * CONV_DTYPE.itemsize), hi - lo, bn,
