@@ -92,6 +92,9 @@ namespace tobf {
 #define TOBF_CONV_ST64 4
 #endif
 
+#ifndef TOBF_CONV_INFO_SLOTS
+#define TOBF_CONV_INFO_SLOTS 4
+#endif
 constexpr int kBM = 128;
 constexpr int kBK = 32;           // fp32 elements per K block = one 128-B swizzle row
 constexpr int kRowBytes = 128;
@@ -117,7 +120,7 @@ struct ConvCfg {
   static constexpr int kStagingOff = kStages * kStageBytes;
   static constexpr int kEpiOff = kStagingOff + kStagingKB * kABytes;
   static constexpr int kEpiBytes = kBM * BN * 4;  // fp32 tile staged for the coalesced epilogue
-  static constexpr int kInfoBytes = 4 * 256;     // tile-info ring (descriptor copies)
+  static constexpr int kInfoBytes = TOBF_CONV_INFO_SLOTS * 256;  // tile-info ring (descriptor copies)
   static_assert(sizeof(tobf_conv_desc) <= 256, "a descriptor fills at most one 256-B ring slot (32 lanes x 8 B)");
   static constexpr int kBarOff = kEpiOff + kEpiBytes + kInfoBytes;
   static constexpr int kTabOff = kBarOff + 512;   // scheduler's copy of the problems' tile_start (kSchedTab ints)
@@ -194,9 +197,6 @@ __device__ unsigned long long g_conv_prof[32];
 // elsewhere. Must be >= 4: the A producer issues cp.async up to
 // kStagingKB-1 = 3 K blocks ahead of its split, which for 1-K-block tiles is
 // 3 tiles ahead, while a slot frees only when its tile is fully drained.
-#ifndef TOBF_CONV_INFO_SLOTS
-#define TOBF_CONV_INFO_SLOTS 4
-#endif
 constexpr int kInfoSlots = TOBF_CONV_INFO_SLOTS;
 // Dynamic tile counters: [0] next tile (beyond the first gridDim.x), [1] CTAs
 // exited; the last CTA to exit resets both, so consecutive launches (stream
@@ -1318,7 +1318,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int look = claim > 1 ? TOBF_CONV_LOOK : 1;
     for (int it = 0;; ++it) {
       const int islot = it % kInfoSlots;
+#ifdef TOBF_SCHED_NOBACKOFF
+      mbar_wait(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
+#else
       mbar_wait_backoff(&info_empty[islot], ((it / kInfoSlots) & 1) ^ 1, 0x114);
+#endif
       // claim lazily: only once the A producer has taken tile it-look, so a
       // CTA holds at most `look` claimed-but-unstarted tiles and the launch's
       // tail stays balanced (the info ring would otherwise let it claim 3 ahead)
