@@ -63,6 +63,14 @@ namespace tobf {
 #ifndef TOBF_CONV_RAWHI
 #define TOBF_CONV_RAWHI 1
 #endif
+// launches with >= TOBF_CONV_CLAIM_MIN tiles per SM claim TOBF_CONV_CLAIM
+// consecutive tiles per atomic
+#ifndef TOBF_CONV_CLAIM
+#define TOBF_CONV_CLAIM 4
+#endif
+#ifndef TOBF_CONV_CLAIM_MIN
+#define TOBF_CONV_CLAIM_MIN 16
+#endif
 // tiles the scheduler may hold claimed ahead of the A producer in launches of
 // many short tiles (1 = claim only once the A warps took the previous tile).
 // 2 measured equal (RN18 step conv 8.84 / 7.26 ms fp32 / bf16 either way):
@@ -1697,7 +1705,7 @@ static int launch_conv(const tobf_conv_desc* d_descs, int n, int64_t total_tiles
   }
   // claim 4 tiles at a time when there are many (short-tile levels: the stem,
   // 1x1 convs); one at a time otherwise (few long tiles: LPT balance)
-  const int claim = total_tiles >= 16 * (int64_t)sms[dev] ? 4 : 1;
+  const int claim = total_tiles >= TOBF_CONV_CLAIM_MIN * (int64_t)sms[dev] ? TOBF_CONV_CLAIM : 1;
   const int grid = (int)std::min<int64_t>((total_tiles + claim - 1) / claim, sms[dev]);
   conv_tc_kernel<BN, PREC, AM><<<grid, kThreads, ConvCfg<BN, PREC>::kSmem, st>>>(d_descs, n, (int)total_tiles,
                                                                                 sched, claim);
