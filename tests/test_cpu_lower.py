@@ -114,3 +114,32 @@ def test_tail_alignment_keeps_dependencies(monkeypatch):
                 assert len(np.unique(new[old == a])) == 1
             pairs = sorted({(int(a), int(b)) for a, b in zip(old, new)})
             assert all(b1 < b2 for (_, b1), (_, b2) in zip(pairs, pairs[1:]))
+
+
+def test_regroup_launch_tma_flags():
+    """executor._regroup: one launch per (level, BN); block_n carries
+    TOBF_CONV_TMA when any problem takes A by TMA im2col and
+    TOBF_CONV_TMA_ALL only when every problem does (the kernel variant
+    without the cp.async gather); flag values match include/tobf.h."""
+    import re
+    from pathlib import Path
+
+    from paper_2107_09789_b200 import _native as N
+    from paper_2107_09789_b200 import executor as E
+
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "tobf.h").read_text()
+    assert int(re.search(r"#define TOBF_CONV_TMA 0x([0-9a-fA-F]+)", hdr).group(1), 16) == N.CONV_TMA
+    assert int(re.search(r"#define TOBF_CONV_TMA_ALL 0x([0-9a-fA-F]+)", hdr).group(1), 16) == N.CONV_TMA_ALL
+    n = 7
+    conv = np.zeros(n, E.CONV_DTYPE)
+    conv["mtiles"], conv["ntiles"], conv["ksplit"] = 3, 1, 1
+    level = np.array([0, 0, 1, 1, 2, 2, 2])
+    bn = np.array([64, 64, 128, 128, 64, 64, 64])
+    k = np.array([5, 9, 2, 2, 3, 1, 4])
+    tma = np.array([1, 1, 1, 0, 0, 0, 0])
+    conv["tma"] = tma
+    _, ctma, launches, ws, cnt = E._regroup(conv, tma.astype(np.int64), level, bn, k)
+    flags = {(L[0], L[6] & 0xFF): L[6] & ~0xFF for L in launches}
+    assert flags == {(0, 64): N.CONV_TMA | N.CONV_TMA_ALL, (1, 128): N.CONV_TMA, (2, 64): 0}
+    assert [L[4] for L in launches] == [2, 2, 3] and ws == 0 and cnt == 0
+    assert [L[5] for L in launches] == [6, 6, 9]  # tiles per launch
