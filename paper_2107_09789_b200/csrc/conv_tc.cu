@@ -265,7 +265,13 @@ __device__ __forceinline__ float4 lds_tile(uint32_t epi_s, int row, int g, int b
 // row addresses are linear in the row index (no divisions).
 constexpr int kEpiUnroll = 8;
 
-template <int BN>
+#ifndef TOBF_EPI_FULL
+#define TOBF_EPI_FULL 1
+#endif
+// kFull: every row of the tile is inside M (all but a problem's last M tile),
+// so the row loop carries no per-row bounds branches (the stem / 1x1 levels
+// are epilogue-bound and their row loop was branch-issue bound)
+template <int BN, bool kFull>
 __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt, int ew, int lane) {
   constexpr int kLanesPerRow = BN / 4;
   constexpr int kRowsPerIter = 32 / kLanesPerRow;
@@ -283,7 +289,7 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
     for (int q = 0; q < kEpiUnroll; ++q) {
       const int row = r0 + q * kRowStep;
       mrow[q] = ea.m0 + row;
-      const bool ok = row < kBM && mrow[q] < ea.M;
+      const bool ok = kFull || (row < kBM && mrow[q] < ea.M);  // row < kBM holds by construction
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f), t0 = v, t1 = v;
       if (ok) {
         v = lds_tile(ea.epi_s, row, g, BN);
@@ -330,12 +336,9 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
     }
 #pragma unroll
     for (int q = 0; q < kEpiUnroll; ++q) {
-      if (mrow[q] < 0) continue;
-      if (!cfull) {
+      if (!kFull && mrow[q] < 0) continue;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (c + e >= ea.j) o[q][e] = 0.0f;
-      }
+      for (int e = 0; e < 4; ++e) o[q][e] = (cfull || c + e < ea.j) ? o[q][e] : 0.0f;
       stg128(ea.y + (int64_t)mrow[q] * ea.ldy + c, make_float4(o[q][0], o[q][1], o[q][2], o[q][3]));
     }
   }
@@ -1245,7 +1248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // RN18 sequence candidates; chains with constants / up to 4 operands /
       // 2 BNs take epi_rows_ops; anything else the per-element interpreter.
       if (naff <= 1 && nld <= 2 && nconst == 0) {
-        epi_rows<BN>(ea, prog, nepi, nld, ew, lane);
+        if (TOBF_EPI_FULL && m0 + kBM <= M) epi_rows<BN, true>(ea, prog, nepi, nld, ew, lane);
+        else epi_rows<BN, false>(ea, prog, nepi, nld, ew, lane);
       } else if (TOBF_EPI_OPS && naff <= 2 && nld + nconst <= 4) {
         EpiOps eo;
         uint32_t prog5 = 0;
