@@ -265,14 +265,25 @@ __device__ __forceinline__ float4 lds_tile(uint32_t epi_s, int row, int g, int b
 // row addresses are linear in the row index (no divisions).
 constexpr int kEpiUnroll = 8;
 
+// L1 prefetch of the epilogue's BatchNorm vectors at the drain's tile start:
+// measured slower (RN18 step conv 8.50 -> 8.72 ms fp32, 6.87 -> 7.07 bf16), off
+#ifndef TOBF_EPI_PREFETCH
+#define TOBF_EPI_PREFETCH 0
+#endif
+// full-tile epilogue rows specialised on the number of tensor operands
+#ifndef TOBF_EPI_NT
+#define TOBF_EPI_NT 1
+#endif
 #ifndef TOBF_EPI_FULL
 #define TOBF_EPI_FULL 1
 #endif
 // kFull: every row of the tile is inside M (all but a problem's last M tile),
 // so the row loop carries no per-row bounds branches (the stem / 1x1 levels
 // are epilogue-bound and their row loop was branch-issue bound)
-template <int BN, bool kFull>
-__device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt, int ew, int lane) {
+// NT >= 0: the number of tensor operands fixed at compile time (full tiles)
+template <int BN, bool kFull, int NT = -1>
+__device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt_rt, int ew, int lane) {
+  const int nt = NT >= 0 ? NT : nt_rt;
   constexpr int kLanesPerRow = BN / 4;
   constexpr int kRowsPerIter = 32 / kLanesPerRow;
   constexpr int kRowStep = 4 * kRowsPerIter;
@@ -1097,6 +1108,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int HWo = d.Ho * d.Wo;
       const int M = d.batch * HWo;
       const int kblocks = min(d.kper, d.kblocks - ks * d.kper);
+#if TOBF_EPI_PREFETCH
+      {
+        // the epilogue's folded-BatchNorm vectors into L1 now, so the setup's
+        // loads after the drain hit L1 instead of paying an L2 round trip
+        const int cpf = n_tile * BN + (lane % (BN / 4)) * 4;
+        if (cpf < d.Cpo) {
+#pragma unroll
+          for (int s = 0; s < TOBF_MAX_EPI; ++s) {
+            if (s < d.nepi && d.epi[s].op == TOBF_EPI_AFFINE) {
+              // a paired problem's upper half reads its own vectors (aff2)
+              const bool up = d.pair != 0 && cpf >= 64;
+              const float* ap = up ? d.aff2 : d.epi[s].ptr;
+              const int cc = up ? cpf - 64 : cpf;
+              prefetch_l1(ap + cc);
+              prefetch_l1(ap + d.epi[s].aux + cc);
+            }
+          }
+        }
+      }
+#endif
       const int slot = Cfg::kSplitCorr ? it % (Cfg::kSplitCorr ? Cfg::kCorrSlots : 1) : 0;
       float sum[BN];
 #pragma unroll
@@ -1248,8 +1279,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // RN18 sequence candidates; chains with constants / up to 4 operands /
       // 2 BNs take epi_rows_ops; anything else the per-element interpreter.
       if (naff <= 1 && nld <= 2 && nconst == 0) {
-        if (TOBF_EPI_FULL && m0 + kBM <= M) epi_rows<BN, true>(ea, prog, nepi, nld, ew, lane);
-        else epi_rows<BN, false>(ea, prog, nepi, nld, ew, lane);
+        if (TOBF_EPI_FULL && m0 + kBM <= M) {
+#if TOBF_EPI_NT
+          if (nld == 0) epi_rows<BN, true, 0>(ea, prog, nepi, nld, ew, lane);
+          else if (nld == 1) epi_rows<BN, true, 1>(ea, prog, nepi, nld, ew, lane);
+          else epi_rows<BN, true, 2>(ea, prog, nepi, nld, ew, lane);
+#else
+          epi_rows<BN, true>(ea, prog, nepi, nld, ew, lane);
+#endif
+        } else {
+          epi_rows<BN, false>(ea, prog, nepi, nld, ew, lane);
+        }
       } else if (TOBF_EPI_OPS && naff <= 2 && nld + nconst <= 4) {
         EpiOps eo;
         uint32_t prog5 = 0;
