@@ -374,7 +374,7 @@ struct EpiOps {
   int HWo, Cpo;
 };
 
-template <int BN, int U>
+template <int BN, int U, bool kFull>
 __device__ __forceinline__ void epi_rows_ops(const EpiArgs ea, const EpiOps& eo, uint32_t prog, int nsteps, int ew,
                                              int lane) {
   constexpr int kLanesPerRow = BN / 4;
@@ -393,7 +393,7 @@ __device__ __forceinline__ void epi_rows_ops(const EpiArgs ea, const EpiOps& eo,
     for (int q = 0; q < U; ++q) {
       const int row = r0 + q * kRowStep;
       mrow[q] = ea.m0 + row;
-      const bool ok = row < kBM && mrow[q] < ea.M;
+      const bool ok = kFull || (row < kBM && mrow[q] < ea.M);  // row < kBM holds by construction
       o[q] = ok ? lds_tile(ea.epi_s, row, g, BN) : make_float4(0.f, 0.f, 0.f, 0.f);
       int pix = 0, img = 0;
       if (ok) {
@@ -442,13 +442,11 @@ __device__ __forceinline__ void epi_rows_ops(const EpiArgs ea, const EpiOps& eo,
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      if (mrow[q] < 0) continue;
-      if (!cfull) {
-        if (c + 0 >= ea.j) o[q].x = 0.0f;
-        if (c + 1 >= ea.j) o[q].y = 0.0f;
-        if (c + 2 >= ea.j) o[q].z = 0.0f;
-        if (c + 3 >= ea.j) o[q].w = 0.0f;
-      }
+      if (!kFull && mrow[q] < 0) continue;
+      o[q].x = (cfull || c + 0 < ea.j) ? o[q].x : 0.0f;
+      o[q].y = (cfull || c + 1 < ea.j) ? o[q].y : 0.0f;
+      o[q].z = (cfull || c + 2 < ea.j) ? o[q].z : 0.0f;
+      o[q].w = (cfull || c + 3 < ea.j) ? o[q].w : 0.0f;
       stg128(ea.y + (int64_t)mrow[q] * ea.ldy + c, o[q]);
     }
   }
@@ -1327,7 +1325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           prog5 |= (uint32_t)((eop[s] & 7) | (slot << 3)) << (5 * s);
         }
-        epi_rows_ops<BN, 4>(ea, eo, prog5, nepi, ew, lane);
+        if (TOBF_EPI_FULL && m0 + kBM <= M) epi_rows_ops<BN, 4, true>(ea, eo, prog5, nepi, ew, lane);
+        else epi_rows_ops<BN, 4, false>(ea, eo, prog5, nepi, ew, lane);
       } else {
         epi_rows_generic<BN>(ea, d, ew, lane, HWo);
       }
