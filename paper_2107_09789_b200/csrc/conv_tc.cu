@@ -264,6 +264,9 @@ __device__ __forceinline__ float4 lds_tile(uint32_t epi_s, int row, int g, int b
 // kEpiUnroll steps are issued before any is consumed (loads in flight),
 // row addresses are linear in the row index (no divisions).
 constexpr int kEpiUnroll = 8;
+#ifndef TOBF_EPI_U0
+#define TOBF_EPI_U0 16
+#endif
 
 // L1 prefetch of the epilogue's BatchNorm vectors at the drain's tile start:
 // measured slower (RN18 step conv 8.50 -> 8.72 ms fp32, 6.87 -> 7.07 bf16), off
@@ -284,6 +287,8 @@ constexpr int kEpiUnroll = 8;
 template <int BN, bool kFull, int NT = -1>
 __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int nsteps, int nt_rt, int ew, int lane) {
   const int nt = NT >= 0 ? NT : nt_rt;
+  // full tiles without tensor operands keep twice the rows' stores in flight
+  constexpr int kU = (kFull && NT == 0) ? TOBF_EPI_U0 : kEpiUnroll;
   constexpr int kLanesPerRow = BN / 4;
   constexpr int kRowsPerIter = 32 / kLanesPerRow;
   constexpr int kRowStep = 4 * kRowsPerIter;
@@ -293,11 +298,11 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
   if (!ea.cvalid) return;
   const bool cfull = c + 3 < ea.j;
 #pragma unroll 1
-  for (int r0 = ew * kRowsPerIter + sub; r0 < kBM; r0 += kRowStep * kEpiUnroll) {
-    float o[kEpiUnroll][4], ta[kEpiUnroll][4], tb[kEpiUnroll][4];
-    int mrow[kEpiUnroll];
+  for (int r0 = ew * kRowsPerIter + sub; r0 < kBM; r0 += kRowStep * kU) {
+    float o[kU][4], ta[kU][4], tb[kU][4];
+    int mrow[kU];
 #pragma unroll
-    for (int q = 0; q < kEpiUnroll; ++q) {
+    for (int q = 0; q < kU; ++q) {
       const int row = r0 + q * kRowStep;
       mrow[q] = ea.m0 + row;
       const bool ok = kFull || (row < kBM && mrow[q] < ea.M);  // row < kBM holds by construction
@@ -322,23 +327,23 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
       const uint32_t op = (prog >> (4 * s)) & 7u;
       if (op == TOBF_EPI_AFFINE) {
 #pragma unroll
-        for (int q = 0; q < kEpiUnroll; ++q)
+        for (int q = 0; q < kU; ++q)
 #pragma unroll
           for (int e = 0; e < 4; ++e) o[q][e] = o[q][e] * av[e] + bv[e];
       } else if (op == TOBF_EPI_RELU) {
 #pragma unroll
-        for (int q = 0; q < kEpiUnroll; ++q)
+        for (int q = 0; q < kU; ++q)
 #pragma unroll
           for (int e = 0; e < 4; ++e) o[q][e] = fmaxf(o[q][e], 0.0f);
       } else if (op == TOBF_EPI_ADD_TENSOR) {
         if (ti == 0) {
 #pragma unroll
-          for (int q = 0; q < kEpiUnroll; ++q)
+          for (int q = 0; q < kU; ++q)
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[q][e] += ta[q][e];
         } else {
 #pragma unroll
-          for (int q = 0; q < kEpiUnroll; ++q)
+          for (int q = 0; q < kU; ++q)
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[q][e] += tb[q][e];
         }
@@ -346,7 +351,7 @@ __device__ __forceinline__ void epi_rows(const EpiArgs ea, uint32_t prog, int ns
       }
     }
 #pragma unroll
-    for (int q = 0; q < kEpiUnroll; ++q) {
+    for (int q = 0; q < kU; ++q) {
       if (!kFull && mrow[q] < 0) continue;
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[q][e] = (cfull || c + e < ea.j) ? o[q][e] : 0.0f;
