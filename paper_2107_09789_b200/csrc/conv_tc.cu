@@ -47,6 +47,10 @@ namespace tobf {
 #define TOBF_CONV_RELEASE_LATE 0
 #endif
 // drain / epilogue arithmetic two lanes per instruction (FADD2 / FFMA2)
+// fp32 A stage: hi and lo as one 32-column tcgen05.st each (1) or two x16 (0)
+#ifndef TOBF_A_ST32
+#define TOBF_A_ST32 1
+#endif
 #ifndef TOBF_DRAIN_FADD2
 #define TOBF_DRAIN_FADD2 1
 #endif
@@ -813,11 +817,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_WAIT(1, mbar_wait(&empty_bar[stage], phase ^ 1, 0x101));
       tc_fence_after();
       const uint32_t ta = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + Cfg::kTmemACol + stage * 64;
+#if TOBF_A_ST32
+      tmem_st32(ta, reinterpret_cast<const float(&)[32]>(hh));
+      tmem_st32(ta + 32, reinterpret_cast<const float(&)[32]>(ll));
+#else
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         tmem_st16(ta + half * 16, hh[half]);
         tmem_st16(ta + 32 + half * 16, ll[half]);
       }
+#endif
       PROF_WAIT(3, tmem_wait_st());
       tc_fence_before();
       mbar_arrive(&full_bar[stage]);
