@@ -702,9 +702,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (TMA) {
         // per slot: block mode (TMA or cp.async) and "wholly past K" (zeros)
         const uint32_t bit = 1u << (issued % SD);
-        tma_bits = itma ? (tma_bits | bit) : (tma_bits & ~bit);
-        zero_bits = (itma && isb0 + ikb >= insb) ? (zero_bits | bit) : (zero_bits & ~bit);
-        if (itma) {  // warp 7 loads this block
+        // (kAllTma: constant, so the all-TMA variant carries no gather code)
+        const bool blk_tma = kAllTma || itma;
+        tma_bits = blk_tma ? (tma_bits | bit) : (tma_bits & ~bit);
+        zero_bits = (blk_tma && isb0 + ikb >= insb) ? (zero_bits | bit) : (zero_bits & ~bit);
+        if (blk_tma) {  // warp 7 loads this block
           ++ikb;
           ++issued;
           return;
